@@ -1,0 +1,258 @@
+#!/usr/bin/env python
+"""bench.py -- amplitude-gate updates/s of the B200 gate engine.
+
+Workload (BASELINE.json configs[1] = "config 2"): random circuit on 24 qubits,
+complex128, depth 40 (Haar U2 on every qubit + brickwork CNOTs), initial
+|0..0>, 1420 gates.  One step = qsim_init_basis + qsim_run_circuit(all 1420
+gates) + qsim_expectations (<Q_i> of every qubit, read back to
+the host): every hot-path row of SURVEY.md §8(a) that this circuit uses.
+metric = N_O * 2^n / t  (N_O = user gates per step).
+
+N > 1 (torchrun, one rank per GPU, NCCL): weak scaling, n = 24 + log2(N)
+qubits of the same circuit family sharded over the N GPUs.
+
+--impl reference runs the CPU oracle (oracle/) on a bounded sample of the
+same workload on the host cores (there is no reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "amplitude-gate updates/s"
+UNIT = "AGU/s"
+DEPTH = 40
+BASE_QUBITS = 24
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for r in csv.reader(open(self.path)):
+            if len(r) >= 9:
+                rows.append([x.strip() for x in r])
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_sample(layers: int):
+    """The oracle on the first `layers` layers of the same 24-qubit circuit."""
+    import oracle
+    from workloads import circuits as C
+    gates = C.random_brickwork(BASE_QUBITS, layers, seed=2)
+    o = oracle.Oracle(BASE_QUBITS)
+    o.init_basis(0)
+    t0 = time.perf_counter()
+    o.run(gates)
+    o.expectations()
+    t = time.perf_counter() - t0
+    return len(gates) * (1 << BASE_QUBITS) / t, t, len(gates), oracle.Oracle.threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    layers = 2
+    for _ in range(args.warmup):
+        cpu_sample(layers)
+    vals, tot = [], 0.0
+    for _ in range(args.steps):
+        v, t, ng, cores = cpu_sample(layers)
+        vals.append(v)
+        tot += t
+    value = args.steps * ng * (1 << BASE_QUBITS) / tot
+    sample = f"first {layers} of {DEPTH} layers ({ng} gates) of the config-2 circuit at {BASE_QUBITS} qubits, + <Q_i>"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "config2_random_brickwork", "n_qubits": BASE_QUBITS, "depth": DEPTH},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_quant_ph_0608239_b200 import QSim, pack_gates
+    from paper_quant_ph_0608239_b200 import _native as N
+    from workloads import circuits as C
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G = (world - 1).bit_length()
+    n = BASE_QUBITS + G
+    gates = C.random_brickwork(n, DEPTH, seed=2)
+    n_o = len(gates)
+    packed = pack_gates(gates)
+    sim = QSim.distributed(n) if world > 1 else QSim(n)
+    sim.set_option("timing", 1)
+    stream = sim.stream
+
+    def step():
+        sim.init_basis(0)
+        sim.run_circuit(gates, packed=packed)
+        return sim.expectations()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        ex = step()
+    # sanity: <Q_i> in [0,1] and norm 1 before timing
+    assert abs(sim.norm() - 1) < 1e-10 and all(0 <= x <= 1 for x in ex)
+
+    # ---- device-timed region (events on the engine's stream)
+    clocks = Clocks(local)
+    barrier()
+    sim.reset_stats()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = sim.stats()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = args.steps * n_o * float(1 << n) / (ms / 1e3)
+
+    # ---- end-to-end through the public C-ABI with host buffers: the host
+    # gate array (qsim_gate[]) is marshalled + planned + uploaded every step
+    # and <Q_i> comes back to host memory; wall clock, max over ranks.
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    wall = time.perf_counter() - t0
+    tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+    wall = float(tw.item())
+    e2e = args.steps * n_o * float(1 << n) / wall
+    import ctypes
+    h2d = n_o * ctypes.sizeof(N.qsim_gate)
+
+    peak, peak_src = peaks()
+    pass_ms = st["pass_ms"]
+    achieved = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "pass_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2_random_brickwork" if world == 1 else "config2_family_weak",
+                       "n_qubits": n, "depth": DEPTH, "gates_per_step": n_o, "shard_qubits": n - G,
+                       "parallelism": f"sharded{world}" if world > 1 else "single",
+                       "l2": "state %d MiB per GPU > 126 MB L2 (no flush needed)" % ((16 << (n - G)) >> 20)},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": int(st["kernel_launches"]),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_pass", "peak_source": peak_src,
+                         "launches": int(st["passes"]), "kernel_ms": pass_ms,
+                         "kernel_share_of_step": pass_ms / ms if ms > 0 else None},
+            "clocks": ck,
+            "detail": {"passes_per_step": st["passes"] / args.steps, "plan_ms_per_step": st["plan_ms"] / args.steps,
+                       "exchanges_per_step": st["exchanges"] / args.steps,
+                       "reduce_ms_per_step": st["reduce_ms"] / args.steps},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, tcpu, ng, cores = cpu_sample(4)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": f"first 4 of {DEPTH} layers ({ng} gates) of the same circuit, "
+                                              f"{tcpu:.1f} s"}
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,228 @@
+/*
+ * qsim.h -- C-ABI of the B200-native state-vector gate engine
+ * (arXiv quant-ph/0608239, De Raedt et al., "Massive Parallel Quantum
+ * Computer Simulator").  Library: paper_quant_ph_0608239_b200/libqsim_b200.so
+ *
+ * Problem statement: the state of an L-qubit machine
+ * is a vector of 2^L complex amplitudes a(x_{L-1}..x_0); qubit 0 is the
+ * least-significant bit of the index.  Gates update it in place with the
+ * rules of Eqs. NUM2-NUM8.  Amplitudes are complex128
+ * ("8 bytes for a real number"), stored [re, im] interleaved.
+ *
+ * Conventions
+ *   - controls fire on |1>;
+ *   - a 2x2 matrix u[4] is row-major [u00, u01, u10, u11] and maps
+ *     (a0, a1) -> (u00 a0 + u01 a1, u10 a0 + u11 a1) for every index pair
+ *     differing only in the target bit (Eqs. NUM2-NUM5 generalised);
+ *   - every host array passed in is copied before the call returns and is
+ *     never retained (caller keeps ownership);
+ *   - all functions return qsim_status; no exception crosses the ABI.  On
+ *     an argument error the state is untouched.  After QSIM_ERR_CUDA or
+ *     QSIM_ERR_COMM the context is poisoned: only qsim_destroy is valid.
+ *   - gate calls ENQUEUE (so the planner can fuse); readout calls and
+ *     qsim_sync flush the queue.  A context is used by one host thread.
+ *
+ * Distribution: with P = 2^G shards (GPUs or
+ * virtual shards) each holds 2^M amplitudes, M = n - G.  Physical index
+ * bits >= M select the shard ("nonlocal"/global qubits); the qubit
+ * permutation sigma of P:553-568 maps logical qubits to physical bits and
+ * is maintained by the library; readouts always use LOGICAL order.
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qsim_ctx_s *qsim_ctx;
+
+/* layout-compatible with cuDoubleComplex / std::complex<double> */
+typedef struct {
+    double re, im;
+} qsim_c128;
+
+typedef enum {
+    QSIM_OK = 0,
+    QSIM_ERR_ARG = 1,              /* bad pointer / size / option */
+    QSIM_ERR_QUBIT_RANGE = 2,      /* qubit index outside [0, n) */
+    QSIM_ERR_DUP_QUBIT = 3,        /* a qubit repeated among controls/targets */
+    QSIM_ERR_NOT_UNITARY = 4,      /* max |U^dag U - I| > 1e-12 */
+    QSIM_ERR_NOT_PERMUTATION = 5,  /* perm is not a bijection of [0, 2^t) */
+    QSIM_ERR_OOM = 6,              /* device allocation failed */
+    QSIM_ERR_CUDA = 7,             /* CUDA runtime error (context poisoned) */
+    QSIM_ERR_COMM = 8,             /* NCCL error (context poisoned) */
+    QSIM_ERR_STATE = 9,            /* readout before qsim_init_basis */
+    QSIM_ERR_UNSUPPORTED = 10      /* valid request outside implemented limits */
+} qsim_status;
+
+typedef enum { QSIM_G_1Q = 0, QSIM_G_CTRL = 1, QSIM_G_PERM = 2, QSIM_G_SWAP = 3 } qsim_gate_kind;
+
+#define QSIM_MAX_CONTROLS 8
+#define QSIM_MAX_PERM_TARGETS 12
+
+/* One gate of a circuit (qsim_run_circuit).
+ *   QSIM_G_1Q  : target, u
+ *   QSIM_G_CTRL: controls[0..n_controls), target, u   (CNOT, CP, C-V, Toffoli)
+ *   QSIM_G_PERM: controls[0..n_controls), targets[0..n_targets), perm
+ *                (register bit b <-> targets[b]; perm has 2^n_targets entries)
+ *   QSIM_G_SWAP: targets[0], targets[1] (a qubit SWAP: handled as a relabel
+ *                of sigma, no data moves) */
+typedef struct {
+    int32_t kind;
+    int32_t target;
+    int32_t n_controls;
+    int32_t n_targets;
+    int32_t controls[QSIM_MAX_CONTROLS];
+    int32_t targets[QSIM_MAX_PERM_TARGETS];
+    qsim_c128 u[4];
+    const uint32_t *perm;
+} qsim_gate;
+
+typedef enum {
+    QSIM_TRANSPORT_LOCAL = 0,    /* one shard on the current device (P must be 1) */
+    QSIM_TRANSPORT_VIRTUAL = 1,  /* P shards, all on the current device, exchanged by
+                                    device copies: a test backend for the sharded path */
+    QSIM_TRANSPORT_NCCL = 2      /* one process per GPU, shard exchanges over NCCL */
+} qsim_transport;
+
+/* Creation parameters.  Device buffers and the stream may be supplied by the
+ * caller (e.g. PyTorch allocations); NULL means "library allocates/creates".
+ * Caller-supplied buffers must outlive the context.
+ *   shards[r]   : device buffer of 2^M complex128 for shard r (VIRTUAL: r < P;
+ *                 LOCAL/NCCL: only shards[0], this process's shard), 256-B aligned
+ *   scratch     : device scratch of scratch_bytes (exchange staging, reductions);
+ *                 qsim_scratch_bytes() returns the recommended size
+ *   stream      : cudaStream_t to enqueue all work on
+ *   nccl_id     : 128-byte ncclUniqueId from qsim_get_unique_id on rank 0,
+ *                 broadcast to all ranks by the caller (NCCL transport) */
+typedef struct {
+    int32_t n_qubits;   /* 1 <= n <= 62 */
+    int32_t n_ranks;    /* P in {1,2,4,...,64}, power of two, n - log2 P >= 1 */
+    int32_t rank;       /* this process's rank (NCCL), else 0 */
+    int32_t transport;  /* qsim_transport */
+    void *shards[64];
+    void *scratch;
+    size_t scratch_bytes;
+    void *stream;
+    uint8_t nccl_id[128];
+} qsim_config;
+
+/* Standalone single-GPU context on the current CUDA device; the library
+ * cudaMallocs the 2^n state and creates its stream.  n_gpus must be 1
+ * (multi-GPU contexts are created per rank with qsim_create_ext). */
+qsim_status qsim_create(int n_qubits, int n_gpus, qsim_ctx *out);
+/* General creation; see qsim_config. */
+qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out);
+/* Recommended scratch bytes for (n, P). */
+size_t qsim_scratch_bytes(int n_qubits, int n_ranks);
+/* ncclUniqueId (128 bytes) for rank 0 to broadcast. */
+qsim_status qsim_get_unique_id(void *out128);
+qsim_status qsim_destroy(qsim_ctx ctx);
+
+/* |index> (INITIAL STATE).  Lazy: the initial sigma is chosen by
+ * look-ahead over the gates queued before the next flush.  index < 2^n. */
+qsim_status qsim_init_basis(qsim_ctx ctx, uint64_t index);
+
+/* Single-qubit gate on qubit q (Eqs. NUM2-NUM5; H, X, Y, R(phi)
+ * and any unitary U). */
+qsim_status qsim_apply_1q(qsim_ctx ctx, int q, const qsim_c128 u[4]);
+
+/* Controlled gate: U on target where all n_controls control qubits are 1
+ * (CNOT Eq. NUM6, controlled phase Eq. COMM5 P:285-295,
+ * controlled-V Eq. NUM7, Toffoli Eq. NUM8).
+ * n_controls <= QSIM_MAX_CONTROLS. */
+qsim_status qsim_apply_controlled(qsim_ctx ctx, const int *controls, int n_controls, int target,
+                                  const qsim_c128 u[4]);
+
+/* Controlled classical reversible map of a target register (the
+ * "conditional operation" of Shor's step 2):
+ * |c, w> -> |c, perm[w]> when all controls are 1.  Register bit b of w is
+ * qubit targets[b]; n_targets <= QSIM_MAX_PERM_TARGETS. */
+qsim_status qsim_apply_perm(qsim_ctx ctx, const int *controls, int n_controls, const int *targets,
+                            int n_targets, const uint32_t *perm);
+
+/* Quantum SWAP of qubits a and b (relabel of sigma; no data movement). */
+qsim_status qsim_apply_swap(qsim_ctx ctx, int a, int b);
+
+/* The paper's "SWAP K l_1..l_K g_1..g_K" command (App. A
+ * P:1244-1258): exchange data so that the K given qubits that are currently
+ * nonlocal become local and the K given local qubits become nonlocal
+ * (Eqs. onequbitchange, twoqubitchange0-5).  Optional: the planner inserts
+ * such exchanges itself.  Flushes. */
+qsim_status qsim_remap(qsim_ctx ctx, const int *local_qubits, const int *global_qubits, int K);
+
+/* Enqueue a whole gate list (see qsim_gate). Validated entirely before any
+ * gate is queued. */
+qsim_status qsim_run_circuit(qsim_ctx ctx, const qsim_gate *gates, size_t n_gates);
+
+/* Marginal probabilities over the k listed qubits (k <= 24):
+ * out[beta] = sum_{x : x_{qubits[b]} = beta_b} |a(x)|^2, host array of 2^k
+ * doubles.  k = 0 gives the norm (Eq. STAT1).  Deterministic
+ * fixed-order summation.  Non-collapsing. */
+qsim_status qsim_probabilities(qsim_ctx ctx, const int *qubits, int k, double *out);
+
+/* <Q_i> = sum_k p_k k_i for every qubit i (Eq. Shor7); host
+ * array of n doubles.  Non-collapsing. */
+qsim_status qsim_expectations(qsim_ctx ctx, double *out);
+
+/* n_shots basis states of the listed qubits drawn with probability
+ * |<x|Phi>|^2 by inverse CDF with the counter-based
+ * SplitMix64 rule (reading R14).  Non-collapsing.  Host out. */
+qsim_status qsim_measure(qsim_ctx ctx, const int *qubits, int k, uint64_t seed, uint64_t n_shots,
+                         uint64_t *out);
+
+/* Copy `count` amplitudes starting at LOGICAL index `first` to host memory
+ * (sigma undone).  For tests / small states. */
+qsim_status qsim_get_amplitudes(qsim_ctx ctx, uint64_t first, uint64_t count, qsim_c128 *host_out);
+
+/* Flush the queue and wait for the device. */
+qsim_status qsim_sync(qsim_ctx ctx);
+
+/* Current qubit -> physical-bit map (sigma^-1 of P:558); out[n]. Flushes. */
+qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
+
+/* Options (integers): "fusion" (1 = fused tile passes [default], 0 = one
+ * generic kernel per gate), "timing" (1 = CUDA-event time every launch),
+ * "max_scan" (planner look-ahead window), "exchange_chunk_mb". */
+qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
+
+typedef struct {
+    uint64_t gates;            /* user gates enqueued (N_O) */
+    uint64_t flushes;
+    uint64_t passes;           /* fused tile-pass launches */
+    uint64_t generic_launches; /* one-gate kernels */
+    uint64_t perm_launches;
+    uint64_t exchanges;        /* K-swap remaps */
+    uint64_t exchange_bytes;   /* bytes this rank sent */
+    uint64_t kernel_launches;  /* all kernels of this library */
+    uint64_t relabels;         /* SWAP gates absorbed into sigma */
+    double pass_ms;            /* event time of fused passes (timing=1) */
+    double generic_ms;
+    double perm_ms;
+    double exchange_ms;
+    double reduce_ms;
+    double plan_ms;            /* host planning time */
+    uint64_t pass_amp_bytes;   /* algorithmic bytes of the timed passes (32 B/amp/pass) */
+} qsim_stats;
+
+qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);
+qsim_status qsim_reset_stats(qsim_ctx ctx);
+
+const char *qsim_status_str(qsim_status s);
+const char *qsim_last_error(qsim_ctx ctx);
+
+/* Host-only planner introspection (no GPU needed): plan `gates` for an
+ * n-qubit state over P shards starting from the identity sigma and write a
+ * JSON description of the steps (passes, perms, exchanges, relabels) into
+ * buf.  Returns QSIM_ERR_ARG if buf is too small. */
+qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
+                           int fusion, char *buf, size_t buf_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSIM_H */

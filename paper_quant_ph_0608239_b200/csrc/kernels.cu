@@ -1,0 +1,643 @@
+// kernels.cu -- hand-written sm_100a kernels of the state-vector engine.
+//
+// All kernels update the complex128 shard in place ("all these
+// operations can be done in place").  The hot kernel is k_pass: one HBM
+// read + write of the shard (32 B/amplitude) applies a whole planned list of
+// gates (Eqs. NUM2-NUM8) to 4096-amplitude tiles held in
+// registers, with warp shuffles and swizzled shared-memory transposes.
+// 256-bit global accesses (ld/st.global.v4.f64 -> LDG/STG.E.ENL2.256 on
+// sm_100a) move two amplitudes per instruction.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.h"
+#include "kernels.h"
+
+namespace qsb {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ void ld256(const double2 *p, double2 &a, double2 &b)
+{
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(double2 *p, const double2 &a, const double2 &b)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
+}
+
+__device__ __forceinline__ double2 cmul(double2 f, double2 a)
+{
+    return make_double2(fma(f.x, a.x, -f.y * a.y), fma(f.x, a.y, f.y * a.x));
+}
+
+// (c0 * x + c1 * y), complex
+__device__ __forceinline__ double2 cmac2(double2 c0, double2 x, double2 c1, double2 y)
+{
+    double re = fma(c0.x, x.x, fma(-c0.y, x.y, fma(c1.x, y.x, -c1.y * y.y)));
+    double im = fma(c0.x, x.y, fma(c0.y, x.x, fma(c1.x, y.y, c1.y * y.x)));
+    return make_double2(re, im);
+}
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t v, int p)
+{
+    return ((v >> p) << (p + 1)) | (v & ((1ULL << p) - 1));
+}
+
+// ---------------------------------------------------------------- k_pass
+template <int K, int CODE>
+__device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp *__restrict__ op, uint32_t mreg,
+                                          uint32_t vreg)
+{
+    double2 u00, u01, u10, u11;
+    if (CODE != OPC_XS) {
+        u00 = make_double2(op->m[0], op->m[1]);
+        u01 = make_double2(op->m[2], op->m[3]);
+        u10 = make_double2(op->m[4], op->m[5]);
+        u11 = make_double2(op->m[6], op->m[7]);
+    }
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        const int i0 = ((p >> K) << (K + 1)) | (p & ((1 << K) - 1));
+        const int i1 = i0 | (1 << K);
+        if ((i0 & mreg) != vreg) continue;
+        const double2 x = a[i0], y = a[i1];
+        if (CODE == OPC_XS) {
+            a[i0] = y;
+            a[i1] = x;
+        } else if (CODE == OPC_U2R) {
+            a[i0] = make_double2(fma(u00.x, x.x, u01.x * y.x), fma(u00.x, x.y, u01.x * y.y));
+            a[i1] = make_double2(fma(u10.x, x.x, u11.x * y.x), fma(u10.x, x.y, u11.x * y.y));
+        } else {
+            a[i0] = cmac2(u00, x, u01, y);
+            a[i1] = cmac2(u10, x, u11, y);
+        }
+    }
+}
+
+template <int CODE>
+__device__ __forceinline__ void reg_dispatch(double2 (&a)[16], const KOp *__restrict__ op, int k, uint32_t mreg,
+                                             uint32_t vreg)
+{
+    switch (k) {
+    case 0: reg_apply<0, CODE>(a, op, mreg, vreg); break;
+    case 1: reg_apply<1, CODE>(a, op, mreg, vreg); break;
+    case 2: reg_apply<2, CODE>(a, op, mreg, vreg); break;
+    default: reg_apply<3, CODE>(a, op, mreg, vreg); break;
+    }
+}
+
+__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+__device__ __forceinline__ int pick3(int x, int a0, int a1, int a2) { return x == 0 ? a0 : (x == 1 ? a1 : a2); }
+
+__global__ void __launch_bounds__(kPassThreads, 2)
+    k_pass(const __grid_constant__ PassDesc d, double2 *__restrict__ st, const KOp *__restrict__ ops)
+{
+    extern __shared__ double2 sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    uint64_t base = blockIdx.x;
+#pragma unroll
+    for (int j = 0; j < kTileBits; j++) base = insert_zero(base, d.tile_sorted[j]);
+    const uint64_t gcta = d.rank_bits | base;
+
+    int rREG = d.role_tri[ROLE_REG], rLANE = d.role_tri[ROLE_LANE], rWARP = d.role_tri[ROLE_WARP];
+
+    double2 a[16];
+    uint64_t r0, r1, r2, toff;
+    auto offsets = [&]() {
+        r0 = 1ULL << d.tri[rREG][0];
+        r1 = 1ULL << d.tri[rREG][1];
+        r2 = 1ULL << d.tri[rREG][2];
+        const uint64_t l0 = 1ULL << d.tri[rLANE][0], l1 = 1ULL << d.tri[rLANE][1], l2 = 1ULL << d.tri[rLANE][2];
+        const uint64_t w0 = 1ULL << d.tri[rWARP][0], w1 = 1ULL << d.tri[rWARP][1], w2 = 1ULL << d.tri[rWARP][2];
+        toff = (uint64_t)((lane & 3) << 1) | ((lane & 4) ? l0 : 0) | ((lane & 8) ? l1 : 0) |
+               ((lane & 16) ? l2 : 0) | ((warp & 1) ? w0 : 0) | ((warp & 2) ? w1 : 0) | ((warp & 4) ? w2 : 0);
+    };
+    offsets();
+    {
+        double2 *p = st + base + toff;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t ro = ((j & 1) ? r0 : 0) | ((j & 2) ? r1 : 0) | ((j & 4) ? r2 : 0);
+            ld256(p + ro, a[2 * j], a[2 * j + 1]);
+        }
+    }
+
+    const KOp *__restrict__ prog = ops + d.op_begin;
+    for (int o = 0; o < d.n_ops; o++) {
+        const KOp *__restrict__ op = prog + o;
+        const int code = op->code;
+        if (code == OPC_TRANS) {
+            // registers -> swizzled smem with the current roles, then back with the new roles
+            {
+                const int sl = ((lane & 3) << 1) | ((lane >> 2) << (3 + 3 * rLANE)) | (warp << (3 + 3 * rWARP));
+                const int sh = 3 + 3 * rREG;
+#pragma unroll
+                for (int i = 0; i < 16; i++) sm[swz(sl | (i & 1) | ((i >> 1) << sh))] = a[i];
+            }
+            __syncthreads();
+            const int ta = op->ta, tb = op->tb;
+            const int xa = pick3(ta, rREG, rLANE, rWARP), xb = pick3(tb, rREG, rLANE, rWARP);
+            if (ta == ROLE_REG) rREG = xb; else if (ta == ROLE_LANE) rLANE = xb; else rWARP = xb;
+            if (tb == ROLE_REG) rREG = xa; else if (tb == ROLE_LANE) rLANE = xa; else rWARP = xa;
+            {
+                const int sl = ((lane & 3) << 1) | ((lane >> 2) << (3 + 3 * rLANE)) | (warp << (3 + 3 * rWARP));
+                const int sh = 3 + 3 * rREG;
+#pragma unroll
+                for (int i = 0; i < 16; i++) a[i] = sm[swz(sl | (i & 1) | ((i >> 1) << sh))];
+            }
+            __syncthreads();
+            continue;
+        }
+        const bool tp = ((lane & op->mlane) == op->vlane) && ((warp & op->mwarp) == op->vwarp) &&
+                        ((gcta & op->mout) == op->vout);
+        const uint32_t mreg = op->mreg, vreg = op->vreg;
+        if (code == OPC_PHASE) {
+            if (!tp) continue;
+            const double2 f = make_double2(op->m[0], op->m[1]);
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if ((i & mreg) == vreg) a[i] = cmul(f, a[i]);
+            continue;
+        }
+        if (op->role == ROLE_REG) {
+            if (!tp) continue;
+            const int k = op->k;
+            if (code == OPC_XS) reg_dispatch<OPC_XS>(a, op, k, mreg, vreg);
+            else if (code == OPC_U2R) reg_dispatch<OPC_U2R>(a, op, k, mreg, vreg);
+            else reg_dispatch<OPC_U2>(a, op, k, mreg, vreg);
+            continue;
+        }
+        // LANE role: partner amplitude via shuffles (partners share the predicate)
+        if (!__any_sync(FULL, tp)) continue;
+        const int kb = 1 << op->k;
+        const bool hi = (lane & kb) != 0;
+        if (code == OPC_XS) {
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                double2 p;
+                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+                if (tp && (i & mreg) == vreg) a[i] = p;
+            }
+        } else if (code == OPC_U2R) {
+            const double cs = hi ? op->m[6] : op->m[0];
+            const double co = hi ? op->m[4] : op->m[2];
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                double2 p;
+                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+                if (tp && (i & mreg) == vreg)
+                    a[i] = make_double2(fma(cs, a[i].x, co * p.x), fma(cs, a[i].y, co * p.y));
+            }
+        } else {
+            const double2 cs = hi ? make_double2(op->m[6], op->m[7]) : make_double2(op->m[0], op->m[1]);
+            const double2 co = hi ? make_double2(op->m[4], op->m[5]) : make_double2(op->m[2], op->m[3]);
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                double2 p;
+                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+                if (tp && (i & mreg) == vreg) a[i] = cmac2(cs, a[i], co, p);
+            }
+        }
+    }
+
+    offsets();
+    {
+        double2 *p = st + base + toff;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t ro = ((j & 1) ? r0 : 0) | ((j & 2) ? r1 : 0) | ((j & 4) ? r2 : 0);
+            st256(p + ro, a[2 * j], a[2 * j + 1]);
+        }
+    }
+}
+
+void launch_pass(const PassDesc &d, double2 *st, const KOp *ops, cudaStream_t s)
+{
+    static bool attr = false;
+    const int smem = d.use_smem ? kTileAmps * (int)sizeof(double2) : 0;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileAmps * (int)sizeof(double2));
+        attr = true;
+    }
+    k_pass<<<(unsigned)d.n_inst, kPassThreads, smem, s>>>(d, st, ops);
+}
+
+int pass_regs_per_thread()
+{
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k_pass) != cudaSuccess) return -1;
+    return fa.numRegs;
+}
+
+// -------------------------------------------------------- generic kernels
+struct U8 {
+    double m[8];
+};
+
+__global__ void k_gate_generic(double2 *__restrict__ st, uint64_t half, int t, uint64_t rank_bits, uint64_t cm,
+                               uint64_t cv, int code, U8 u)
+{
+    const double2 u00 = make_double2(u.m[0], u.m[1]), u01 = make_double2(u.m[2], u.m[3]);
+    const double2 u10 = make_double2(u.m[4], u.m[5]), u11 = make_double2(u.m[6], u.m[7]);
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < half;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i0 = insert_zero(p, t), i1 = i0 | (1ULL << t);
+        if (((rank_bits | i0) & cm) != cv) continue;
+        const double2 x = st[i0], y = st[i1];
+        if (code == OPC_XS) {
+            st[i0] = y;
+            st[i1] = x;
+        } else {
+            st[i0] = cmac2(u00, x, u01, y);
+            st[i1] = cmac2(u10, x, u11, y);
+        }
+    }
+}
+
+__global__ void k_phase_generic(double2 *__restrict__ st, uint64_t D, uint64_t rank_bits, uint64_t cm, uint64_t cv,
+                                double fr, double fi)
+{
+    const double2 f = make_double2(fr, fi);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x)
+        if (((rank_bits | i) & cm) == cv) st[i] = cmul(f, st[i]);
+}
+
+static unsigned grid_for(uint64_t work, int threads)
+{
+    uint64_t g = (work + threads - 1) / threads;
+    const uint64_t cap = 148ULL * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+void launch_gate_generic(double2 *st, int M, uint64_t rank_bits, int t, uint64_t cm, uint64_t cv, int code,
+                         const double *m, cudaStream_t s)
+{
+    U8 u;
+    for (int k = 0; k < 8; k++) u.m[k] = m[k];
+    const uint64_t half = 1ULL << (M - 1);
+    k_gate_generic<<<grid_for(half, 256), 256, 0, s>>>(st, half, t, rank_bits, cm, cv, code, u);
+}
+
+void launch_phase_generic(double2 *st, int M, uint64_t rank_bits, uint64_t cm, uint64_t cv, double fr, double fi,
+                          cudaStream_t s)
+{
+    const uint64_t D = 1ULL << M;
+    k_phase_generic<<<grid_for(D, 256), 256, 0, s>>>(st, D, rank_bits, cm, cv, fr, fi);
+}
+
+// ------------------------------------------------------------------ perm
+__device__ __forceinline__ uint64_t dep_tile(uint32_t e, const int32_t *pos, int nb)
+{
+    uint64_t r = 0;
+    for (int b = 0; b < nb; b++) r |= (uint64_t)((e >> b) & 1) << pos[b];
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_perm(const __grid_constant__ PermDesc d, double2 *__restrict__ st,
+                                              const uint32_t *__restrict__ perm_tab)
+{
+    extern __shared__ double2 sm[];
+    uint64_t base = blockIdx.x;
+    for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
+    if (((d.rank_bits | base) & d.m_ctrl_out) != d.v_ctrl_out) return;
+    const uint32_t E = 1u << d.tile_bits, T = (1u << d.t) - 1;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) sm[e] = st[base + dep_tile(e, d.tile_pos, d.tile_bits)];
+    __syncthreads();
+    const uint32_t *perm = perm_tab + d.perm_offset;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        if ((e & d.m_ctrl_tile) != d.v_ctrl_tile) continue;
+        const uint32_t dst = (e & ~T) | perm[e & T];
+        st[base + dep_tile(dst, d.tile_pos, d.tile_bits)] = sm[e];
+    }
+}
+
+void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaStream_t s)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileAmps * (int)sizeof(double2));
+        attr = true;
+    }
+    k_perm<<<(unsigned)d.n_inst, 256, (1 << d.tile_bits) * (int)sizeof(double2), s>>>(d, st, perm_tab);
+}
+
+// ------------------------------------------------------------------ init
+__global__ void k_fill_zero(double2 *__restrict__ st, uint64_t n_pairs)
+{
+    const double2 z = make_double2(0.0, 0.0);
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n_pairs;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        st256(st + 2 * p, z, z);
+}
+
+__global__ void k_set_amp(double2 *st, uint64_t idx) { st[idx] = make_double2(1.0, 0.0); }
+
+void launch_init(double2 *st, uint64_t n_amps, int64_t one_at, cudaStream_t s)
+{
+    if (n_amps >= 2) {
+        const uint64_t pairs = n_amps / 2;
+        k_fill_zero<<<grid_for(pairs, 256), 256, 0, s>>>(st, pairs);
+    } else {
+        k_phase_generic<<<1, 32, 0, s>>>(st, 1, 0, 0, 0, 0.0, 0.0);
+    }
+    if (one_at >= 0) k_set_amp<<<1, 1, 0, s>>>(st, (uint64_t)one_at);
+}
+
+// ------------------------------------------------------------- reductions
+// fixed-shape block sum of one value per thread (deterministic)
+__device__ double block_sum(double v, double *red)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < nw ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
+    }
+    return r;  // valid in thread 0
+}
+
+// Marginal over listed qubits, stage 1: per 2^cb-amplitude chunk, |a|^2 into
+// smem and pairwise-reduce the unlisted chunk bits in ascending order.
+__global__ void __launch_bounds__(256) k_probs_chunk(const double2 *__restrict__ st, const __grid_constant__ ProbsDesc d,
+                                                     double *__restrict__ partial)
+{
+    extern __shared__ double v[];
+    const uint32_t E = 1u << d.cb;
+    const uint64_t c = blockIdx.x;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        const double2 x = st[(c << d.cb) + e];
+        v[e] = x.x * x.x + x.y * x.y;
+    }
+    __syncthreads();
+    uint32_t doneb = 0;
+    for (int b = 0; b < d.cb; b++) {
+        if (!((d.red_mask >> b) & 1)) continue;
+        for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
+            if (!(e & (1u << b)) && !(e & doneb)) v[e] += v[e | (1u << b)];
+        doneb |= 1u << b;
+        __syncthreads();
+    }
+    const uint32_t B = 1u << d.k_low;
+    for (uint32_t bl = threadIdx.x; bl < B; bl += blockDim.x) {
+        uint32_t e = 0;
+        for (int j = 0; j < d.k_low; j++) e |= ((bl >> j) & 1u) << d.lowpos[j];
+        partial[c * B + bl] = v[e];
+    }
+}
+
+// stage 2: one block per output bin; fixed thread-strided order + block tree
+__global__ void __launch_bounds__(256) k_probs_final(const double *__restrict__ partial, const __grid_constant__ ProbsDesc d,
+                                                     double *__restrict__ out)
+{
+    __shared__ double red[32];
+    const uint64_t beta = blockIdx.x;
+    uint32_t bl = 0;
+    uint64_t cfix = 0;
+    bool ok = true;
+    int jl = 0;
+    for (int j = 0; j < d.k; j++) {
+        const uint64_t bv = (beta >> j) & 1;
+        const int p = d.pos[j];
+        if (p < d.cb) bl |= (uint32_t)bv << jl++;
+        else if (p < d.M) cfix |= bv << (p - d.cb);
+        else if (((d.rank >> (p - d.M)) & 1) != bv) ok = false;
+    }
+    if (!ok) {
+        if (threadIdx.x == 0) out[beta] = 0.0;
+        return;
+    }
+    const uint64_t nj = 1ULL << d.n_free, B = 1ULL << d.k_low;
+    double s = 0.0;
+    for (uint64_t j = threadIdx.x; j < nj; j += blockDim.x) {
+        uint64_t c = cfix;
+        for (int b = 0; b < d.n_free; b++) c |= ((j >> b) & 1) << d.freepos[b];
+        s += partial[c * B + bl];
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[beta] = s;
+}
+
+void launch_probs(const double2 *st, const ProbsDesc &d, double *partial, double *out, cudaStream_t s)
+{
+    const uint64_t nchunks = 1ULL << (d.M - d.cb);
+    k_probs_chunk<<<(unsigned)nchunks, 256, (1 << d.cb) * (int)sizeof(double), s>>>(st, d, partial);
+    k_probs_final<<<(unsigned)(1ULL << d.k), 256, 0, s>>>(partial, d, out);
+}
+
+// <Q_b> partial sums per chunk: for every chunk bit b the sum over amplitudes
+// with bit b = 1, plus the chunk total (index cb).
+__global__ void __launch_bounds__(256) k_expect_chunk(const double2 *__restrict__ st, int cb,
+                                                      double *__restrict__ partial)
+{
+    extern __shared__ double v[];
+    __shared__ double red[32];
+    const uint32_t E = 1u << cb;
+    const uint64_t c = blockIdx.x;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        const double2 x = st[(c << cb) + e];
+        v[e] = x.x * x.x + x.y * x.y;
+    }
+    __syncthreads();
+    for (int b = 0; b <= cb; b++) {
+        double s = 0.0;
+        if (b < cb) {
+            for (uint32_t j = threadIdx.x; j < (E >> 1); j += blockDim.x)
+                s += v[insert_zero(j, b) | (1u << b)];
+        } else {
+            for (uint32_t j = threadIdx.x; j < E; j += blockDim.x) s += v[j];
+        }
+        s = block_sum(s, red);
+        if (threadIdx.x == 0) partial[c * (cb + 1) + b] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_expect_final(const double *__restrict__ partial, int cb, int M,
+                                                      double *__restrict__ out)
+{
+    __shared__ double red[32];
+    const int o = blockIdx.x;  // physical bit o < M, or o == M: total
+    const uint64_t nch = 1ULL << (M - cb);
+    double s = 0.0;
+    for (uint64_t c = threadIdx.x; c < nch; c += blockDim.x) {
+        if (o < cb) s += partial[c * (cb + 1) + o];
+        else if (o < M) s += ((c >> (o - cb)) & 1) ? partial[c * (cb + 1) + cb] : 0.0;
+        else s += partial[c * (cb + 1) + cb];
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[o] = s;
+}
+
+void launch_expect(const double2 *st, int M, double *partial, double *out, cudaStream_t s)
+{
+    const int cb = M < 12 ? M : 12;
+    const uint64_t nch = 1ULL << (M - cb);
+    k_expect_chunk<<<(unsigned)nch, 256, (1 << cb) * (int)sizeof(double), s>>>(st, cb, partial);
+    k_expect_final<<<M + 1, 256, 0, s>>>(partial, cb, M, out);
+}
+
+// ------------------------------------------------------------- sampling
+__device__ __forceinline__ uint64_t sm64_dev(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(1024) k_cdf(const double *__restrict__ p, uint64_t B, double *__restrict__ C)
+{
+    __shared__ double tot[1024];
+    const uint64_t seg = (B + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * seg, hi = lo + seg < B ? lo + seg : B;
+    double acc = 0.0;
+    for (uint64_t i = lo; i < hi; i++) { acc += p[i]; C[i] = acc; }
+    tot[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < (int)blockDim.x; t++) { const double x = tot[t]; tot[t] = run; run += x; }
+    }
+    __syncthreads();
+    const double off = tot[threadIdx.x];
+    for (uint64_t i = lo; i < hi; i++) C[i] += off;
+}
+
+__global__ void k_sample(const double *__restrict__ C, uint64_t B, uint64_t seed, uint64_t n, uint64_t *__restrict__ out)
+{
+    const double tot = C[B - 1];
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n; s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = sm64_dev(seed + (s + 1) * 0x9E3779B97F4A7C15ULL);
+        const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0) * tot;
+        uint64_t lo = 0, hi = B - 1;  // min beta with C[beta] > u (B-1 if none)
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (C[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        out[s] = lo;
+    }
+}
+
+void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *out, cudaStream_t s)
+{
+    const uint64_t B = 1ULL << k;
+    k_cdf<<<1, 1024, 0, s>>>(p, B, cdf);
+    if (n_shots) k_sample<<<grid_for(n_shots, 256), 256, 0, s>>>(cdf, B, seed, n_shots, out);
+}
+
+// ------------------------------------------------------------- readout
+struct Phys64 {
+    int32_t p[64];
+};
+
+__global__ void k_gather(double2 *__restrict__ out, uint64_t first, uint64_t count, double2 *const *shards, int virt,
+                         int my_rank, int M, int n, Phys64 ph)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = first + i;
+        uint64_t phys = 0;
+        for (int q = 0; q < n; q++) phys |= ((x >> q) & 1) << ph.p[q];
+        const uint64_t r = phys >> M, li = phys & ((1ULL << M) - 1);
+        double2 v;
+        if (virt) v = shards[r][li];
+        else v = ((int)r == my_rank) ? shards[0][li] : make_double2(0.0, 0.0);
+        out[i] = v;
+    }
+}
+
+void launch_gather(double2 *out, uint64_t first, uint64_t count, double2 *const *shards_dev, int virt, int my_rank,
+                   int M, int n, const int *phys_of, cudaStream_t s)
+{
+    Phys64 ph;
+    for (int q = 0; q < 64; q++) ph.p[q] = q < n ? phys_of[q] : 0;
+    k_gather<<<grid_for(count, 256), 256, 0, s>>>(out, first, count, shards_dev, virt, my_rank, M, n, ph);
+}
+
+// ------------------------------------------------------------- exchange
+struct LPos {
+    int32_t sorted[8];
+    uint64_t off_bits[8];  // 1 << lpos[i] in pairing order
+};
+
+__device__ __forceinline__ uint64_t other_index(uint64_t j, const LPos &L, int K)
+{
+    for (int i = 0; i < K; i++) j = insert_zero(j, L.sorted[i]);
+    return j;
+}
+
+__global__ void k_swap_blocks(double2 *__restrict__ A, double2 *__restrict__ B, uint64_t n_other, int K, LPos L,
+                              uint64_t offA, uint64_t offB)
+{
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_other;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t idx = other_index(j, L, K);
+        const double2 x = A[idx | offA], y = B[idx | offB];
+        A[idx | offA] = y;
+        B[idx | offB] = x;
+    }
+}
+
+__global__ void k_pack(double2 *__restrict__ shard, double2 *__restrict__ buf, uint64_t first, uint64_t count, int K,
+                       LPos L, uint64_t off, int unpack)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t idx = other_index(first + i, L, K) | off;
+        if (unpack) shard[idx] = buf[i];
+        else buf[i] = shard[idx];
+    }
+}
+
+static LPos make_lpos(int K, const int *lpos, uint64_t c, uint64_t *off)
+{
+    LPos L{};
+    int tmp[8];
+    for (int i = 0; i < K; i++) tmp[i] = lpos[i];
+    for (int i = 0; i < K; i++)
+        for (int j = i + 1; j < K; j++)
+            if (tmp[j] < tmp[i]) { int x = tmp[i]; tmp[i] = tmp[j]; tmp[j] = x; }
+    *off = 0;
+    for (int i = 0; i < K; i++) {
+        L.sorted[i] = tmp[i];
+        L.off_bits[i] = 1ULL << lpos[i];
+        if ((c >> i) & 1) *off |= 1ULL << lpos[i];
+    }
+    return L;
+}
+
+void launch_swap_blocks(double2 *A, double2 *B, int M, int K, const int *lpos, uint64_t cA, uint64_t cB, cudaStream_t s)
+{
+    uint64_t offA, offB;
+    LPos L = make_lpos(K, lpos, cA, &offA);
+    make_lpos(K, lpos, cB, &offB);
+    const uint64_t n_other = 1ULL << (M - K);
+    k_swap_blocks<<<grid_for(n_other, 256), 256, 0, s>>>(A, B, n_other, K, L, offA, offB);
+}
+
+void launch_pack(const double2 *shard, double2 *buf, int M, int K, const int *lpos, uint64_t c, uint64_t first,
+                 uint64_t count, int unpack, cudaStream_t s)
+{
+    uint64_t off;
+    LPos L = make_lpos(K, lpos, c, &off);
+    (void)M;
+    k_pack<<<grid_for(count, 256), 256, 0, s>>>(const_cast<double2 *>(shard), buf, first, count, K, L, off, unpack);
+}
+
+}  // namespace qsb

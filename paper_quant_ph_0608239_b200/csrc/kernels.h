@@ -1,0 +1,44 @@
+// kernels.h -- host launch wrappers of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.h"
+
+namespace qsb {
+
+struct ProbsDesc {
+    int32_t cb;          // chunk bits (min(12, M))
+    int32_t M;
+    int32_t k;           // listed qubits
+    int32_t k_low;       // listed qubits with physical bit < cb
+    int32_t n_free;      // chunk-index bits not fixed by listed qubits
+    int32_t rank_glob_ok_mask_unused;
+    uint64_t rank;       // this shard's rank
+    uint32_t red_mask;   // chunk bits to reduce (unlisted, < cb)
+    int32_t lowpos[12];  // physical positions of low listed qubits (partial bin bit j)
+    int32_t pos[24];     // physical position of listed qubit j (any class)
+    int32_t freepos[64]; // chunk-index bit positions that are free
+};
+
+void launch_pass(const PassDesc &d, double2 *st, const KOp *ops, cudaStream_t s);
+void launch_gate_generic(double2 *st, int M, uint64_t rank_bits, int t, uint64_t cm, uint64_t cv, int code,
+                         const double *m, cudaStream_t s);
+void launch_phase_generic(double2 *st, int M, uint64_t rank_bits, uint64_t cm, uint64_t cv, double fr, double fi,
+                          cudaStream_t s);
+void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaStream_t s);
+void launch_init(double2 *st, uint64_t n_amps, int64_t one_at, cudaStream_t s);
+void launch_probs(const double2 *st, const ProbsDesc &d, double *partial, double *out, cudaStream_t s);
+void launch_expect(const double2 *st, int M, double *partial, double *out /* M+1 */, cudaStream_t s);
+void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *out,
+                   cudaStream_t s);
+void launch_gather(double2 *out, uint64_t first, uint64_t count, double2 *const *shards_dev, int virt, int my_rank,
+                   int M, int n, const int *phys_of, cudaStream_t s);
+void launch_swap_blocks(double2 *A, double2 *B, int M, int K, const int *lpos, uint64_t cA, uint64_t cB,
+                        cudaStream_t s);
+void launch_pack(const double2 *shard, double2 *buf, int M, int K, const int *lpos, uint64_t c, uint64_t first,
+                 uint64_t count, int unpack, cudaStream_t s);
+int pass_regs_per_thread();
+
+}  // namespace qsb

@@ -1,0 +1,88 @@
+// plan.h -- host-side gate queue classification and the fusion / placement
+// planner.  Pure C++, no CUDA.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+namespace qsb {
+
+enum GateKind { GK_U2 = 0, GK_PERM = 2, GK_SWAP = 3 };
+enum GateClass { CLS_GENERAL = 0, CLS_REAL = 1, CLS_DIAG = 2, CLS_XS = 3 };
+
+// A validated gate in LOGICAL qubits.
+struct GateRec {
+    int kind = GK_U2;
+    int target = -1;                  // U2
+    std::vector<int> controls;
+    std::vector<int> targets;         // PERM (register order) / SWAP (2)
+    double u[8] = {1, 0, 0, 0, 0, 0, 1, 0};
+    int cls = CLS_GENERAL;
+    std::vector<uint32_t> perm;
+    uint64_t qN = 0;  // logical qubits acted on non-diagonally
+    uint64_t qD = 0;  // logical qubits acted on only diagonally (controls, diag target)
+    int id = 0;       // position in the user's sequence
+};
+
+void classify(GateRec &g);  // sets cls, qN, qD
+
+enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5 };
+
+struct Step {
+    int type = ST_PASS;
+    // ST_PASS
+    PassDesc pass{};              // op_begin relative to this step's ops
+    std::vector<KOp> ops;
+    std::vector<int> op_gate;     // gate id behind each op (-1 for TRANS)
+    std::vector<int> op_t;        // physical target of each op (-1: PHASE/TRANS)
+    std::vector<uint64_t> op_cm, op_cv;  // full-index predicate of each op (for introspection)
+    // ST_GENERIC: one U2 on physical target t, controls (full-index mask/val)
+    // ST_PHASE  : multiply by f where (full & mask) == val
+    int code = OPC_U2;
+    int t = -1;
+    uint64_t cm = 0, cv = 0;
+    double m[8] = {0};
+    int gate_id = -1;
+    // ST_PERM
+    std::vector<int> ptargets;    // physical positions, register order
+    std::vector<uint32_t> perm;
+    // ST_EXCHANGE: swap local bits lpos[i] with global bits gpos[i]
+    std::vector<int> lpos, gpos;
+    // ST_RELABEL: swap physical roles of logical qubits a,b (no data)
+    int ra = -1, rb = -1;
+};
+
+struct PlanOptions {
+    bool fusion = true;
+    int max_scan = 1 << 30;   // look-ahead window (gates) per pass
+};
+
+class Planner {
+public:
+    Planner(int n, int G);
+    int n, G, M;
+    std::vector<int> phys_of;   // logical qubit -> physical bit
+    std::vector<int> qubit_at;  // physical bit -> logical qubit
+
+    // initial sigma by look-ahead: perm targets on the lowest
+    // bits; the G qubits whose first non-diagonal use is latest go global.
+    void choose_initial_layout(const std::vector<GateRec> &gates);
+    void plan(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out);
+    // explicit paper "SWAP K" command
+    void remap(const std::vector<int> &local_q, const std::vector<int> &global_q, std::vector<Step> &out);
+
+private:
+    void emit_exchange(const std::vector<GateRec> &gates, const std::vector<char> &done, size_t first,
+                       std::vector<Step> &out);
+    void build_pass(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
+                    const PlanOptions &opt, std::vector<Step> &out);
+    void emit_generic(const GateRec &g, std::vector<Step> &out);
+    void emit_perm(const GateRec &g, std::vector<Step> &out);
+    void swap_layout(int pa, int pb);
+};
+
+std::string plan_to_json(const Planner &final_state, const std::vector<Step> &steps);
+
+}  // namespace qsb

@@ -1,0 +1,1033 @@
+// runtime.cpp -- the qsim_* C-ABI (include/qsim.h): context, validation,
+// gate queue, flush (planner -> device steps), exchange engine (virtual
+// shards / NCCL), reductions, sampling and readout.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qsim.h"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace qsb;
+
+namespace {
+
+struct TimedRange {
+    cudaEvent_t a, b;
+    int cat;  // 0 pass, 1 generic, 2 perm, 3 exchange, 4 reduce
+    uint64_t bytes;
+};
+
+}  // namespace
+
+struct qsim_ctx_s {
+    int n = 0, P = 1, G = 0, M = 0, rank = 0, transport = QSIM_TRANSPORT_LOCAL;
+    std::vector<double2 *> shards;
+    bool own_shards = false;
+    double2 *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    bool own_scratch = false;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    Planner *planner = nullptr;
+    bool initialized = false, init_pending = false;
+    uint64_t init_index = 0;
+    std::vector<GateRec> queue;
+    // device program buffers
+    KOp *d_ops = nullptr;
+    size_t d_ops_cap = 0;
+    uint32_t *d_perm = nullptr;
+    size_t d_perm_cap = 0;
+    KOp *h_ops = nullptr;
+    size_t h_ops_cap = 0;
+    uint32_t *h_perm = nullptr;
+    size_t h_perm_cap = 0;
+    cudaEvent_t upload_done = nullptr;
+    double2 **d_shard_ptrs = nullptr;
+    double *d_red = nullptr;
+    size_t d_red_cap = 0;
+    // options
+    bool fusion = true, timing = false;
+    int max_scan = 1 << 30;
+    int64_t chunk_mb = 1024;
+    // stats
+    qsim_stats stats{};
+    std::vector<TimedRange> ranges;
+    std::vector<cudaEvent_t> event_pool;
+    bool poisoned = false;
+    std::string last_error;
+};
+
+#define FAIL(ctx, code, ...)                                            \
+    do {                                                                \
+        char _b[512];                                                   \
+        snprintf(_b, sizeof(_b), __VA_ARGS__);                          \
+        if (ctx) (ctx)->last_error = _b;                                \
+        return code;                                                    \
+    } while (0)
+
+#define CK(ctx, call)                                                                               \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess) {                                                                    \
+            (ctx)->poisoned = true;                                                                 \
+            FAIL(ctx, QSIM_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+        }                                                                                           \
+    } while (0)
+
+#define CKN(ctx, call)                                                                            \
+    do {                                                                                          \
+        ncclResult_t _r = (call);                                                                 \
+        if (_r != ncclSuccess) {                                                                  \
+            (ctx)->poisoned = true;                                                               \
+            FAIL(ctx, QSIM_ERR_COMM, "%s: %s", #call, ncclGetErrorString(_r));                    \
+        }                                                                                         \
+    } while (0)
+
+#define LAUNCHED(ctx)                                                                         \
+    do {                                                                                      \
+        cudaError_t _e = cudaGetLastError();                                                  \
+        if (_e != cudaSuccess) {                                                              \
+            (ctx)->poisoned = true;                                                           \
+            FAIL(ctx, QSIM_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(_e));            \
+        }                                                                                     \
+        (ctx)->stats.kernel_launches++;                                                       \
+    } while (0)
+
+static int ilog2(int P)
+{
+    int g = 0;
+    while ((1 << g) < P) g++;
+    return g;
+}
+
+// ------------------------------------------------------------ validation
+static bool unitary(const qsim_c128 *u)
+{
+    // U^dag U - I, entries (i,j) = sum_k conj(U_ki) U_kj
+    double r[2][2][2];
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++) {
+            double re = 0, im = 0;
+            for (int k = 0; k < 2; k++) {
+                const qsim_c128 a = u[2 * k + i], b = u[2 * k + j];
+                re += a.re * b.re + a.im * b.im;
+                im += a.re * b.im - a.im * b.re;
+            }
+            r[i][j][0] = re - (i == j ? 1.0 : 0.0);
+            r[i][j][1] = im;
+        }
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++)
+            if (std::fabs(r[i][j][0]) > 1e-12 || std::fabs(r[i][j][1]) > 1e-12 || !std::isfinite(r[i][j][0]))
+                return false;
+    return true;
+}
+
+static qsim_status to_rec(qsim_ctx ctx, int n, const qsim_gate &g, GateRec &r)
+{
+    auto inr = [&](int q) { return q >= 0 && q < n; };
+    r = GateRec();
+    if (g.kind == QSIM_G_1Q || g.kind == QSIM_G_CTRL) {
+        int nc = g.kind == QSIM_G_1Q ? 0 : g.n_controls;
+        if (nc < 0 || nc > QSIM_MAX_CONTROLS) FAIL(ctx, QSIM_ERR_ARG, "n_controls=%d out of [0,%d]", nc, QSIM_MAX_CONTROLS);
+        if (!inr(g.target)) FAIL(ctx, QSIM_ERR_QUBIT_RANGE, "target %d outside [0,%d)", g.target, n);
+        uint64_t seen = 1ULL << g.target;
+        for (int i = 0; i < nc; i++) {
+            int c = g.controls[i];
+            if (!inr(c)) FAIL(ctx, QSIM_ERR_QUBIT_RANGE, "control %d outside [0,%d)", c, n);
+            if ((seen >> c) & 1) FAIL(ctx, QSIM_ERR_DUP_QUBIT, "qubit %d repeated", c);
+            seen |= 1ULL << c;
+            r.controls.push_back(c);
+        }
+        if (!unitary(g.u)) FAIL(ctx, QSIM_ERR_NOT_UNITARY, "matrix is not unitary within 1e-12");
+        r.kind = GK_U2;
+        r.target = g.target;
+        for (int k = 0; k < 4; k++) { r.u[2 * k] = g.u[k].re; r.u[2 * k + 1] = g.u[k].im; }
+    } else if (g.kind == QSIM_G_PERM) {
+        int nt = g.n_targets, nc = g.n_controls;
+        if (nt < 1 || nt > QSIM_MAX_PERM_TARGETS) FAIL(ctx, QSIM_ERR_ARG, "n_targets=%d out of [1,%d]", nt, QSIM_MAX_PERM_TARGETS);
+        if (nt > n) FAIL(ctx, QSIM_ERR_ARG, "n_targets > n");
+        if (nc < 0 || nc > QSIM_MAX_CONTROLS) FAIL(ctx, QSIM_ERR_ARG, "n_controls=%d out of range", nc);
+        if (!g.perm) FAIL(ctx, QSIM_ERR_ARG, "perm is NULL");
+        uint64_t seen = 0;
+        for (int i = 0; i < nt; i++) {
+            int t = g.targets[i];
+            if (!inr(t)) FAIL(ctx, QSIM_ERR_QUBIT_RANGE, "target %d outside [0,%d)", t, n);
+            if ((seen >> t) & 1) FAIL(ctx, QSIM_ERR_DUP_QUBIT, "qubit %d repeated", t);
+            seen |= 1ULL << t;
+            r.targets.push_back(t);
+        }
+        for (int i = 0; i < nc; i++) {
+            int c = g.controls[i];
+            if (!inr(c)) FAIL(ctx, QSIM_ERR_QUBIT_RANGE, "control %d outside [0,%d)", c, n);
+            if ((seen >> c) & 1) FAIL(ctx, QSIM_ERR_DUP_QUBIT, "qubit %d repeated", c);
+            seen |= 1ULL << c;
+            r.controls.push_back(c);
+        }
+        const uint32_t W = 1u << nt;
+        std::vector<char> hit(W, 0);
+        r.perm.assign(g.perm, g.perm + W);
+        for (uint32_t w = 0; w < W; w++) {
+            if (g.perm[w] >= W || hit[g.perm[w]]) FAIL(ctx, QSIM_ERR_NOT_PERMUTATION, "perm is not a bijection of [0,%u)", W);
+            hit[g.perm[w]] = 1;
+        }
+        r.kind = GK_PERM;
+    } else if (g.kind == QSIM_G_SWAP) {
+        int a = g.targets[0], b = g.targets[1];
+        if (!inr(a) || !inr(b)) FAIL(ctx, QSIM_ERR_QUBIT_RANGE, "swap qubit outside [0,%d)", n);
+        if (a == b) FAIL(ctx, QSIM_ERR_DUP_QUBIT, "swap of qubit %d with itself", a);
+        r.kind = GK_SWAP;
+        r.targets = {a, b};
+    } else {
+        FAIL(ctx, QSIM_ERR_ARG, "unknown gate kind %d", g.kind);
+    }
+    classify(r);
+    return QSIM_OK;
+}
+
+// ------------------------------------------------------------ helpers
+static cudaEvent_t ev_get(qsim_ctx c)
+{
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct RangeGuard {
+    qsim_ctx c;
+    int cat;
+    uint64_t bytes;
+    cudaEvent_t a = nullptr;
+    RangeGuard(qsim_ctx c_, int cat_, uint64_t bytes_) : c(c_), cat(cat_), bytes(bytes_)
+    {
+        if (c->timing) {
+            a = ev_get(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~RangeGuard()
+    {
+        if (c->timing) {
+            cudaEvent_t b = ev_get(c);
+            cudaEventRecord(b, c->stream);
+            c->ranges.push_back({a, b, cat, bytes});
+        }
+    }
+};
+
+static qsim_status collect_timing(qsim_ctx c)
+{
+    if (c->ranges.empty()) return QSIM_OK;
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (auto &r : c->ranges) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        switch (r.cat) {
+        case 0: c->stats.pass_ms += ms; c->stats.pass_amp_bytes += r.bytes; break;
+        case 1: c->stats.generic_ms += ms; break;
+        case 2: c->stats.perm_ms += ms; break;
+        case 3: c->stats.exchange_ms += ms; break;
+        default: c->stats.reduce_ms += ms; break;
+        }
+        c->event_pool.push_back(r.a);
+        c->event_pool.push_back(r.b);
+    }
+    c->ranges.clear();
+    return QSIM_OK;
+}
+
+template <class T>
+static qsim_status ensure_dev(qsim_ctx c, T *&p, size_t &cap, size_t need)
+{
+    if (need <= cap) return QSIM_OK;
+    size_t nc = std::max(need, cap * 2);
+    if (p) {
+        CK(c, cudaStreamSynchronize(c->stream));
+        CK(c, cudaFree(p));
+        p = nullptr;
+    }
+    cudaError_t e = cudaMalloc((void **)&p, nc * sizeof(T));
+    if (e != cudaSuccess) { cap = 0; FAIL(c, QSIM_ERR_OOM, "cudaMalloc(%zu): %s", nc * sizeof(T), cudaGetErrorString(e)); }
+    cap = nc;
+    return QSIM_OK;
+}
+
+template <class T>
+static qsim_status ensure_host(qsim_ctx c, T *&p, size_t &cap, size_t need)
+{
+    if (need <= cap) return QSIM_OK;
+    size_t nc = std::max(need, cap * 2);
+    if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));
+    if (p) CK(c, cudaFreeHost(p));
+    p = nullptr;
+    CK(c, cudaMallocHost((void **)&p, nc * sizeof(T)));
+    cap = nc;
+    return QSIM_OK;
+}
+
+static inline uint64_t rank_sub(uint64_t r, const std::vector<int> &gpos, int M)
+{
+    uint64_t v = 0;
+    for (size_t i = 0; i < gpos.size(); i++) v |= ((r >> (gpos[i] - M)) & 1) << i;
+    return v;
+}
+static inline uint64_t with_sub(uint64_t r, const std::vector<int> &gpos, int M, uint64_t v)
+{
+    for (size_t i = 0; i < gpos.size(); i++) {
+        uint64_t b = 1ULL << (gpos[i] - M);
+        r = ((v >> i) & 1) ? (r | b) : (r & ~b);
+    }
+    return r;
+}
+
+// ------------------------------------------------------------ exchange
+static qsim_status exec_exchange(qsim_ctx c, const Step &s)
+{
+    const int K = (int)s.lpos.size(), M = c->M;
+    if (K == 0) return QSIM_OK;
+    const uint64_t chunk = 1ULL << (M - K);
+    const uint64_t nval = 1ULL << K;
+    RangeGuard rg(c, 3, 0);
+    c->stats.exchanges++;
+    if (c->transport == QSIM_TRANSPORT_VIRTUAL) {
+        for (uint64_t r = 0; r < (uint64_t)c->P; r++) {
+            const uint64_t my = rank_sub(r, s.gpos, M);
+            for (uint64_t v = 0; v < nval; v++) {
+                if (v == my) continue;
+                const uint64_t peer = with_sub(r, s.gpos, M, v);
+                if (peer < r) continue;
+                launch_swap_blocks(c->shards[r], c->shards[peer], M, K, s.lpos.data(), v, my, c->stream);
+                LAUNCHED(c);
+            }
+        }
+        c->stats.exchange_bytes += (nval - 1) * chunk * 16;
+        return QSIM_OK;
+    }
+    if (c->transport != QSIM_TRANSPORT_NCCL) FAIL(c, QSIM_ERR_STATE, "exchange without a multi-shard transport");
+    // NCCL: every rank trades chunk v with the peer whose global sub-bits are v
+    const uint64_t my = rank_sub((uint64_t)c->rank, s.gpos, M);
+    bool contiguous = true;
+    {
+        std::vector<int> l = s.lpos;
+        std::sort(l.begin(), l.end());
+        for (int i = 0; i < K; i++)
+            if (l[i] != M - K + i) contiguous = false;
+    }
+    const uint64_t npeer = nval - 1;
+    const uint64_t scratch_amps = c->scratch_bytes / sizeof(double2);
+    uint64_t piece = chunk;
+    const uint64_t limit_amps = (uint64_t)c->chunk_mb * (1ULL << 20) / sizeof(double2);
+    while (piece > 1 && (piece * npeer * (contiguous ? 1 : 2) > scratch_amps || piece > limit_amps)) piece >>= 1;
+    if (piece * npeer * (contiguous ? 1 : 2) > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for exchange");
+    double2 *recvb = c->scratch;
+    double2 *sendb = c->scratch + piece * npeer;
+    for (uint64_t off = 0; off < chunk; off += piece) {
+        if (!contiguous) {
+            uint64_t idx = 0;
+            for (uint64_t v = 0; v < nval; v++) {
+                if (v == my) continue;
+                launch_pack(c->shards[0], sendb + idx * piece, M, K, s.lpos.data(), v, off, piece, 0, c->stream);
+                LAUNCHED(c);
+                idx++;
+            }
+        }
+        CKN(c, ncclGroupStart());
+        uint64_t idx = 0;
+        for (uint64_t v = 0; v < nval; v++) {
+            if (v == my) continue;
+            const int peer = (int)with_sub((uint64_t)c->rank, s.gpos, M, v);
+            const double2 *src;
+            if (contiguous) {
+                uint64_t base = 0;
+                for (int i = 0; i < K; i++)
+                    if ((v >> i) & 1) base |= 1ULL << s.lpos[i];
+                src = c->shards[0] + base + off;
+            } else {
+                src = sendb + idx * piece;
+            }
+            CKN(c, ncclSend(src, piece * 2, ncclDouble, peer, c->comm, c->stream));
+            CKN(c, ncclRecv(recvb + idx * piece, piece * 2, ncclDouble, peer, c->comm, c->stream));
+            idx++;
+        }
+        CKN(c, ncclGroupEnd());
+        idx = 0;
+        for (uint64_t v = 0; v < nval; v++) {
+            if (v == my) continue;
+            launch_pack(c->shards[0], recvb + idx * piece, M, K, s.lpos.data(), v, off, piece, 1, c->stream);
+            LAUNCHED(c);
+            idx++;
+        }
+    }
+    c->stats.exchange_bytes += npeer * chunk * 16;
+    return QSIM_OK;
+}
+
+// ------------------------------------------------------------ flush
+static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
+{
+    size_t nops = 0, nperm = 0;
+    for (Step &s : steps) {
+        if (s.type == ST_PASS) {
+            s.pass.op_begin = (int)nops;
+            nops += s.ops.size();
+        } else if (s.type == ST_PERM) {
+            nperm += s.perm.size();
+        }
+    }
+    if (nops == 0 && nperm == 0) return QSIM_OK;
+    qsim_status st;
+    if ((st = ensure_host(c, c->h_ops, c->h_ops_cap, nops + 1)) != QSIM_OK) return st;
+    if ((st = ensure_host(c, c->h_perm, c->h_perm_cap, nperm + 1)) != QSIM_OK) return st;
+    if ((st = ensure_dev(c, c->d_ops, c->d_ops_cap, nops + 1)) != QSIM_OK) return st;
+    if ((st = ensure_dev(c, c->d_perm, c->d_perm_cap, nperm + 1)) != QSIM_OK) return st;
+    if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));  // staging reuse
+    size_t o = 0, p = 0;
+    for (Step &s : steps) {
+        if (s.type == ST_PASS) {
+            std::memcpy(c->h_ops + o, s.ops.data(), s.ops.size() * sizeof(KOp));
+            o += s.ops.size();
+        } else if (s.type == ST_PERM) {
+            std::memcpy(c->h_perm + p, s.perm.data(), s.perm.size() * sizeof(uint32_t));
+            s.t = (int)p;  // perm offset
+            p += s.perm.size();
+        }
+    }
+    if (nops) CK(c, cudaMemcpyAsync(c->d_ops, c->h_ops, nops * sizeof(KOp), cudaMemcpyHostToDevice, c->stream));
+    if (nperm) CK(c, cudaMemcpyAsync(c->d_perm, c->h_perm, nperm * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (!c->upload_done) CK(c, cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
+    CK(c, cudaEventRecord(c->upload_done, c->stream));
+    return QSIM_OK;
+}
+
+static int local_ranks(qsim_ctx c, int i) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? i : c->rank; }
+static int n_local(qsim_ctx c) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? c->P : 1; }
+
+static qsim_status exec_perm(qsim_ctx c, const Step &s)
+{
+    PermDesc d{};
+    const int M = c->M, t = (int)s.ptargets.size();
+    int tb = std::min(kTileBits, M);
+    if (tb < t) tb = t;
+    d.M = M;
+    d.t = t;
+    d.tile_bits = tb;
+    d.perm_offset = s.t;
+    bool used[64] = {false};
+    for (int i = 0; i < t; i++) { d.tile_pos[i] = s.ptargets[i]; used[s.ptargets[i]] = true; }
+    int nb = t;
+    for (int p = 0; p < M && nb < tb; p++)
+        if (!used[p]) { d.tile_pos[nb++] = p; used[p] = true; }
+    int srt[kTileBits];
+    for (int i = 0; i < tb; i++) srt[i] = d.tile_pos[i];
+    std::sort(srt, srt + tb);
+    for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
+    d.n_inst = 1ULL << (M - tb);
+    for (int b = 0; b < 64; b++) {
+        if (!((s.cm >> b) & 1)) continue;
+        int tl = -1;
+        for (int i = 0; i < tb; i++)
+            if (d.tile_pos[i] == b) tl = i;
+        if (tl >= 0) { d.m_ctrl_tile |= 1u << tl; d.v_ctrl_tile |= 1u << tl; }
+        else { d.m_ctrl_out |= 1ULL << b; d.v_ctrl_out |= 1ULL << b; }
+    }
+    RangeGuard rg(c, 2, 0);
+    for (int i = 0; i < n_local(c); i++) {
+        d.rank_bits = (uint64_t)local_ranks(c, i) << M;
+        launch_perm(d, c->shards[i], c->d_perm, c->stream);
+        LAUNCHED(c);
+        c->stats.perm_launches++;
+    }
+    return QSIM_OK;
+}
+
+static qsim_status flush(qsim_ctx c)
+{
+    if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
+    if (!c->init_pending && c->queue.empty()) return QSIM_OK;
+    if (!c->init_pending && !c->initialized) FAIL(c, QSIM_ERR_STATE, "gates queued before qsim_init_basis");
+    auto t0 = std::chrono::steady_clock::now();
+    if (c->init_pending) {
+        c->planner->choose_initial_layout(c->queue);
+        uint64_t phys = 0;
+        for (int q = 0; q < c->n; q++)
+            if ((c->init_index >> q) & 1) phys |= 1ULL << c->planner->phys_of[q];
+        const uint64_t owner = phys >> c->M, li = phys & ((1ULL << c->M) - 1);
+        for (int i = 0; i < n_local(c); i++) {
+            const bool mine = (uint64_t)local_ranks(c, i) == owner;
+            launch_init(c->shards[i], 1ULL << c->M, mine ? (int64_t)li : -1, c->stream);
+            LAUNCHED(c);
+        }
+        c->init_pending = false;
+        c->initialized = true;
+    }
+    std::vector<Step> steps;
+    PlanOptions opt;
+    opt.fusion = c->fusion;
+    opt.max_scan = c->max_scan;
+    c->planner->plan(c->queue, opt, steps);
+    c->queue.clear();
+    c->stats.flushes++;
+    c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    qsim_status st = upload_program(c, steps);
+    if (st != QSIM_OK) return st;
+    const int M = c->M;
+    for (const Step &s : steps) {
+        switch (s.type) {
+        case ST_PASS: {
+            RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
+            for (int i = 0; i < n_local(c); i++) {
+                PassDesc d = s.pass;
+                d.rank_bits = (uint64_t)local_ranks(c, i) << M;
+                launch_pass(d, c->shards[i], c->d_ops, c->stream);
+                LAUNCHED(c);
+                c->stats.passes++;
+            }
+            break;
+        }
+        case ST_GENERIC:
+        case ST_PHASE: {
+            RangeGuard rg(c, 1, 0);
+            for (int i = 0; i < n_local(c); i++) {
+                const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
+                if (s.type == ST_GENERIC)
+                    launch_gate_generic(c->shards[i], M, rb, s.t, s.cm, s.cv, s.code, s.m, c->stream);
+                else
+                    launch_phase_generic(c->shards[i], M, rb, s.cm, s.cv, s.m[0], s.m[1], c->stream);
+                LAUNCHED(c);
+                c->stats.generic_launches++;
+            }
+            break;
+        }
+        case ST_PERM:
+            if ((st = exec_perm(c, s)) != QSIM_OK) return st;
+            break;
+        case ST_EXCHANGE:
+            if ((st = exec_exchange(c, s)) != QSIM_OK) return st;
+            break;
+        case ST_RELABEL:
+            c->stats.relabels++;
+            break;
+        }
+    }
+    return QSIM_OK;
+}
+
+// ------------------------------------------------------------ ABI
+extern "C" {
+
+const char *qsim_status_str(qsim_status s)
+{
+    switch (s) {
+    case QSIM_OK: return "QSIM_OK";
+    case QSIM_ERR_ARG: return "QSIM_ERR_ARG";
+    case QSIM_ERR_QUBIT_RANGE: return "QSIM_ERR_QUBIT_RANGE";
+    case QSIM_ERR_DUP_QUBIT: return "QSIM_ERR_DUP_QUBIT";
+    case QSIM_ERR_NOT_UNITARY: return "QSIM_ERR_NOT_UNITARY";
+    case QSIM_ERR_NOT_PERMUTATION: return "QSIM_ERR_NOT_PERMUTATION";
+    case QSIM_ERR_OOM: return "QSIM_ERR_OOM";
+    case QSIM_ERR_CUDA: return "QSIM_ERR_CUDA";
+    case QSIM_ERR_COMM: return "QSIM_ERR_COMM";
+    case QSIM_ERR_STATE: return "QSIM_ERR_STATE";
+    case QSIM_ERR_UNSUPPORTED: return "QSIM_ERR_UNSUPPORTED";
+    }
+    return "unknown";
+}
+
+const char *qsim_last_error(qsim_ctx ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+size_t qsim_scratch_bytes(int n_qubits, int n_ranks)
+{
+    if (n_ranks <= 1 || n_qubits < 2) return 0;
+    const int M = n_qubits - ilog2(n_ranks);
+    const size_t shard = (size_t)16 << M;
+    return std::min<size_t>(shard, (size_t)4 << 30);
+}
+
+qsim_status qsim_get_unique_id(void *out128)
+{
+    if (!out128) return QSIM_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return QSIM_ERR_COMM;
+    std::memcpy(out128, &id, sizeof(id));
+    return QSIM_OK;
+}
+
+qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
+{
+    if (!cfg || !out) return QSIM_ERR_ARG;
+    *out = nullptr;
+    const int n = cfg->n_qubits, P = cfg->n_ranks;
+    if (n < 1 || n > 62) return QSIM_ERR_QUBIT_RANGE;
+    if (P < 1 || P > 64 || (P & (P - 1))) return QSIM_ERR_ARG;
+    const int G = ilog2(P);
+    if (n - G < 1) return QSIM_ERR_ARG;
+    if (cfg->transport == QSIM_TRANSPORT_LOCAL && P != 1) return QSIM_ERR_ARG;
+    if (cfg->transport < 0 || cfg->transport > 2) return QSIM_ERR_ARG;
+    if (cfg->transport == QSIM_TRANSPORT_NCCL && (cfg->rank < 0 || cfg->rank >= P)) return QSIM_ERR_ARG;
+    qsim_ctx c = new qsim_ctx_s();
+    c->n = n;
+    c->P = P;
+    c->G = G;
+    c->M = n - G;
+    c->rank = cfg->transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
+    c->transport = cfg->transport;
+    c->planner = new Planner(n, G);
+    auto bail = [&](qsim_status s) {
+        qsim_destroy(c);
+        return s;
+    };
+    const size_t shard_bytes = (size_t)16 << c->M;
+    const int nsh = cfg->transport == QSIM_TRANSPORT_VIRTUAL ? P : 1;
+    bool any_null = false;
+    for (int i = 0; i < nsh; i++) any_null |= cfg->shards[i] == nullptr;
+    c->own_shards = any_null;
+    for (int i = 0; i < nsh; i++) {
+        double2 *p = (double2 *)cfg->shards[i];
+        if (any_null) {
+            if (cudaMalloc((void **)&p, shard_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                c->shards.resize(i);
+                return bail(QSIM_ERR_OOM);
+            }
+        } else if ((uintptr_t)p % 256) {
+            return bail(QSIM_ERR_ARG);
+        }
+        c->shards.push_back(p);
+    }
+    if (cfg->stream) {
+        c->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(QSIM_ERR_CUDA);
+        c->own_stream = true;
+    }
+    if (cfg->transport == QSIM_TRANSPORT_NCCL) {
+        c->scratch = (double2 *)cfg->scratch;
+        c->scratch_bytes = cfg->scratch_bytes;
+        if (!c->scratch) {
+            c->scratch_bytes = qsim_scratch_bytes(n, P);
+            if (cudaMalloc((void **)&c->scratch, c->scratch_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return bail(QSIM_ERR_OOM);
+            }
+            c->own_scratch = true;
+        }
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        if (ncclCommInitRank(&c->comm, P, id, cfg->rank) != ncclSuccess) return bail(QSIM_ERR_COMM);
+    }
+    if (cudaMalloc((void **)&c->d_shard_ptrs, sizeof(double2 *) * nsh) != cudaSuccess) return bail(QSIM_ERR_OOM);
+    if (cudaMemcpy(c->d_shard_ptrs, c->shards.data(), sizeof(double2 *) * nsh, cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(QSIM_ERR_CUDA);
+    *out = c;
+    return QSIM_OK;
+}
+
+qsim_status qsim_create(int n_qubits, int n_gpus, qsim_ctx *out)
+{
+    if (n_gpus != 1) return QSIM_ERR_ARG;
+    qsim_config cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.n_qubits = n_qubits;
+    cfg.n_ranks = 1;
+    cfg.transport = QSIM_TRANSPORT_LOCAL;
+    return qsim_create_ext(&cfg, out);
+}
+
+qsim_status qsim_destroy(qsim_ctx c)
+{
+    if (!c) return QSIM_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->own_shards)
+        for (double2 *p : c->shards) cudaFree(p);
+    if (c->own_scratch) cudaFree(c->scratch);
+    if (c->d_ops) cudaFree(c->d_ops);
+    if (c->d_perm) cudaFree(c->d_perm);
+    if (c->d_red) cudaFree(c->d_red);
+    if (c->d_shard_ptrs) cudaFree(c->d_shard_ptrs);
+    if (c->h_ops) cudaFreeHost(c->h_ops);
+    if (c->h_perm) cudaFreeHost(c->h_perm);
+    if (c->upload_done) cudaEventDestroy(c->upload_done);
+    for (auto &r : c->ranges) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c->planner;
+    delete c;
+    return QSIM_OK;
+}
+
+#define GUARD(c)                                                                          \
+    do {                                                                                  \
+        if (!(c)) return QSIM_ERR_ARG;                                                    \
+        if ((c)->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", (c)->last_error.c_str()); \
+    } while (0)
+
+qsim_status qsim_init_basis(qsim_ctx c, uint64_t index)
+{
+    GUARD(c);
+    if (c->n < 64 && index >> c->n) FAIL(c, QSIM_ERR_ARG, "index %llu >= 2^%d", (unsigned long long)index, c->n);
+    // discard queued gates: the state is being re-initialised
+    c->queue.clear();
+    delete c->planner;
+    c->planner = new Planner(c->n, c->G);
+    c->init_pending = true;
+    c->init_index = index;
+    return QSIM_OK;
+}
+
+static qsim_status enqueue(qsim_ctx c, const qsim_gate &g)
+{
+    GateRec r;
+    qsim_status s = to_rec(c, c->n, g, r);
+    if (s != QSIM_OK) return s;
+    if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "gate before qsim_init_basis");
+    r.id = (int)c->queue.size();
+    c->queue.push_back(std::move(r));
+    c->stats.gates++;
+    return QSIM_OK;
+}
+
+qsim_status qsim_apply_1q(qsim_ctx c, int q, const qsim_c128 u[4])
+{
+    GUARD(c);
+    if (!u) return QSIM_ERR_ARG;
+    qsim_gate g;
+    std::memset(&g, 0, sizeof(g));
+    g.kind = QSIM_G_1Q;
+    g.target = q;
+    for (int k = 0; k < 4; k++) g.u[k] = u[k];
+    return enqueue(c, g);
+}
+
+qsim_status qsim_apply_controlled(qsim_ctx c, const int *controls, int n_controls, int target, const qsim_c128 u[4])
+{
+    GUARD(c);
+    if (!u || (n_controls > 0 && !controls) || n_controls < 0 || n_controls > QSIM_MAX_CONTROLS) return QSIM_ERR_ARG;
+    qsim_gate g;
+    std::memset(&g, 0, sizeof(g));
+    g.kind = QSIM_G_CTRL;
+    g.target = target;
+    g.n_controls = n_controls;
+    for (int i = 0; i < n_controls; i++) g.controls[i] = controls[i];
+    for (int k = 0; k < 4; k++) g.u[k] = u[k];
+    return enqueue(c, g);
+}
+
+qsim_status qsim_apply_perm(qsim_ctx c, const int *controls, int n_controls, const int *targets, int n_targets,
+                            const uint32_t *perm)
+{
+    GUARD(c);
+    if ((n_controls > 0 && !controls) || n_controls < 0 || n_controls > QSIM_MAX_CONTROLS) return QSIM_ERR_ARG;
+    if (!targets || n_targets < 1 || n_targets > QSIM_MAX_PERM_TARGETS) return QSIM_ERR_ARG;
+    qsim_gate g;
+    std::memset(&g, 0, sizeof(g));
+    g.kind = QSIM_G_PERM;
+    g.n_controls = n_controls;
+    g.n_targets = n_targets;
+    for (int i = 0; i < n_controls; i++) g.controls[i] = controls[i];
+    for (int i = 0; i < n_targets; i++) g.targets[i] = targets[i];
+    g.perm = perm;
+    return enqueue(c, g);
+}
+
+qsim_status qsim_apply_swap(qsim_ctx c, int a, int b)
+{
+    GUARD(c);
+    qsim_gate g;
+    std::memset(&g, 0, sizeof(g));
+    g.kind = QSIM_G_SWAP;
+    g.targets[0] = a;
+    g.targets[1] = b;
+    return enqueue(c, g);
+}
+
+qsim_status qsim_run_circuit(qsim_ctx c, const qsim_gate *gates, size_t n_gates)
+{
+    GUARD(c);
+    if (n_gates && !gates) return QSIM_ERR_ARG;
+    if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "gate before qsim_init_basis");
+    std::vector<GateRec> recs(n_gates);
+    for (size_t i = 0; i < n_gates; i++) {
+        qsim_status s = to_rec(c, c->n, gates[i], recs[i]);
+        if (s != QSIM_OK) {
+            std::string e = c->last_error;
+            FAIL(c, s, "gate %zu: %s", i, e.c_str());
+        }
+    }
+    for (auto &r : recs) {
+        r.id = (int)c->queue.size();
+        c->queue.push_back(std::move(r));
+    }
+    c->stats.gates += n_gates;
+    return QSIM_OK;
+}
+
+qsim_status qsim_remap(qsim_ctx c, const int *local_qubits, const int *global_qubits, int K)
+{
+    GUARD(c);
+    if (K < 0 || K > c->G || (K && (!local_qubits || !global_qubits))) FAIL(c, QSIM_ERR_ARG, "K=%d out of [0,%d]", K, c->G);
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    uint64_t seen = 0;
+    std::vector<int> lq, gq;
+    for (int i = 0; i < K; i++) {
+        int l = local_qubits[i], g = global_qubits[i];
+        if (l < 0 || l >= c->n || g < 0 || g >= c->n) FAIL(c, QSIM_ERR_QUBIT_RANGE, "qubit outside range");
+        if (((seen >> l) & 1) || ((seen >> g) & 1) || l == g) FAIL(c, QSIM_ERR_DUP_QUBIT, "qubit repeated");
+        seen |= (1ULL << l) | (1ULL << g);
+        if (c->planner->phys_of[l] >= c->M) FAIL(c, QSIM_ERR_ARG, "qubit %d is not local", l);
+        if (c->planner->phys_of[g] < c->M) FAIL(c, QSIM_ERR_ARG, "qubit %d is not nonlocal", g);
+        lq.push_back(l);
+        gq.push_back(g);
+    }
+    std::vector<Step> steps;
+    c->planner->remap(lq, gq, steps);
+    for (auto &st : steps)
+        if ((s = exec_exchange(c, st)) != QSIM_OK) return s;
+    return QSIM_OK;
+}
+
+qsim_status qsim_sync(qsim_ctx c)
+{
+    GUARD(c);
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    CK(c, cudaStreamSynchronize(c->stream));
+    return collect_timing(c);
+}
+
+qsim_status qsim_get_layout(qsim_ctx c, int *out)
+{
+    GUARD(c);
+    if (!out) return QSIM_ERR_ARG;
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    for (int q = 0; q < c->n; q++) out[q] = c->planner->phys_of[q];
+    return QSIM_OK;
+}
+
+// cross-shard sum of per-shard host vectors in fixed rank order
+static qsim_status sum_over_ranks(qsim_ctx c, std::vector<std::vector<double>> &per, double *out, size_t len)
+{
+    if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1) {
+        qsim_status s;
+        if ((s = ensure_dev(c, c->d_red, c->d_red_cap, len * (c->P + 1))) != QSIM_OK) return s;
+        CK(c, cudaMemcpyAsync(c->d_red, per[0].data(), len * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CKN(c, ncclAllGather(c->d_red, c->d_red + len, len, ncclDouble, c->comm, c->stream));
+        std::vector<double> all(len * c->P);
+        CK(c, cudaMemcpyAsync(all.data(), c->d_red + len, len * c->P * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        for (size_t j = 0; j < len; j++) {
+            double a = 0.0;
+            for (int r = 0; r < c->P; r++) a += all[r * len + j];
+            out[j] = a;
+        }
+        return QSIM_OK;
+    }
+    for (size_t j = 0; j < len; j++) {
+        double a = 0.0;
+        for (size_t r = 0; r < per.size(); r++) a += per[r][j];
+        out[j] = a;
+    }
+    return QSIM_OK;
+}
+
+static qsim_status probabilities_impl(qsim_ctx c, const int *qubits, int k, double *out)
+{
+    if (k < 0 || k > 24 || (k && !qubits) || !out) FAIL(c, QSIM_ERR_ARG, "bad qubit list (k=%d)", k);
+    if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
+    uint64_t seen = 0;
+    for (int j = 0; j < k; j++) {
+        if (qubits[j] < 0 || qubits[j] >= c->n) FAIL(c, QSIM_ERR_QUBIT_RANGE, "qubit %d", qubits[j]);
+        if ((seen >> qubits[j]) & 1) FAIL(c, QSIM_ERR_DUP_QUBIT, "qubit %d repeated", qubits[j]);
+        seen |= 1ULL << qubits[j];
+    }
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    const int M = c->M, cb = std::min(12, M);
+    ProbsDesc d{};
+    d.cb = cb;
+    d.M = M;
+    d.k = k;
+    uint32_t listed_low = 0;
+    uint64_t listed_chunk = 0;
+    for (int j = 0; j < k; j++) {
+        const int p = c->planner->phys_of[qubits[j]];
+        d.pos[j] = p;
+        if (p < cb) { d.lowpos[d.k_low++] = p; listed_low |= 1u << p; }
+        else if (p < M) listed_chunk |= 1ULL << (p - cb);
+    }
+    d.red_mask = ((1u << cb) - 1) & ~listed_low;
+    for (int b = 0; b < M - cb; b++)
+        if (!((listed_chunk >> b) & 1)) d.freepos[d.n_free++] = b;
+    const uint64_t nch = 1ULL << (M - cb);
+    const size_t partial_len = (size_t)nch << d.k_low, B = (size_t)1 << k;
+    if (partial_len * 8 > ((size_t)8 << 30)) FAIL(c, QSIM_ERR_UNSUPPORTED, "marginal partial buffer too large");
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, partial_len + B)) != QSIM_OK) return s;
+    std::vector<std::vector<double>> per(n_local(c), std::vector<double>(B));
+    RangeGuard rg(c, 4, 0);
+    for (int i = 0; i < n_local(c); i++) {
+        d.rank = (uint64_t)local_ranks(c, i);
+        launch_probs(c->shards[i], d, c->d_red, c->d_red + partial_len, c->stream);
+        LAUNCHED(c);
+        CK(c, cudaMemcpyAsync(per[i].data(), c->d_red + partial_len, B * sizeof(double), cudaMemcpyDeviceToHost,
+                              c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
+    return sum_over_ranks(c, per, out, B);
+}
+
+qsim_status qsim_probabilities(qsim_ctx c, const int *qubits, int k, double *out)
+{
+    GUARD(c);
+    return probabilities_impl(c, qubits, k, out);
+}
+
+qsim_status qsim_expectations(qsim_ctx c, double *out)
+{
+    GUARD(c);
+    if (!out) return QSIM_ERR_ARG;
+    if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    const int M = c->M, cb = std::min(12, M), n = c->n;
+    const uint64_t nch = 1ULL << (M - cb);
+    const size_t plen = nch * (cb + 1);
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, plen + M + 1)) != QSIM_OK) return s;
+    std::vector<std::vector<double>> per(n_local(c), std::vector<double>(n, 0.0));
+    std::vector<double> phys(M + 1);
+    RangeGuard rg(c, 4, 0);
+    for (int i = 0; i < n_local(c); i++) {
+        launch_expect(c->shards[i], M, c->d_red, c->d_red + plen, c->stream);
+        LAUNCHED(c);
+        CK(c, cudaMemcpyAsync(phys.data(), c->d_red + plen, (M + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        const uint64_t r = (uint64_t)local_ranks(c, i);
+        for (int q = 0; q < n; q++) {
+            const int p = c->planner->phys_of[q];
+            per[i][q] = p < M ? phys[p] : (((r >> (p - M)) & 1) ? phys[M] : 0.0);
+        }
+    }
+    return sum_over_ranks(c, per, out, n);
+}
+
+qsim_status qsim_measure(qsim_ctx c, const int *qubits, int k, uint64_t seed, uint64_t n_shots, uint64_t *out)
+{
+    GUARD(c);
+    if (n_shots && !out) return QSIM_ERR_ARG;
+    const size_t B = (size_t)1 << (k < 0 ? 0 : k);
+    std::vector<double> p(B);
+    qsim_status s = probabilities_impl(c, qubits, k, p.data());
+    if (s != QSIM_OK) return s;
+    const size_t need = 2 * B + (n_shots + 1) / 2 + 1;
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
+    double *dp = c->d_red, *dc = c->d_red + B;
+    uint64_t *dout = (uint64_t *)(c->d_red + 2 * B);
+    CK(c, cudaMemcpyAsync(dp, p.data(), B * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_sample(dp, k, seed, n_shots, dc, dout, c->stream);
+    LAUNCHED(c);
+    if (n_shots) CK(c, cudaMemcpyAsync(out, dout, n_shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return QSIM_OK;
+}
+
+qsim_status qsim_get_amplitudes(qsim_ctx c, uint64_t first, uint64_t count, qsim_c128 *host_out)
+{
+    GUARD(c);
+    if (count && !host_out) return QSIM_ERR_ARG;
+    if (c->n < 64 && (first > (1ULL << c->n) || count > (1ULL << c->n) - first)) FAIL(c, QSIM_ERR_ARG, "range outside [0,2^n)");
+    if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
+    qsim_status s = flush(c);
+    if (s != QSIM_OK) return s;
+    const uint64_t piece = 1ULL << 22;
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, 2 * piece)) != QSIM_OK) return s;
+    const int virt = c->transport == QSIM_TRANSPORT_VIRTUAL;
+    for (uint64_t off = 0; off < count; off += piece) {
+        const uint64_t cnt = std::min(piece, count - off);
+        double2 *dout = (double2 *)c->d_red;
+        launch_gather(dout, first + off, cnt, c->d_shard_ptrs, virt, c->rank, c->M, c->n, c->planner->phys_of.data(),
+                      c->stream);
+        LAUNCHED(c);
+        if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1)
+            CKN(c, ncclAllReduce(dout, dout, cnt * 2, ncclDouble, ncclSum, c->comm, c->stream));
+        CK(c, cudaMemcpyAsync(host_out + off, dout, cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
+    return QSIM_OK;
+}
+
+qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
+{
+    GUARD(c);
+    if (!key) return QSIM_ERR_ARG;
+    std::string k(key);
+    if (k == "fusion") c->fusion = value != 0;
+    else if (k == "timing") c->timing = value != 0;
+    else if (k == "max_scan") c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30);
+    else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
+    return QSIM_OK;
+}
+
+qsim_status qsim_get_stats(qsim_ctx c, qsim_stats *out)
+{
+    GUARD(c);
+    if (!out) return QSIM_ERR_ARG;
+    qsim_status s = collect_timing(c);
+    if (s != QSIM_OK) return s;
+    *out = c->stats;
+    return QSIM_OK;
+}
+
+qsim_status qsim_reset_stats(qsim_ctx c)
+{
+    GUARD(c);
+    qsim_status s = collect_timing(c);
+    if (s != QSIM_OK) return s;
+    std::memset(&c->stats, 0, sizeof(c->stats));
+    return QSIM_OK;
+}
+
+qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates, int fusion, char *buf,
+                           size_t buf_bytes)
+{
+    if (n_qubits < 1 || n_qubits > 62 || n_ranks < 1 || (n_ranks & (n_ranks - 1)) || !buf) return QSIM_ERR_ARG;
+    const int G = ilog2(n_ranks);
+    if (n_qubits - G < 1) return QSIM_ERR_ARG;
+    std::vector<GateRec> recs(n_gates);
+    for (size_t i = 0; i < n_gates; i++) {
+        qsim_status s = to_rec(nullptr, n_qubits, gates[i], recs[i]);
+        if (s != QSIM_OK) return s;
+        recs[i].id = (int)i;
+    }
+    Planner P(n_qubits, G);
+    P.choose_initial_layout(recs);
+    std::string init = "{\"initial_phys_of\":[";
+    for (int q = 0; q < n_qubits; q++) init += (q ? "," : "") + std::to_string(P.phys_of[q]);
+    init += "],\"plan\":";
+    std::vector<Step> steps;
+    PlanOptions opt;
+    opt.fusion = fusion != 0;
+    P.plan(recs, opt, steps);
+    std::string js = init + plan_to_json(P, steps) + "}";
+    if (js.size() + 1 > buf_bytes) return QSIM_ERR_ARG;
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+    return QSIM_OK;
+}
+
+}  // extern "C"

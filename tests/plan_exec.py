@@ -1,0 +1,84 @@
+"""Execute a qsim_plan_json plan on ONE numpy array in PHYSICAL index order
+(test infrastructure).  Checks the planner's reordering, sigma bookkeeping,
+relabels and exchanges (as index-bit interchanges, Eq. onequbitchange) on
+the CPU, independently of the CUDA kernels."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+
+def _apply(psi, idx, code, t, cm, cv, m):
+    sel = (idx & cm) == cv
+    if code == 3:  # PHASE
+        psi[sel] *= complex(m[0], m[1])
+        return
+    tb = 1 << t
+    i0 = idx[sel & ((idx & tb) == 0)]
+    i1 = i0 | tb
+    x, y = psi[i0].copy(), psi[i1].copy()
+    if code == 2:  # exact swap
+        psi[i0], psi[i1] = y, x
+        return
+    u00, u01 = complex(m[0], m[1]), complex(m[2], m[3])
+    u10, u11 = complex(m[4], m[5]), complex(m[6], m[7])
+    psi[i0] = u00 * x + u01 * y
+    psi[i1] = u10 * x + u11 * y
+
+
+def _swap_bits(idx, a, b):
+    ba, bb = (idx >> a) & 1, (idx >> b) & 1
+    return idx ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
+
+
+def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
+    d = json.loads(js)
+    plan = d["plan"]
+    phys0 = d["initial_phys_of"]
+    idx = np.arange(1 << n, dtype=np.int64)
+    psi = np.zeros(1 << n, dtype=np.complex128)
+    p0 = sum(((init_index >> q) & 1) << phys0[q] for q in range(n))
+    psi[p0] = 1.0
+    for st in plan["steps"]:
+        ty = st["type"]
+        if ty == "pass":
+            for op in st["ops"]:
+                if op["code"] == 4:
+                    continue
+                _apply(psi, idx, op["code"], op["t"], op["cm"], op["cv"], op["m"])
+        elif ty == "generic":
+            _apply(psi, idx, st["code"], st["t"], st["cm"], st["cv"], st["m"])
+        elif ty == "phase":
+            _apply(psi, idx, 3, -1, st["cm"], st["cv"], st["m"])
+        elif ty == "perm":
+            g = gates[st["gate"]]
+            T = st["targets"]
+            cm = st["cm"]
+            new = psi.copy()
+            w = np.zeros_like(idx)
+            for b, p in enumerate(T):
+                w |= ((idx >> p) & 1) << b
+            pw = np.asarray(g.perm, dtype=np.int64)[w]
+            dest = idx.copy()
+            for b, p in enumerate(T):
+                dest = (dest & ~(1 << p)) | (((pw >> b) & 1) << p)
+            sel = (idx & cm) == cm
+            new[dest[sel]] = psi[idx[sel]]
+            psi = new
+        elif ty == "exchange":
+            j = idx
+            for a, b in zip(st["lpos"], st["gpos"]):
+                j = _swap_bits(j, a, b)
+            new = np.empty_like(psi)
+            new[j] = psi
+            psi = new
+        elif ty == "relabel":
+            pass
+        else:
+            raise ValueError(ty)
+    fin = plan["final_phys_of"]
+    phys = np.zeros_like(idx)
+    for q in range(n):
+        phys |= ((idx >> q) & 1) << fin[q]
+    return psi[phys]

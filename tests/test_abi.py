@@ -1,0 +1,129 @@
+"""C-ABI library checks and host-side planner logic (-m "not gpu")."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.plan_exec import run_plan
+from workloads import circuits as C
+from workloads import gates as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_quant_ph_0608239_b200 import build
+    build.build()
+    import paper_quant_ph_0608239_b200 as P
+    return P
+
+
+def test_library_exports_every_header_symbol(pkg):
+    hdr = open(os.path.join(ROOT, "include", "qsim.h")).read()
+    names = set(re.findall(r"\b(qsim_[a-z_0-9]+)\s*\(", hdr))
+    assert len(names) >= 20
+    lib = ctypes.CDLL(pkg.LIB_PATH)
+    for nme in sorted(names):
+        assert hasattr(lib, nme), nme
+    assert names == set(pkg.EXPORTS)
+
+
+def test_library_is_sm100a(pkg):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pkg.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings(pkg):
+    lib = pkg._native.lib() if hasattr(pkg, "_native") else None
+    from paper_quant_ph_0608239_b200 import _native as N
+    lib = N.lib()
+    for i, nme in enumerate(N.STATUS):
+        assert lib.qsim_status_str(i).decode() == nme
+
+
+def _plan(pkg, n, P, gates, fusion=True):
+    return pkg.plan_json(n, P, gates, fusion)
+
+
+def test_validation_codes(pkg):
+    from paper_quant_ph_0608239_b200 import QsimError
+    cases = [
+        ([G.one_q(0, (1, 1, 0, 1))], 4),                          # not unitary
+        ([G.ctrl([1], 1, G.PAULI_X)], 3),                          # control == target
+        ([G.one_q(9, G.H)], 2),                                    # out of range
+        ([G.perm_gate((), (0, 1), np.array([0, 1, 1, 2]))], 5),   # not a bijection
+        ([G.perm_gate((0,), (0, 1), np.arange(4))], 3),            # control among targets
+        ([G.swap(2, 2)], 3),
+    ]
+    for gates, code in cases:
+        with pytest.raises(QsimError) as e:
+            _plan(pkg, 4, 1, gates)
+        assert e.value.status == code
+
+
+def _check_plan(pkg, oracle_mod, n, P, init, gates, fusion=True):
+    js = _plan(pkg, n, P, gates, fusion)
+    got = run_plan(js, n, init, gates)
+    o = oracle_mod.Oracle(n)
+    o.init_basis(init)
+    o.run(gates)
+    ref = o.amplitudes()
+    assert np.max(np.abs(got - ref)) <= 1e-12
+    return json.loads(js)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_plan_random_brickwork(pkg, oracle_mod, P):
+    n = 14
+    gates = C.random_brickwork(n, 6, seed=11)
+    d = _check_plan(pkg, oracle_mod, n, P, 0, gates)
+    steps = d["plan"]["steps"]
+    npass = sum(s["type"] == "pass" for s in steps)
+    assert npass < len(gates) / 4  # fusion actually fuses
+    if P > 1:
+        assert any(s["type"] == "exchange" for s in steps)
+
+
+def test_plan_qft_sharded(pkg, oracle_mod):
+    w = C.qft_basis(14, 12345)
+    d = _check_plan(pkg, oracle_mod, 14, 4, w.init, w.gates)
+    assert sum(s["type"] == "relabel" for s in d["plan"]["steps"]) == 7
+
+
+def test_plan_shor_sharded(pkg, oracle_mod):
+    w = C.shor_order_finding(35, 3, 8, 6)
+    _check_plan(pkg, oracle_mod, w.n, 2, w.init, w.gates)
+    _check_plan(pkg, oracle_mod, w.n, 1, w.init, w.gates)
+
+
+def test_plan_chain_three_global(pkg, oracle_mod):
+    gates = C.random_chain(15, 2, seed=5, sweep=True)
+    _check_plan(pkg, oracle_mod, 15, 8, 0, gates)
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_plan_generic_small(pkg, oracle_mod, P):
+    n = 8
+    rng = G.SplitMix64(4)
+    gates = C.random_brickwork(n, 3, seed=2) + [G.toffoli(0, 5, 7), G.ctrl([7, 1], 3, G.haar_u2(rng)),
+                                                G.perm_gate((6,), (0, 3, 7), np.array([3, 1, 4, 0, 7, 6, 5, 2])),
+                                                G.swap(1, 6), G.cphase(7, 2, 0.4)]
+    _check_plan(pkg, oracle_mod, n, P, 37, gates, fusion=True)
+    _check_plan(pkg, oracle_mod, n, P, 37, gates, fusion=False)
+
+
+def test_plan_controls_and_diagonals_on_global(pkg, oracle_mod):
+    """Diagonal gates and controls on nonlocal qubits need no exchange
+    (the optimisation P:623-628 and P:753-756 describe)."""
+    n, P = 14, 4
+    gates = [G.one_q(q, G.H) for q in range(12)]  # qubits 12,13 are never targeted -> global
+    gates += [G.cphase(13, 2, 0.3), G.ctrl([12], 5, G.haar_u2(G.SplitMix64(1))), G.one_q(13, G.R(0.9)),
+              G.toffoli(12, 13, 0)]
+    d = _check_plan(pkg, oracle_mod, n, P, 0, gates)
+    assert not any(s["type"] == "exchange" for s in d["plan"]["steps"])

@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle (-m gpu).
+
+Bar (BASELINE.json north_star): max |delta amplitude| <= 1e-11,
+|1 - ||psi||^2| <= 1e-12, measured basis states / integer outcomes exact
+(sampling ties within 1e-12 of a CDF boundary excluded, reading R14).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tests import pins
+from workloads import circuits as C
+from workloads import gates as G
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+NORM_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_quant_ph_0608239_b200 as pkg
+    return pkg
+
+
+def gpu_run(P, n, init, gates, ranks=1, fusion=True, transport=None):
+    tp = transport or ("local" if ranks == 1 else "virtual")
+    sim = P.QSim(n, n_ranks=ranks, transport=tp)
+    sim.set_option("fusion", int(fusion))
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    return sim
+
+
+def oracle_run(oracle_mod, n, init, gates):
+    o = oracle_mod.Oracle(n)
+    o.init_basis(init)
+    o.run(gates)
+    return o
+
+
+def assert_parity(sim, o, n):
+    got = sim.get_amplitudes()
+    ref = o.amplitudes()
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL, err
+    assert abs(1 - sim.norm()) <= NORM_TOL
+    return got
+
+
+def kitchen_sink(n, seed):
+    """Every gate kind on every position: Haar layer, H/X/Y/Xbar/Ybar/R, CNOT,
+    CP, controlled-V, Toffoli, 2-control U2, perms, swaps."""
+    rng = G.SplitMix64(seed)
+    r = np.random.default_rng(seed)
+    gates = [G.one_q(q, G.haar_u2(rng)) for q in range(n)]
+    named = [G.H, G.X, G.Y, G.XBAR, G.YBAR, G.R(0.37)]
+    for q in range(n):
+        gates.append(G.one_q(q, named[q % len(named)]))
+        c = (q + 1 + q % 3) % n
+        gates.append(G.cnot(c, q))
+        gates.append(G.cphase((q + 5) % n, q, 0.1 * (q + 1)))
+        gates.append(G.ctrl([(q + 2) % n], q, G.V(0.3 + q)))
+        a, b = (q + 3) % n, (q + 7) % n
+        if len({a, b, q}) == 3:
+            gates.append(G.toffoli(a, b, q))
+            gates.append(G.ctrl([a, b], q, G.haar_u2(rng)))
+        gates.append(G.one_q(q, G.haar_u2(rng)))
+    for t0 in range(0, n - 2, 3):
+        tg = [t0, (t0 + 4) % n, (t0 + 9) % n]
+        if len(set(tg)) == 3:
+            ctl = [x for x in [(t0 + 1) % n] if x not in tg]
+            gates.append(G.perm_gate(ctl, tg, r.permutation(8).astype(np.uint32)))
+    gates.append(G.swap(0, n - 1))
+    gates.append(G.one_q(0, G.haar_u2(rng)))
+    gates.append(G.swap(2, 5))
+    gates += [G.one_q(q, G.haar_u2(rng)) for q in range(n)]
+    return gates
+
+
+@pytest.mark.parametrize("n", [11, 12, 13, 16])
+@pytest.mark.parametrize("fusion", [True, False])
+def test_every_gate_every_position(P, oracle_mod, n, fusion):
+    gates = kitchen_sink(n, seed=n)
+    sim = gpu_run(P, n, 5, gates, fusion=fusion)
+    assert_parity(sim, oracle_run(oracle_mod, n, 5, gates), n)
+
+
+@pytest.mark.parametrize("ranks,n", [(2, 14), (4, 15), (8, 16), (8, 12), (4, 9)])
+def test_every_gate_sharded_virtual(P, oracle_mod, ranks, n):
+    gates = kitchen_sink(n, seed=100 + n)
+    sim = gpu_run(P, n, 3, gates, ranks=ranks)
+    assert_parity(sim, oracle_run(oracle_mod, n, 3, gates), n)
+    st = sim.stats()
+    assert st["exchanges"] > 0
+
+
+def test_tiny_states(P, oracle_mod):
+    for n, ranks in [(1, 1), (2, 1), (2, 2), (3, 4), (5, 1)]:
+        gates = [G.one_q(q, G.haar_u2(G.SplitMix64(q))) for q in range(n)]
+        if n >= 2:
+            gates += [G.cnot(0, 1), G.cphase(1, 0, 0.5)]
+        sim = gpu_run(P, n, (1 << n) - 1, gates, ranks=ranks)
+        assert_parity(sim, oracle_run(oracle_mod, n, (1 << n) - 1, gates), n)
+
+
+def test_config1_adder(P, oracle_mod):
+    w = C.config1_adder()
+    sim = gpu_run(P, w.n, w.init, w.gates)
+    got = assert_parity(sim, oracle_run(oracle_mod, w.n, w.init, w.gates), w.n)
+    p = np.abs(got) ** 2
+    assert int(np.argmax(p)) == w.meta["expect_index"]
+    assert p[w.meta["expect_index"]] >= 1 - 1e-12
+    shots = sim.measure(list(range(w.n)), seed=7, shots=64)
+    assert np.all(shots == w.meta["expect_index"])
+
+
+def test_adder_all_inputs_m5(P):
+    m = 5
+    gates = C.qft_adder([list(range(m)), list(range(m, 2 * m))])
+    for a in range(0, 32, 3):
+        for b in range(0, 32, 5):
+            sim = gpu_run(P, 2 * m, a + (b << m), gates)
+            pb = sim.probabilities(list(range(m, 2 * m)))
+            assert pb[(a + b) % 32] >= 1 - 1e-12
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4, 8])
+def test_random_brickwork_small(P, oracle_mod, ranks):
+    n = 18
+    gates = C.random_brickwork(n, 12, seed=2)
+    sim = gpu_run(P, n, 0, gates, ranks=ranks)
+    assert_parity(sim, oracle_run(oracle_mod, n, 0, gates), n)
+
+
+def test_config2_full(P, oracle_mod):
+    """BASELINE config 2 at full size (24 q, depth 40, 1420 gates): full state."""
+    w = C.config2_random()
+    sim = gpu_run(P, w.n, w.init, w.gates)
+    o = oracle_run(oracle_mod, w.n, w.init, w.gates)
+    assert_parity(sim, o, w.n)
+    ex = sim.expectations()
+    assert np.max(np.abs(ex - o.expectations())) <= 1e-12
+
+
+def test_config2_echo_and_determinism(P):
+    w = C.config2_random()
+    sim = gpu_run(P, w.n, 0, w.gates)
+    a1 = sim.get_amplitudes(0, 1 << 16)
+    sim2 = gpu_run(P, w.n, 0, w.gates)
+    a2 = sim2.get_amplitudes(0, 1 << 16)
+    assert np.array_equal(a1, a2)  # bitwise deterministic
+    sim.run_circuit(C.inverse(w.gates))
+    amps = sim.get_amplitudes(0, 1 << 12)
+    assert abs(amps[0] - 1) < 1e-11 and np.max(np.abs(amps[1:])) < 1e-11
+
+
+def test_shor_small(P, oracle_mod):
+    w = C.shor_order_finding(35, 3, 10, 6)
+    sim = gpu_run(P, w.n, w.init, w.gates)
+    o = oracle_run(oracle_mod, w.n, w.init, w.gates)
+    assert_parity(sim, o, w.n)
+    ctl = list(range(10))
+    pg = sim.probabilities(ctl)
+    assert np.max(np.abs(pg - pins.shor_pk(w.meta["r"], 10))) < 1e-12
+    shots = sim.measure(ctl, seed=11, shots=500)
+    ref, tie = o.measure(ctl, seed=11, shots=500)
+    ok = tie == 0
+    assert np.array_equal(shots[ok], ref[ok])
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_shor_sharded(P, oracle_mod, ranks):
+    w = C.shor_order_finding(21, 2, 9, 5)
+    sim = gpu_run(P, w.n, w.init, w.gates, ranks=ranks)
+    assert_parity(sim, oracle_run(oracle_mod, w.n, w.init, w.gates), w.n)
+
+
+def test_config3_full(P, oracle_mod):
+    """BASELINE config 3 (28 q, N=899): the control-register marginal equals
+    the corrected closed form (reading 1/8) and samples match the oracle's
+    sampler applied to that closed form with the same seed."""
+    w = C.config3_shor()
+    sim = gpu_run(P, w.n, w.init, w.gates)
+    ctl = list(range(18))
+    pg = sim.probabilities(ctl)
+    pk = pins.shor_pk(w.meta["r"], 18)
+    assert np.max(np.abs(pg - pk)) <= 1e-10
+    assert abs(1 - sim.norm()) <= NORM_TOL
+    from oracle.oracle import sample_from
+    shots = sim.measure(ctl, seed=3, shots=2000)
+    ref, tie = sample_from(pk, 18, 3, 2000)
+    ok = tie == 0
+    assert ok.sum() > 1900 and np.array_equal(shots[ok], ref[ok])
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4, 8])
+def test_qft_closed_form(P, ranks):
+    n, x0 = 20, 0xABCDE
+    w = C.qft_basis(n, x0)
+    sim = gpu_run(P, n, x0, w.gates, ranks=ranks)
+    got = sim.get_amplitudes()
+    assert np.max(np.abs(got - pins.qft_closed_form(n, x0))) <= TOL
+
+
+def test_config4_qft32_one_gpu(P):
+    """BASELINE config 4 (32 q, 64 GiB) on one GPU: sampled blocks vs the
+    closed form with integer phase reduction."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < (70 << 30):
+        pytest.skip("needs ~70 GB free")
+    w = C.config4_qft()
+    sim = gpu_run(P, 32, w.init, w.gates)
+    rng = np.random.default_rng(4)
+    x0 = w.meta["x0"]
+    for start in rng.integers(0, (1 << 32) - 4096, size=16):
+        got = sim.get_amplitudes(int(start), 4096)
+        k = np.arange(int(start), int(start) + 4096, dtype=np.uint64)
+        ph = (np.uint64(x0) * k) & np.uint64((1 << 32) - 1)
+        ref = np.exp(2j * np.pi * ph.astype(np.float64) / 2.0 ** 32) / 2.0 ** 16
+        assert np.max(np.abs(got - ref)) <= TOL
+    assert abs(1 - sim.norm()) <= NORM_TOL
+    sim.close()
+
+
+def test_config5_family_sharded(P, oracle_mod):
+    """config 5's circuit family (H all, Haar layers + CNOT chain, sweep) on
+    8 virtual shards (3 nonlocal qubits)."""
+    n = 18
+    gates = C.random_chain(n, 3, seed=5, sweep=True)
+    sim = gpu_run(P, n, 0, gates, ranks=8)
+    o = oracle_run(oracle_mod, n, 0, gates)
+    assert_parity(sim, o, n)
+    assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-12
+
+
+@pytest.mark.parametrize("ranks", [1, 4])
+def test_readouts(P, oracle_mod, ranks):
+    n = 16
+    gates = C.random_brickwork(n, 5, seed=8)
+    sim = gpu_run(P, n, 0, gates, ranks=ranks)
+    o = oracle_run(oracle_mod, n, 0, gates)
+    for qs in ([], [0], [15], [3, 14], [13, 0, 7], list(range(10)), [15, 14, 1, 2, 12, 8]):
+        assert np.max(np.abs(sim.probabilities(qs) - o.probabilities(qs))) <= 1e-13
+    assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-13
+    qs = [2, 9, 15, 0]
+    shots = sim.measure(qs, seed=1234, shots=5000)
+    ref, tie = o.measure(qs, seed=1234, shots=5000)
+    assert np.array_equal(shots[tie == 0], ref[tie == 0])
+
+
+def _table_blocks():
+    blocks, cur = [], None
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "tables_I_II.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        if line.startswith("TABLE"):
+            parts = line.split()
+            cur = {"table": parts[1], "remap": parts[-1], "rows": []}
+            blocks.append(cur)
+        else:
+            cur["rows"].append([int(x, 2) for x in line.split()])
+    return blocks
+
+
+def test_paper_tables_I_II_placement(P):
+    """Tables I and II: after the paper's local<->nonlocal
+    interchanges (Eqs. onequbitchange, twoqubitchange0-5) rank R, address A
+    holds exactly the printed a(x).  L=4, M=2, four virtual shards."""
+    blocks = _table_blocks()
+    for x in range(16):
+        sim = None
+        for b in blocks:
+            if b["remap"] == "-":
+                sim = P.QSim(4, n_ranks=4, transport="virtual")
+                sim.init_basis(x)
+                sim.sync()
+            else:
+                pairs = [p.split(":") for p in b["remap"].split(",")]
+                sim.remap([int(a) for a, _ in pairs], [int(g) for _, g in pairs])
+                sim.sync()
+            shards = [t.cpu().numpy().view(np.complex128) for t in sim.shard_tensors()]
+            where = [(r, a) for r in range(4) for a in range(4) if abs(shards[r][a]) > 0.5]
+            assert len(where) == 1
+            r, a = where[0]
+            assert b["rows"][a][r] == x, (b["table"], b["remap"], x, where)
+            assert abs(sim.get_amplitudes(x, 1)[0] - 1) == 0
+
+
+def test_remap_roundtrip_exact(P, oracle_mod):
+    n = 14
+    gates = C.random_brickwork(n, 4, seed=1)
+    sim = gpu_run(P, n, 0, gates, ranks=4)
+    before = sim.get_amplitudes()
+    lay = sim.layout()
+    glob = [q for q in range(n) if lay[q] >= n - 2]
+    loc = [q for q in range(n) if lay[q] < n - 2][:2]
+    sim.remap(loc, glob)
+    sim.remap(glob, loc)
+    assert np.array_equal(sim.get_amplitudes(), before)
+
+
+def test_errors_leave_state_untouched(P):
+    from paper_quant_ph_0608239_b200 import QsimError
+    n = 13
+    sim = gpu_run(P, n, 0, C.random_brickwork(n, 2, seed=3))
+    before = sim.get_amplitudes()
+    bad = [([G.one_q(0, (1, 1, 0, 1))], 4), ([G.cnot(3, 3)], 3), ([G.one_q(13, G.H)], 2),
+           ([G.perm_gate((), (0, 1), np.array([0, 0, 1, 2]))], 5)]
+    for gates, code in bad:
+        with pytest.raises(QsimError) as e:
+            sim.run_circuit(gates)
+        assert e.value.status == code
+    with pytest.raises(QsimError):
+        sim.probabilities([0, 0])
+    assert np.array_equal(sim.get_amplitudes(), before)
+    s2 = P.QSim(5)
+    with pytest.raises(QsimError) as e:
+        s2.norm()
+    assert e.value.name == "QSIM_ERR_STATE"
