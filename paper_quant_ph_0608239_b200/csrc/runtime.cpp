@@ -79,6 +79,7 @@ struct qsim_ctx_s {
     do {                                                                                            \
         cudaError_t _e = (call);                                                                    \
         if (_e != cudaSuccess) {                                                                    \
+            cudaGetLastError();                                                                     \
             (ctx)->poisoned = true;                                                                 \
             FAIL(ctx, QSIM_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
         }                                                                                           \
@@ -579,6 +580,7 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
     if (cfg->transport == QSIM_TRANSPORT_LOCAL && P != 1) return QSIM_ERR_ARG;
     if (cfg->transport < 0 || cfg->transport > 2) return QSIM_ERR_ARG;
     if (cfg->transport == QSIM_TRANSPORT_NCCL && (cfg->rank < 0 || cfg->rank >= P)) return QSIM_ERR_ARG;
+    cudaGetLastError();  // do not inherit a stale error of another context
     qsim_ctx c = new qsim_ctx_s();
     c->n = n;
     c->P = P;
@@ -934,7 +936,7 @@ qsim_status qsim_measure(qsim_ctx c, const int *qubits, int k, uint64_t seed, ui
     std::vector<double> p(B);
     qsim_status s = probabilities_impl(c, qubits, k, p.data());
     if (s != QSIM_OK) return s;
-    const size_t need = 2 * B + (n_shots + 1) / 2 + 1;
+    const size_t need = 2 * B + n_shots + 1;  // p, CDF (doubles) + outcomes (uint64)
     if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
     double *dp = c->d_red, *dc = c->d_red + B;
     uint64_t *dout = (uint64_t *)(c->d_red + 2 * B);
