@@ -23,6 +23,8 @@ constexpr int kTileBits = 12;
 constexpr int kTileAmps = 1 << kTileBits;
 constexpr int kPassThreads = 256;
 constexpr int kAmpsPerThread = 16;
+// ops of one pass travel in the kernel parameter block (<= 32 KB on sm_100)
+constexpr int kMaxPassOps = 240;
 
 enum OpCode : int32_t {
     OPC_U2 = 0,     // general complex 2x2 on target (REG or LANE role)

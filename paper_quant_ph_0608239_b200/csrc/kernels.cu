@@ -49,22 +49,21 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t v, int p)
 }
 
 // ---------------------------------------------------------------- k_pass
-template <int K, int CODE>
-__device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp *__restrict__ op, uint32_t mreg,
-                                          uint32_t vreg)
+template <int K, int CODE, bool PRED>
+__device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint32_t mreg, uint32_t vreg)
 {
     double2 u00, u01, u10, u11;
     if (CODE != OPC_XS) {
-        u00 = make_double2(op->m[0], op->m[1]);
-        u01 = make_double2(op->m[2], op->m[3]);
-        u10 = make_double2(op->m[4], op->m[5]);
-        u11 = make_double2(op->m[6], op->m[7]);
+        u00 = make_double2(op.m[0], op.m[1]);
+        u01 = make_double2(op.m[2], op.m[3]);
+        u10 = make_double2(op.m[4], op.m[5]);
+        u11 = make_double2(op.m[6], op.m[7]);
     }
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         const int i0 = ((p >> K) << (K + 1)) | (p & ((1 << K) - 1));
         const int i1 = i0 | (1 << K);
-        if ((i0 & mreg) != vreg) continue;
+        if (PRED && (i0 & mreg) != vreg) continue;
         const double2 x = a[i0], y = a[i1];
         if (CODE == OPC_XS) {
             a[i0] = y;
@@ -79,15 +78,63 @@ __device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp *__restric
     }
 }
 
-template <int CODE>
-__device__ __forceinline__ void reg_dispatch(double2 (&a)[16], const KOp *__restrict__ op, int k, uint32_t mreg,
-                                             uint32_t vreg)
+template <int CODE, bool PRED>
+__device__ __forceinline__ void reg_dispatch(double2 (&a)[16], const KOp &op, int k, uint32_t mreg, uint32_t vreg)
 {
     switch (k) {
-    case 0: reg_apply<0, CODE>(a, op, mreg, vreg); break;
-    case 1: reg_apply<1, CODE>(a, op, mreg, vreg); break;
-    case 2: reg_apply<2, CODE>(a, op, mreg, vreg); break;
-    default: reg_apply<3, CODE>(a, op, mreg, vreg); break;
+    case 0: reg_apply<0, CODE, PRED>(a, op, mreg, vreg); break;
+    case 1: reg_apply<1, CODE, PRED>(a, op, mreg, vreg); break;
+    case 2: reg_apply<2, CODE, PRED>(a, op, mreg, vreg); break;
+    default: reg_apply<3, CODE, PRED>(a, op, mreg, vreg); break;
+    }
+}
+
+template <bool PRED>
+__device__ __forceinline__ void reg_op(double2 (&a)[16], const KOp &op, int code, uint32_t mreg, uint32_t vreg)
+{
+    const int k = op.k;
+    if (code == OPC_XS) reg_dispatch<OPC_XS, PRED>(a, op, k, mreg, vreg);
+    else if (code == OPC_U2R) reg_dispatch<OPC_U2R, PRED>(a, op, k, mreg, vreg);
+    else reg_dispatch<OPC_U2, PRED>(a, op, k, mreg, vreg);
+}
+
+// LANE-role op: partner amplitude through warp shuffles; partners share the
+// predicate because a gate never controls on its own target bit.
+template <bool PRED>
+__device__ __forceinline__ void lane_op(double2 (&a)[16], const KOp &op, int code, int lane, bool tp, uint32_t mreg,
+                                        uint32_t vreg)
+{
+    const int kb = 1 << op.k;
+    const bool hi = (lane & kb) != 0;
+    if (code == OPC_XS) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            double2 p;
+            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+            if (!PRED || (tp && (i & mreg) == vreg)) a[i] = p;
+        }
+    } else if (code == OPC_U2R) {
+        const double cs = hi ? op.m[6] : op.m[0];
+        const double co = hi ? op.m[4] : op.m[2];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            double2 p;
+            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+            if (!PRED || (tp && (i & mreg) == vreg))
+                a[i] = make_double2(fma(cs, a[i].x, co * p.x), fma(cs, a[i].y, co * p.y));
+        }
+    } else {
+        const double2 cs = hi ? make_double2(op.m[6], op.m[7]) : make_double2(op.m[0], op.m[1]);
+        const double2 co = hi ? make_double2(op.m[4], op.m[5]) : make_double2(op.m[2], op.m[3]);
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            double2 p;
+            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
+            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
+            if (!PRED || (tp && (i & mreg) == vreg)) a[i] = cmac2(cs, a[i], co, p);
+        }
     }
 }
 
@@ -95,9 +142,17 @@ __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (
 
 __device__ __forceinline__ int pick3(int x, int a0, int a1, int a2) { return x == 0 ? a0 : (x == 1 ? a1 : a2); }
 
-__global__ void __launch_bounds__(kPassThreads, 2)
-    k_pass(const __grid_constant__ PassDesc d, double2 *__restrict__ st, const KOp *__restrict__ ops)
+template <int CAP>
+struct PassParams {
+    PassDesc d;
+    KOp ops[CAP];
+};
+
+template <int CAP, int MINB>
+__global__ void __launch_bounds__(kPassThreads, MINB)
+    k_pass(const __grid_constant__ PassParams<CAP> P, double2 *__restrict__ st)
 {
+    const PassDesc &d = P.d;
     extern __shared__ double2 sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -129,10 +184,9 @@ __global__ void __launch_bounds__(kPassThreads, 2)
         }
     }
 
-    const KOp *__restrict__ prog = ops + d.op_begin;
     for (int o = 0; o < d.n_ops; o++) {
-        const KOp *__restrict__ op = prog + o;
-        const int code = op->code;
+        const KOp &op = P.ops[o];
+        const int code = op.code;
         if (code == OPC_TRANS) {
             // registers -> swizzled smem with the current roles, then back with the new roles
             {
@@ -142,7 +196,7 @@ __global__ void __launch_bounds__(kPassThreads, 2)
                 for (int i = 0; i < 16; i++) sm[swz(sl | (i & 1) | ((i >> 1) << sh))] = a[i];
             }
             __syncthreads();
-            const int ta = op->ta, tb = op->tb;
+            const int ta = op.ta, tb = op.tb;
             const int xa = pick3(ta, rREG, rLANE, rWARP), xb = pick3(tb, rREG, rLANE, rWARP);
             if (ta == ROLE_REG) rREG = xb; else if (ta == ROLE_LANE) rLANE = xb; else rWARP = xb;
             if (tb == ROLE_REG) rREG = xa; else if (tb == ROLE_LANE) rLANE = xa; else rWARP = xa;
@@ -155,59 +209,30 @@ __global__ void __launch_bounds__(kPassThreads, 2)
             __syncthreads();
             continue;
         }
-        const bool tp = ((lane & op->mlane) == op->vlane) && ((warp & op->mwarp) == op->vwarp) &&
-                        ((gcta & op->mout) == op->vout);
-        const uint32_t mreg = op->mreg, vreg = op->vreg;
+        const bool tp = ((lane & op.mlane) == op.vlane) && ((warp & op.mwarp) == op.vwarp) &&
+                        ((gcta & op.mout) == op.vout);
+        const uint32_t mreg = op.mreg, vreg = op.vreg;
         if (code == OPC_PHASE) {
             if (!tp) continue;
-            const double2 f = make_double2(op->m[0], op->m[1]);
+            const double2 f = make_double2(op.m[0], op.m[1]);
+            if (mreg == 0) {
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if ((i & mreg) == vreg) a[i] = cmul(f, a[i]);
+                for (int i = 0; i < 16; i++) a[i] = cmul(f, a[i]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    if ((i & mreg) == vreg) a[i] = cmul(f, a[i]);
+            }
             continue;
         }
-        if (op->role == ROLE_REG) {
+        if (op.role == ROLE_REG) {
             if (!tp) continue;
-            const int k = op->k;
-            if (code == OPC_XS) reg_dispatch<OPC_XS>(a, op, k, mreg, vreg);
-            else if (code == OPC_U2R) reg_dispatch<OPC_U2R>(a, op, k, mreg, vreg);
-            else reg_dispatch<OPC_U2>(a, op, k, mreg, vreg);
+            if (mreg == 0) reg_op<false>(a, op, code, 0, 0);
+            else reg_op<true>(a, op, code, mreg, vreg);
             continue;
         }
-        // LANE role: partner amplitude via shuffles (partners share the predicate)
-        if (!__any_sync(FULL, tp)) continue;
-        const int kb = 1 << op->k;
-        const bool hi = (lane & kb) != 0;
-        if (code == OPC_XS) {
-#pragma unroll
-            for (int i = 0; i < 16; i++) {
-                double2 p;
-                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-                if (tp && (i & mreg) == vreg) a[i] = p;
-            }
-        } else if (code == OPC_U2R) {
-            const double cs = hi ? op->m[6] : op->m[0];
-            const double co = hi ? op->m[4] : op->m[2];
-#pragma unroll
-            for (int i = 0; i < 16; i++) {
-                double2 p;
-                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-                if (tp && (i & mreg) == vreg)
-                    a[i] = make_double2(fma(cs, a[i].x, co * p.x), fma(cs, a[i].y, co * p.y));
-            }
-        } else {
-            const double2 cs = hi ? make_double2(op->m[6], op->m[7]) : make_double2(op->m[0], op->m[1]);
-            const double2 co = hi ? make_double2(op->m[4], op->m[5]) : make_double2(op->m[2], op->m[3]);
-#pragma unroll
-            for (int i = 0; i < 16; i++) {
-                double2 p;
-                p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-                p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-                if (tp && (i & mreg) == vreg) a[i] = cmac2(cs, a[i], co, p);
-            }
-        }
+        if (__all_sync(FULL, tp) && mreg == 0) lane_op<false>(a, op, code, lane, true, 0, 0);
+        else if (__any_sync(FULL, tp)) lane_op<true>(a, op, code, lane, tp, mreg, vreg);
     }
 
     offsets();
@@ -221,21 +246,40 @@ __global__ void __launch_bounds__(kPassThreads, 2)
     }
 }
 
-void launch_pass(const PassDesc &d, double2 *st, const KOp *ops, cudaStream_t s)
+template <int CAP, int MINB>
+static void launch_pass_cap(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s)
 {
     static bool attr = false;
-    const int smem = d.use_smem ? kTileAmps * (int)sizeof(double2) : 0;
     if (!attr) {
-        cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileAmps * (int)sizeof(double2));
+        cudaFuncSetAttribute(k_pass<CAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTileAmps * (int)sizeof(double2));
         attr = true;
     }
-    k_pass<<<(unsigned)d.n_inst, kPassThreads, smem, s>>>(d, st, ops);
+    PassParams<CAP> P;
+    P.d = d;
+    for (int i = 0; i < d.n_ops; i++) P.ops[i] = ops[i];
+    const int smem = d.use_smem ? kTileAmps * (int)sizeof(double2) : 0;
+    k_pass<CAP, MINB><<<(unsigned)d.n_inst, kPassThreads, smem, s>>>(P, st);
+}
+
+template <int MINB>
+static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s)
+{
+    if (d.n_ops <= 32) launch_pass_cap<32, MINB>(d, ops, st, s);
+    else if (d.n_ops <= 96) launch_pass_cap<96, MINB>(d, ops, st, s);
+    else launch_pass_cap<kMaxPassOps, MINB>(d, ops, st, s);
+}
+
+void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s)
+{
+    if (variant == 2) launch_pass_minb<2>(d, ops, st, s);
+    else launch_pass_minb<1>(d, ops, st, s);
 }
 
 int pass_regs_per_thread()
 {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, k_pass) != cudaSuccess) return -1;
+    if (cudaFuncGetAttributes(&fa, (k_pass<kMaxPassOps, 1>)) != cudaSuccess) return -1;
     return fa.numRegs;
 }
 

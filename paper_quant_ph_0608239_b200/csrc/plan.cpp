@@ -219,7 +219,9 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     uint64_t bN = 0, bD = 0;
     int scanned = 0;
     std::vector<std::pair<int, int>> relabels;
-    for (size_t i = first; i < gates.size() && scanned < opt.max_scan; i++) {
+    // each op may need a transpose in front of it: keep the lowered pass within kMaxPassOps
+    const size_t max_pops = kMaxPassOps / 2;
+    for (size_t i = first; i < gates.size() && scanned < opt.max_scan && pops.size() + 2 <= max_pops; i++) {
         if (done[i]) continue;
         scanned++;
         const GateRec &g = gates[i];

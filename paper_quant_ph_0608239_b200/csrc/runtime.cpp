@@ -58,6 +58,7 @@ struct qsim_ctx_s {
     // options
     bool fusion = true, timing = false;
     int max_scan = 1 << 30;
+    int pass_variant = 1;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
     // stats
     qsim_stats stats{};
@@ -381,15 +382,9 @@ static qsim_status exec_exchange(qsim_ctx c, const Step &s)
 // ------------------------------------------------------------ flush
 static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 {
-    size_t nops = 0, nperm = 0;
-    for (Step &s : steps) {
-        if (s.type == ST_PASS) {
-            s.pass.op_begin = (int)nops;
-            nops += s.ops.size();
-        } else if (s.type == ST_PERM) {
-            nperm += s.perm.size();
-        }
-    }
+    size_t nops = 0, nperm = 0;  // pass ops travel in the kernel parameter block
+    for (Step &s : steps)
+        if (s.type == ST_PERM) nperm += s.perm.size();
     if (nops == 0 && nperm == 0) return QSIM_OK;
     qsim_status st;
     if ((st = ensure_host(c, c->h_ops, c->h_ops_cap, nops + 1)) != QSIM_OK) return st;
@@ -494,7 +489,7 @@ static qsim_status flush(qsim_ctx c)
             for (int i = 0; i < n_local(c); i++) {
                 PassDesc d = s.pass;
                 d.rank_bits = (uint64_t)local_ranks(c, i) << M;
-                launch_pass(d, c->shards[i], c->d_ops, c->stream);
+                launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream);
                 LAUNCHED(c);
                 c->stats.passes++;
             }
@@ -982,6 +977,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30);
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else if (k == "pass_variant") c->pass_variant = value == 2 ? 2 : 1;
     else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
     return QSIM_OK;
 }

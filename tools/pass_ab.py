@@ -1,0 +1,43 @@
+"""A/B timing of engine options on config 2 (24 q, 1420 gates).
+usage: python tools/pass_ab.py key=v1,v2 [key2=...]"""
+import itertools
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_quant_ph_0608239_b200 import QSim, pack_gates  # noqa: E402
+from workloads import circuits as C  # noqa: E402
+
+w = C.config2_random()
+packed = pack_gates(w.gates)
+opts = {}
+for a in sys.argv[1:]:
+    k, v = a.split("=")
+    opts[k] = [int(x) for x in v.split(",")]
+keys = list(opts)
+sim = QSim(w.n)
+for combo in itertools.product(*[opts[k] for k in keys]) if keys else [()]:
+    for k, v in zip(keys, combo):
+        sim.set_option(k, v)
+    sim.set_option("timing", 1)
+    for _ in range(3):
+        sim.init_basis(0); sim.run_circuit(w.gates, packed=packed); sim.sync()
+    sim.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = 5
+    e0.record(sim.stream)
+    for _ in range(K):
+        sim.init_basis(0); sim.run_circuit(w.gates, packed=packed)
+        sim.sync()
+    e1.record(sim.stream)
+    torch.cuda.synchronize()
+    st = sim.stats()
+    ms = e0.elapsed_time(e1) / K
+    print(json.dumps({"opts": dict(zip(keys, combo)), "ms_per_step": round(ms, 3),
+                      "agu_per_s": len(w.gates) * 2 ** w.n / (ms / 1e3),
+                      "pass_ms_per_launch": st["pass_ms"] / max(1, st["passes"]),
+                      "passes_per_step": st["passes"] / K, "pass_GBps": st["pass_amp_bytes"] / (st["pass_ms"] / 1e3) / 1e9,
+                      "plan_ms": st["plan_ms"] / K}))
