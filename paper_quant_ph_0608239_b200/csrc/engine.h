@@ -3,17 +3,20 @@
 // with a plain C++ compiler.
 //
 // Fused tile pass.  A pass loads a tile of 2^12 amplitudes
-// spanned by 12 physical index bits -- bits 0,1,2 (so every warp access is
-// made of whole 128-B lines) plus 9 free local bits grouped in three
-// "triples" -- applies a list of gates to it, and stores it back: one HBM
-// read + write (32 B/amplitude) for many gates.  Thread coordinates:
-//   i    (4 bits, in-thread register index): bit0 <-> physical bit 0,
-//        bits1..3 <-> the triple in role REG;
-//   lane (5 bits): bits0,1 <-> physical bits 1,2; bits2..4 <-> triple in role LANE;
-//   warp (3 bits): triple in role WARP.
-// Gates whose target is in REG are applied in registers, in LANE with warp
-// shuffles; a target in WARP needs an OPC_TRANS (swap of the triples held
-// by two roles, through swizzled shared memory).
+// spanned by 12 physical index bits -- tile-local bits 0,1,2 are physical
+// bits 0,1,2 (so every warp access is made of whole 128-B lines), bits 3..11
+// are 9 free local bits -- applies a list of gates to it, and stores it back:
+// one HBM read + write (32 B/amplitude) for many gates.
+//
+// A "config" assigns the 12 tile-local bits to thread coordinates:
+//   i    (4 bits, in-thread register index) <-> r[0..3]
+//   lane (5 bits)                           <-> l[0..4]
+//   warp (3 bits)                           <-> w[0..2]
+// Gates are applied to register bits only (k = position in r); OPC_TRANS
+// moves the tile to another config through XOR-swizzled shared memory.
+// Load/store configs have r[0] = 0, l[0] = 1, l[1] = 2 (256-bit accesses of
+// amplitude pairs, whole 128-B lines per 4 lanes).
+// A config is packed in 12 nibbles: r0 r1 r2 r3 l0 l1 l2 l3 l4 w0 w1 w2.
 #pragma once
 #include <cstdint>
 
@@ -27,43 +30,49 @@ constexpr int kAmpsPerThread = 16;
 constexpr int kMaxPassOps = 240;
 
 enum OpCode : int32_t {
-    OPC_U2 = 0,     // general complex 2x2 on target (REG or LANE role)
+    OPC_U2 = 0,     // general complex 2x2 on register bit k
     OPC_U2R = 1,    // real 2x2 (imaginary parts zero), e.g. Hadamard
     OPC_XS = 2,     // exact [[0,1],[1,0]]: conditional swap (CNOT/Toffoli target)
     OPC_PHASE = 3,  // multiply by f = m[0] + i m[1] where the predicate holds
-    OPC_TRANS = 4   // swap the triples held by roles ta and tb
+    OPC_TRANS = 4   // re-layout the tile to config `cfg` through shared memory
 };
 
 enum Role : int32_t { ROLE_REG = 0, ROLE_LANE = 1, ROLE_WARP = 2, ROLE_OUT = 3 };
 
 // One kernel op (128 B).  Predicate: (i & mreg) == vreg && (lane & mlane) == vlane
 // && (warp & mwarp) == vwarp && (full_index & mout) == vout, where full_index =
-// (rank << M) | local index restricted to bits outside the tile.
+// (rank << M) | local index, restricted to bits outside the tile.
 struct alignas(16) KOp {
     int32_t code;
-    int32_t role;  // target role (REG / LANE) for U2-type ops
-    int32_t k;     // bit within the role
-    int32_t ta, tb;
+    int32_t k;  // register bit (0..3) of the target
     uint32_t mreg, vreg;
     uint32_t mlane, vlane;
     uint32_t mwarp, vwarp;
-    uint32_t pad;
     uint64_t mout, vout;
+    uint64_t cfg;  // OPC_TRANS: the new config
+    uint64_t pad;
     double m[8];  // u00r u00i u01r u01i u10r u10i u11r u11i ; PHASE: f = (m[0], m[1])
 };
 static_assert(sizeof(KOp) == 128, "KOp layout");
 
 struct PassDesc {
-    uint64_t rank_bits;      // rank << M
-    uint64_t n_inst;         // 2^(M-12) tile instances
+    uint64_t rank_bits;  // rank << M
+    uint64_t n_inst;     // 2^(M-12) tile instances
+    uint64_t cfg0;       // load config
     int32_t M;
-    int32_t op_begin;
     int32_t n_ops;
     int32_t use_smem;
-    int32_t tri[3][3];       // physical bit positions of triples 0,1,2
-    int32_t role_tri[3];     // initial triple index held by roles REG, LANE, WARP
-    int32_t tile_sorted[kTileBits];
+    int32_t pad;
+    int32_t tp[kTileBits];           // physical position of tile-local bit t
+    int32_t tile_sorted[kTileBits];  // tp sorted ascending (instance deposit)
 };
+
+#ifdef __CUDACC__
+#define QSB_HD __host__ __device__ __forceinline__
+#else
+#define QSB_HD inline
+#endif
+QSB_HD int cfg_nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
 
 // Controlled permutation of a target register (one launch per perm gate).
 struct PermDesc {

@@ -98,49 +98,58 @@ __device__ __forceinline__ void reg_op(double2 (&a)[16], const KOp &op, int code
     else reg_dispatch<OPC_U2, PRED>(a, op, k, mreg, vreg);
 }
 
-// LANE-role op: partner amplitude through warp shuffles; partners share the
-// predicate because a gate never controls on its own target bit.
-template <bool PRED>
-__device__ __forceinline__ void lane_op(double2 (&a)[16], const KOp &op, int code, int lane, bool tp, uint32_t mreg,
-                                        uint32_t vreg)
-{
-    const int kb = 1 << op.k;
-    const bool hi = (lane & kb) != 0;
-    if (code == OPC_XS) {
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            double2 p;
-            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-            if (!PRED || (tp && (i & mreg) == vreg)) a[i] = p;
-        }
-    } else if (code == OPC_U2R) {
-        const double cs = hi ? op.m[6] : op.m[0];
-        const double co = hi ? op.m[4] : op.m[2];
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            double2 p;
-            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-            if (!PRED || (tp && (i & mreg) == vreg))
-                a[i] = make_double2(fma(cs, a[i].x, co * p.x), fma(cs, a[i].y, co * p.y));
-        }
-    } else {
-        const double2 cs = hi ? make_double2(op.m[6], op.m[7]) : make_double2(op.m[0], op.m[1]);
-        const double2 co = hi ? make_double2(op.m[4], op.m[5]) : make_double2(op.m[2], op.m[3]);
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            double2 p;
-            p.x = __shfl_xor_sync(FULL, a[i].x, kb);
-            p.y = __shfl_xor_sync(FULL, a[i].y, kb);
-            if (!PRED || (tp && (i & mreg) == vreg)) a[i] = cmac2(cs, a[i], co, p);
-        }
-    }
-}
-
+// Shared-memory layout of a tile: 16-B unit of tile-local index s sits at
+// swz(s) = s ^ fold3(s >> 3).  Tile-local bit t lands in 16-B bank group
+// residue t mod 3, so a warp access whose 5 lane bits cover all three
+// residues touches every bank group exactly 4 times (4 wavefronts per
+// 512 B: conflict-free).  swz is GF(2)-linear: swz(a ^ b) = swz(a) ^ swz(b).
 __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
-__device__ __forceinline__ int pick3(int x, int a0, int a1, int a2) { return x == 0 ? a0 : (x == 1 ? a1 : a2); }
+// thread's lane/warp part of the smem index and the 4 register-bit parts
+__device__ __forceinline__ void smem_coords(uint64_t c, int lane, int warp, int &zt, int (&zr)[4])
+{
+    int st = 0;
+#pragma unroll
+    for (int j = 0; j < 5; j++) st |= ((lane >> j) & 1) << cfg_nib(c, 4 + j);
+#pragma unroll
+    for (int j = 0; j < 3; j++) st |= ((warp >> j) & 1) << cfg_nib(c, 9 + j);
+    zt = swz(st);
+#pragma unroll
+    for (int j = 0; j < 4; j++) zr[j] = swz(1 << cfg_nib(c, j));
+}
+
+template <int I>
+__device__ __forceinline__ int zsel(int zt, const int (&zr)[4])
+{
+    return zt ^ ((I & 1) ? zr[0] : 0) ^ ((I & 2) ? zr[1] : 0) ^ ((I & 4) ? zr[2] : 0) ^ ((I & 8) ? zr[3] : 0);
+}
+
+template <int I>
+__device__ __forceinline__ void sts_all(double2 *sm, const double2 (&a)[16], int zt, const int (&zr)[4])
+{
+    sm[zsel<I>(zt, zr)] = a[I];
+    if constexpr (I + 1 < 16) sts_all<I + 1>(sm, a, zt, zr);
+}
+template <int I>
+__device__ __forceinline__ void lds_all(const double2 *sm, double2 (&a)[16], int zt, const int (&zr)[4])
+{
+    a[I] = sm[zsel<I>(zt, zr)];
+    if constexpr (I + 1 < 16) lds_all<I + 1>(sm, a, zt, zr);
+}
+
+// global offset of the thread's lane/warp part and register-bit parts (load/store configs)
+__device__ __forceinline__ void global_coords(const PassDesc &d, uint64_t c, int lane, int warp, uint64_t &gt,
+                                              uint64_t &g1, uint64_t &g2, uint64_t &g3)
+{
+    gt = (uint64_t)((lane & 3) << 1);  // l0 = tile bit 1 = phys 1, l1 = tile bit 2 = phys 2
+#pragma unroll
+    for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << d.tp[cfg_nib(c, 4 + j)];
+#pragma unroll
+    for (int j = 0; j < 3; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, 9 + j)];
+    g1 = 1ULL << d.tp[cfg_nib(c, 1)];
+    g2 = 1ULL << d.tp[cfg_nib(c, 2)];
+    g3 = 1ULL << d.tp[cfg_nib(c, 3)];
+}
 
 template <int CAP>
 struct PassParams {
@@ -161,25 +170,15 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     for (int j = 0; j < kTileBits; j++) base = insert_zero(base, d.tile_sorted[j]);
     const uint64_t gcta = d.rank_bits | base;
 
-    int rREG = d.role_tri[ROLE_REG], rLANE = d.role_tri[ROLE_LANE], rWARP = d.role_tri[ROLE_WARP];
-
+    uint64_t cfg = d.cfg0;
     double2 a[16];
-    uint64_t r0, r1, r2, toff;
-    auto offsets = [&]() {
-        r0 = 1ULL << d.tri[rREG][0];
-        r1 = 1ULL << d.tri[rREG][1];
-        r2 = 1ULL << d.tri[rREG][2];
-        const uint64_t l0 = 1ULL << d.tri[rLANE][0], l1 = 1ULL << d.tri[rLANE][1], l2 = 1ULL << d.tri[rLANE][2];
-        const uint64_t w0 = 1ULL << d.tri[rWARP][0], w1 = 1ULL << d.tri[rWARP][1], w2 = 1ULL << d.tri[rWARP][2];
-        toff = (uint64_t)((lane & 3) << 1) | ((lane & 4) ? l0 : 0) | ((lane & 8) ? l1 : 0) |
-               ((lane & 16) ? l2 : 0) | ((warp & 1) ? w0 : 0) | ((warp & 2) ? w1 : 0) | ((warp & 4) ? w2 : 0);
-    };
-    offsets();
     {
-        double2 *p = st + base + toff;
+        uint64_t gt, g1, g2, g3;
+        global_coords(d, cfg, lane, warp, gt, g1, g2, g3);
+        const double2 *p = st + base + gt;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            const uint64_t ro = ((j & 1) ? r0 : 0) | ((j & 2) ? r1 : 0) | ((j & 4) ? r2 : 0);
+            const uint64_t ro = ((j & 1) ? g1 : 0) | ((j & 2) ? g2 : 0) | ((j & 4) ? g3 : 0);
             ld256(p + ro, a[2 * j], a[2 * j + 1]);
         }
     }
@@ -188,32 +187,21 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
         const KOp &op = P.ops[o];
         const int code = op.code;
         if (code == OPC_TRANS) {
-            // registers -> swizzled smem with the current roles, then back with the new roles
-            {
-                const int sl = ((lane & 3) << 1) | ((lane >> 2) << (3 + 3 * rLANE)) | (warp << (3 + 3 * rWARP));
-                const int sh = 3 + 3 * rREG;
-#pragma unroll
-                for (int i = 0; i < 16; i++) sm[swz(sl | (i & 1) | ((i >> 1) << sh))] = a[i];
-            }
+            int zt, zr[4];
+            smem_coords(cfg, lane, warp, zt, zr);
+            sts_all<0>(sm, a, zt, zr);
             __syncthreads();
-            const int ta = op.ta, tb = op.tb;
-            const int xa = pick3(ta, rREG, rLANE, rWARP), xb = pick3(tb, rREG, rLANE, rWARP);
-            if (ta == ROLE_REG) rREG = xb; else if (ta == ROLE_LANE) rLANE = xb; else rWARP = xb;
-            if (tb == ROLE_REG) rREG = xa; else if (tb == ROLE_LANE) rLANE = xa; else rWARP = xa;
-            {
-                const int sl = ((lane & 3) << 1) | ((lane >> 2) << (3 + 3 * rLANE)) | (warp << (3 + 3 * rWARP));
-                const int sh = 3 + 3 * rREG;
-#pragma unroll
-                for (int i = 0; i < 16; i++) a[i] = sm[swz(sl | (i & 1) | ((i >> 1) << sh))];
-            }
+            cfg = op.cfg;
+            smem_coords(cfg, lane, warp, zt, zr);
+            lds_all<0>(sm, a, zt, zr);
             __syncthreads();
             continue;
         }
         const bool tp = ((lane & op.mlane) == op.vlane) && ((warp & op.mwarp) == op.vwarp) &&
                         ((gcta & op.mout) == op.vout);
+        if (!tp) continue;
         const uint32_t mreg = op.mreg, vreg = op.vreg;
         if (code == OPC_PHASE) {
-            if (!tp) continue;
             const double2 f = make_double2(op.m[0], op.m[1]);
             if (mreg == 0) {
 #pragma unroll
@@ -225,22 +213,17 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
             }
             continue;
         }
-        if (op.role == ROLE_REG) {
-            if (!tp) continue;
-            if (mreg == 0) reg_op<false>(a, op, code, 0, 0);
-            else reg_op<true>(a, op, code, mreg, vreg);
-            continue;
-        }
-        if (__all_sync(FULL, tp) && mreg == 0) lane_op<false>(a, op, code, lane, true, 0, 0);
-        else if (__any_sync(FULL, tp)) lane_op<true>(a, op, code, lane, tp, mreg, vreg);
+        if (mreg == 0) reg_op<false>(a, op, code, 0, 0);
+        else reg_op<true>(a, op, code, mreg, vreg);
     }
 
-    offsets();
     {
-        double2 *p = st + base + toff;
+        uint64_t gt, g1, g2, g3;
+        global_coords(d, cfg, lane, warp, gt, g1, g2, g3);
+        double2 *p = st + base + gt;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            const uint64_t ro = ((j & 1) ? r0 : 0) | ((j & 2) ? r1 : 0) | ((j & 4) ? r2 : 0);
+            const uint64_t ro = ((j & 1) ? g1 : 0) | ((j & 2) ? g2 : 0) | ((j & 4) ? g3 : 0);
             st256(p + ro, a[2 * j], a[2 * j + 1]);
         }
     }
@@ -272,8 +255,8 @@ static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cud
 
 void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s)
 {
-    if (variant == 2) launch_pass_minb<2>(d, ops, st, s);
-    else launch_pass_minb<1>(d, ops, st, s);
+    if (variant == 1) launch_pass_minb<1>(d, ops, st, s);
+    else launch_pass_minb<2>(d, ops, st, s);
 }
 
 int pass_regs_per_thread()

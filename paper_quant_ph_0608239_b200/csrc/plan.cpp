@@ -110,9 +110,6 @@ struct POp {
     int gid;
 };
 
-struct RoleState {
-    int rt[3];  // role -> triple
-};
 }  // namespace
 
 static void set_u2_code(const GateRec &g, POp &p)
@@ -121,91 +118,165 @@ static void set_u2_code(const GateRec &g, POp &p)
     for (int k = 0; k < 8; k++) p.m[k] = g.u[k];
 }
 
-// simulate role assignment + transposes; returns cost, fills ops if emit
-static int lower_pass(const std::vector<POp> &pops, const int tri[3][3], const int init_rt[3],
-                      bool emit, std::vector<KOp> *kops, std::vector<int> *kgate, Step *st = nullptr)
-{
-    int where[64];  // physical bit -> triple index (or -1)
-    int widx[64];
-    for (int p = 0; p < 64; p++) where[p] = -1, widx[p] = 0;
-    for (int x = 0; x < 3; x++)
-        for (int j = 0; j < 3; j++) { where[tri[x][j]] = x; widx[tri[x][j]] = j; }
-    int rt[3] = {init_rt[0], init_rt[1], init_rt[2]};
-    auto role_of = [&](int x) {
-        for (int r = 0; r < 3; r++)
-            if (rt[r] == x) return r;
+namespace {
+// thread-coordinate assignment of the 12 tile-local bits (see engine.h)
+struct Cfg {
+    int r[4], l[5], w[3];
+    uint64_t pack() const
+    {
+        uint64_t c = 0;
+        int v[12] = {r[0], r[1], r[2], r[3], l[0], l[1], l[2], l[3], l[4], w[0], w[1], w[2]};
+        for (int j = 0; j < 12; j++) c |= (uint64_t)v[j] << (4 * j);
+        return c;
+    }
+    bool store_ok() const { return r[0] == 0 && l[0] == 1 && l[1] == 2; }
+    int role_of(int t, int &j) const
+    {
+        for (j = 0; j < 4; j++)
+            if (r[j] == t) return ROLE_REG;
+        for (j = 0; j < 5; j++)
+            if (l[j] == t) return ROLE_LANE;
+        for (j = 0; j < 3; j++)
+            if (w[j] == t) return ROLE_WARP;
+        j = -1;
         return -1;
+    }
+};
+
+// Complete a register set into a config.  Lanes must cover tile-bit residues
+// {0,1,2} mod 3 for conflict-free transposes (kernels.cu swz).
+Cfg make_cfg(const std::vector<int> &reg_in, bool store)
+{
+    Cfg c;
+    std::vector<int> reg = reg_in;
+    if (store) {
+        reg.erase(std::remove(reg.begin(), reg.end(), 0), reg.end());
+        reg.insert(reg.begin(), 0);
+    }
+    bool used[kTileBits] = {false};
+    for (int j = 0; j < 4; j++) { c.r[j] = reg[j]; used[reg[j]] = true; }
+    std::vector<int> lanes;
+    if (store) { lanes = {1, 2}; used[1] = used[2] = true; }
+    // one lane bit of every missing residue first
+    for (int res = 0; res < 3; res++) {
+        bool have = false;
+        for (int t : lanes) have |= (t % 3) == res;
+        if (have) continue;
+        for (int t = 0; t < kTileBits; t++)
+            if (!used[t] && t % 3 == res) { lanes.push_back(t); used[t] = true; break; }
+    }
+    for (int t = 0; t < kTileBits && (int)lanes.size() < 5; t++)
+        if (!used[t]) { lanes.push_back(t); used[t] = true; }
+    for (int j = 0; j < 5; j++) c.l[j] = lanes[j];
+    int nw = 0;
+    for (int t = 0; t < kTileBits; t++)
+        if (!used[t]) c.w[nw++] = t;
+    return c;
+}
+
+bool conflict(const POp &a, const POp &b)
+{
+    const uint64_t Na = a.code == OPC_PHASE ? 0 : bit(a.t), Nb = b.code == OPC_PHASE ? 0 : bit(b.t);
+    return (Na & (Nb | b.cm)) || (a.cm & Nb);
+}
+}  // namespace
+
+// Schedule the pass ops (dependency-respecting list scheduling that prefers
+// ops whose target is already in registers), insert OPC_TRANS re-layouts,
+// split every predicate over the thread coordinates.
+static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &st, uint64_t &cfg0)
+{
+    const size_t n = pops.size();
+    std::vector<std::vector<int>> preds(n);
+    for (size_t b = 0; b < n; b++)
+        for (size_t a = 0; a < b; a++)
+            if (conflict(pops[a], pops[b])) preds[b].push_back((int)a);
+    std::vector<char> done(n, 0);
+    auto ready = [&](size_t b) {
+        for (int a : preds[b])
+            if (!done[a]) return false;
+        return true;
     };
-    int cost = 0;
-    for (size_t o = 0; o < pops.size(); o++) {
-        const POp &p = pops[o];
-        int role = -1, k = 0;
-        if (p.code != OPC_PHASE) {
-            int t = p.t;
-            if (t == 0) { role = ROLE_REG; k = 0; }
-            else if (t == 1 || t == 2) { role = ROLE_LANE; k = t - 1; }
-            else {
-                int x = where[t];
-                role = role_of(x);
-                if (role == ROLE_WARP) {
-                    // evict the role whose triple is needed furthest ahead
-                    int best = ROLE_REG;
-                    size_t bestd = 0;
-                    for (int pr = ROLE_REG; pr <= ROLE_LANE; pr++) {
-                        int xx = rt[pr];
-                        size_t d = pops.size() + 1;
-                        for (size_t q = o + 1; q < pops.size(); q++)
-                            if (pops[q].code != OPC_PHASE && where[pops[q].t] == xx) { d = q - o; break; }
-                        if (d > bestd || (d == bestd && pr == ROLE_LANE)) { bestd = d; best = pr; }
-                    }
-                    if (emit) {
-                        KOp tr{};
-                        tr.code = OPC_TRANS;
-                        tr.ta = ROLE_WARP;
-                        tr.tb = best;
-                        kops->push_back(tr);
-                        kgate->push_back(-1);
-                        st->op_t.push_back(-1);
-                        st->op_cm.push_back(0);
-                        st->op_cv.push_back(0);
-                    }
-                    std::swap(rt[ROLE_WARP], rt[best]);
-                    cost += 4;
-                    role = best;
-                }
-                k = (role == ROLE_REG ? 1 : 2) + widx[t];
+    auto tl = [&](const POp &p) { return tl_of[p.t]; };
+    // upcoming register bits: targets of ready ops first, then of the rest, in order
+    auto upcoming = [&](bool store, std::vector<int> &reg) {
+        reg.clear();
+        if (store) reg.push_back(0);
+        for (int pass = 0; pass < 2 && reg.size() < 4; pass++)
+            for (size_t b = 0; b < n && reg.size() < 4; b++) {
+                if (done[b] || pops[b].code == OPC_PHASE) continue;
+                if ((pass == 0) != ready(b)) continue;
+                int t = tl(pops[b]);
+                if (store && (t == 1 || t == 2)) continue;
+                if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
             }
-            if (role == ROLE_LANE) cost += 1;
+        for (int t = 3; reg.size() < 4 && t < kTileBits; t++)
+            if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
+    };
+    std::vector<int> reg;
+    upcoming(true, reg);
+    Cfg cfg = make_cfg(reg, true);
+    cfg0 = cfg.pack();
+    auto emit_trans = [&](const Cfg &nc) {
+        KOp tr{};
+        tr.code = OPC_TRANS;
+        tr.cfg = nc.pack();
+        st.ops.push_back(tr);
+        st.op_gate.push_back(-1);
+        st.op_t.push_back(-1);
+        st.op_cm.push_back(0);
+        st.op_cv.push_back(0);
+    };
+    size_t left = n;
+    while (left) {
+        size_t pick = n;
+        for (size_t b = 0; b < n; b++) {
+            if (done[b] || !ready(b)) continue;
+            int j;
+            if (pops[b].code == OPC_PHASE || cfg.role_of(tl(pops[b]), j) == ROLE_REG) { pick = b; break; }
         }
-        if (!emit) continue;
+        if (pick == n) {
+            upcoming(false, reg);
+            cfg = make_cfg(reg, false);
+            emit_trans(cfg);
+            continue;
+        }
+        const POp &p = pops[pick];
         KOp op{};
         op.code = p.code;
-        op.role = role;
-        op.k = k;
-        for (int j = 0; j < 8; j++) op.m[j] = p.m[j];
-        // split the predicate over the roles
+        int j = 0;
+        if (p.code != OPC_PHASE) {
+            cfg.role_of(tl(p), j);
+            op.k = j;
+        }
+        for (int k = 0; k < 8; k++) op.m[k] = p.m[k];
         for (int b = 0; b < 64; b++) {
             if (!((p.cm >> b) & 1)) continue;
-            uint32_t v = (uint32_t)((p.cv >> b) & 1);
-            if (b == 0) { op.mreg |= 1u; op.vreg |= v; }
-            else if ((b == 1 || b == 2)) { op.mlane |= 1u << (b - 1); op.vlane |= v << (b - 1); }
-            else if (where[b] >= 0) {
-                int r = role_of(where[b]), j = widx[b];
-                if (r == ROLE_REG) { op.mreg |= 1u << (1 + j); op.vreg |= v << (1 + j); }
-                else if (r == ROLE_LANE) { op.mlane |= 1u << (2 + j); op.vlane |= v << (2 + j); }
-                else { op.mwarp |= 1u << j; op.vwarp |= v << j; }
-            } else {
-                op.mout |= 1ULL << b;
-                op.vout |= (uint64_t)v << b;
-            }
+            const uint32_t v = (uint32_t)((p.cv >> b) & 1);
+            const int t = tl_of[b];
+            int role = t >= 0 ? cfg.role_of(t, j) : -1;
+            if (role == ROLE_REG) { op.mreg |= 1u << j; op.vreg |= v << j; }
+            else if (role == ROLE_LANE) { op.mlane |= 1u << j; op.vlane |= v << j; }
+            else if (role == ROLE_WARP) { op.mwarp |= 1u << j; op.vwarp |= v << j; }
+            else { op.mout |= 1ULL << b; op.vout |= (uint64_t)v << b; }
         }
-        kops->push_back(op);
-        kgate->push_back(p.gid);
-        st->op_t.push_back(p.code == OPC_PHASE ? -1 : p.t);
-        st->op_cm.push_back(p.cm);
-        st->op_cv.push_back(p.cv);
+        st.ops.push_back(op);
+        st.op_gate.push_back(p.gid);
+        st.op_t.push_back(p.code == OPC_PHASE ? -1 : p.t);
+        st.op_cm.push_back(p.cm);
+        st.op_cv.push_back(p.cv);
+        done[pick] = 1;
+        left--;
     }
-    return cost;
+    if (!cfg.store_ok()) {
+        std::vector<int> r2;
+        for (int k = 0; k < 4; k++)
+            if (cfg.r[k] != 1 && cfg.r[k] != 2) r2.push_back(cfg.r[k]);
+        for (int t = 3; r2.size() < 4 && t < kTileBits; t++)
+            if (std::find(r2.begin(), r2.end(), t) == r2.end()) r2.push_back(t);
+        if (std::find(r2.begin(), r2.end(), 0) == r2.end()) { r2.insert(r2.begin(), 0); r2.pop_back(); }
+        emit_trans(make_cfg(r2, true));
+    }
 }
 
 void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
@@ -272,43 +343,34 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
         pops.push_back(p);
         done[i] = 1;
     }
-    // order free bits by first use, then fill the tile
+    // tile: physical bits 0,1,2 + the free bits (first-use order), filled up to 12
     std::vector<int> order;
     for (const POp &p : pops)
-        if (p.code != OPC_PHASE && p.t >= 3 &&
-            std::find(order.begin(), order.end(), p.t) == order.end())
+        if (p.code != OPC_PHASE && p.t >= 3 && std::find(order.begin(), order.end(), p.t) == order.end())
             order.push_back(p.t);
-    for (int p = 3; (int)order.size() < 9 && p < M; p++)
-        if (!in_tile[p]) { in_tile[p] = true; order.push_back(p); }
     for (int b : freeb)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
+    for (int p = 3; (int)order.size() < 9 && p < M; p++)
+        if (!in_tile[p]) { in_tile[p] = true; order.push_back(p); }
 
     Step st;
     st.type = ST_PASS;
-    int tri[3][3];
-    for (int x = 0; x < 3; x++)
-        for (int j = 0; j < 3; j++) tri[x][j] = order[3 * x + j];
-    // choose the initial role assignment with the lowest simulated cost
-    static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    int best = 0, bestc = 1 << 30;
-    for (int a = 0; a < 6; a++) {
-        int c = lower_pass(pops, tri, perms[a], false, nullptr, nullptr);
-        if (c < bestc) { bestc = c; best = a; }
-    }
-    lower_pass(pops, tri, perms[best], true, &st.ops, &st.op_gate, &st);
     PassDesc &d = st.pass;
+    int tl_of[64];
+    for (int b = 0; b < 64; b++) tl_of[b] = -1;
+    for (int t = 0; t < 3; t++) { d.tp[t] = t; tl_of[t] = t; }
+    for (int j = 0; j < 9; j++) { d.tp[3 + j] = order[j]; tl_of[order[j]] = 3 + j; }
+    uint64_t cfg0 = 0;
+    lower_pass(pops, tl_of, st, cfg0);
+    d.cfg0 = cfg0;
     d.M = M;
     d.n_inst = 1ULL << (M - kTileBits);
-    d.op_begin = 0;
     d.n_ops = (int)st.ops.size();
     d.use_smem = 0;
     for (const KOp &k : st.ops)
         if (k.code == OPC_TRANS) d.use_smem = 1;
-    for (int x = 0; x < 3; x++)
-        for (int j = 0; j < 3; j++) d.tri[x][j] = tri[x][j];
-    for (int r = 0; r < 3; r++) d.role_tri[r] = perms[best][r];
-    int tiles[kTileBits] = {0, 1, 2};
-    for (int j = 0; j < 9; j++) tiles[3 + j] = order[j];
+    int tiles[kTileBits];
+    for (int j = 0; j < kTileBits; j++) tiles[j] = d.tp[j];
     std::sort(tiles, tiles + kTileBits);
     for (int j = 0; j < kTileBits; j++) d.tile_sorted[j] = tiles[j];
     out.push_back(std::move(st));
@@ -471,16 +533,14 @@ std::string plan_to_json(const Planner &P, const std::vector<Step> &steps)
         case ST_PASS: {
             o << "{\"type\":\"pass\",\"tile\":[";
             for (int j = 0; j < kTileBits; j++) o << (j ? "," : "") << st.pass.tile_sorted[j];
-            o << "],\"tri\":[";
-            for (int x = 0; x < 3; x++)
-                for (int j = 0; j < 3; j++) o << (x + j ? "," : "") << st.pass.tri[x][j];
-            o << "],\"role_tri\":[" << st.pass.role_tri[0] << "," << st.pass.role_tri[1] << ","
-              << st.pass.role_tri[2] << "],\"ops\":[";
+            o << "],\"tp\":[";
+            for (int j = 0; j < kTileBits; j++) o << (j ? "," : "") << st.pass.tp[j];
+            o << "],\"cfg0\":" << st.pass.cfg0 << ",\"ops\":[";
             for (size_t k = 0; k < st.ops.size(); k++) {
                 const KOp &op = st.ops[k];
                 o << (k ? "," : "") << "{\"gate\":" << st.op_gate[k] << ",\"t\":" << st.op_t[k]
                   << ",\"cm\":" << st.op_cm[k] << ",\"cv\":" << st.op_cv[k] << ",\"code\":" << op.code
-                  << ",\"role\":" << op.role << ",\"k\":" << op.k << ",\"ta\":" << op.ta << ",\"tb\":" << op.tb
+                  << ",\"k\":" << op.k << ",\"cfg\":" << op.cfg
                   << ",\"mreg\":" << op.mreg << ",\"vreg\":" << op.vreg << ",\"mlane\":" << op.mlane
                   << ",\"vlane\":" << op.vlane << ",\"mwarp\":" << op.mwarp << ",\"vwarp\":" << op.vwarp
                   << ",\"mout\":" << op.mout << ",\"vout\":" << op.vout << ",\"m\":[";

@@ -58,7 +58,7 @@ struct qsim_ctx_s {
     // options
     bool fusion = true, timing = false;
     int max_scan = 1 << 30;
-    int pass_variant = 1;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
+    int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
     // stats
     qsim_stats stats{};
@@ -385,25 +385,20 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
     size_t nops = 0, nperm = 0;  // pass ops travel in the kernel parameter block
     for (Step &s : steps)
         if (s.type == ST_PERM) nperm += s.perm.size();
-    if (nops == 0 && nperm == 0) return QSIM_OK;
+    (void)nops;
+    if (nperm == 0) return QSIM_OK;
     qsim_status st;
-    if ((st = ensure_host(c, c->h_ops, c->h_ops_cap, nops + 1)) != QSIM_OK) return st;
     if ((st = ensure_host(c, c->h_perm, c->h_perm_cap, nperm + 1)) != QSIM_OK) return st;
-    if ((st = ensure_dev(c, c->d_ops, c->d_ops_cap, nops + 1)) != QSIM_OK) return st;
     if ((st = ensure_dev(c, c->d_perm, c->d_perm_cap, nperm + 1)) != QSIM_OK) return st;
     if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));  // staging reuse
-    size_t o = 0, p = 0;
+    size_t p = 0;
     for (Step &s : steps) {
-        if (s.type == ST_PASS) {
-            std::memcpy(c->h_ops + o, s.ops.data(), s.ops.size() * sizeof(KOp));
-            o += s.ops.size();
-        } else if (s.type == ST_PERM) {
+        if (s.type == ST_PERM) {
             std::memcpy(c->h_perm + p, s.perm.data(), s.perm.size() * sizeof(uint32_t));
             s.t = (int)p;  // perm offset
             p += s.perm.size();
         }
     }
-    if (nops) CK(c, cudaMemcpyAsync(c->d_ops, c->h_ops, nops * sizeof(KOp), cudaMemcpyHostToDevice, c->stream));
     if (nperm) CK(c, cudaMemcpyAsync(c->d_perm, c->h_perm, nperm * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
     if (!c->upload_done) CK(c, cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
     CK(c, cudaEventRecord(c->upload_done, c->stream));
@@ -977,7 +972,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30);
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
-    else if (k == "pass_variant") c->pass_variant = value == 2 ? 2 : 1;
+    else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
     else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
     return QSIM_OK;
 }
