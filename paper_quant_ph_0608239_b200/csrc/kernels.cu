@@ -49,6 +49,38 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t v, int p)
 }
 
 // ---------------------------------------------------------------- k_pass
+// In-place pair updates: every output is finished by one FMA that consumes
+// the old value held in the same register, after all partial sums that still
+// need the old values are formed.  This keeps the 16 amplitudes in fixed
+// registers across the op loop (no compiler copies).
+__device__ __forceinline__ void u2_inplace(double2 &x, double2 &y, const double2 u00, const double2 u01,
+                                           const double2 u10, const double2 u11)
+{
+    const double p1 = fma(-u00.y, x.y, fma(u01.x, y.x, -u01.y * y.y));  // x'.re - u00r x.re
+    const double p2 = fma(u00.y, x.x, fma(u01.x, y.y, u01.y * y.x));    // x'.im - u00r x.im
+    const double p3 = fma(u10.x, x.x, fma(-u10.y, x.y, -u11.y * y.y));  // y'.re - u11r y.re
+    const double p4 = fma(u10.x, x.y, fma(u10.y, x.x, u11.y * y.x));    // y'.im - u11r y.im
+    x.x = fma(u00.x, x.x, p1);
+    x.y = fma(u00.x, x.y, p2);
+    y.x = fma(u11.x, y.x, p3);
+    y.y = fma(u11.x, y.y, p4);
+}
+
+__device__ __forceinline__ void u2r_inplace(double2 &x, double2 &y, double u00, double u01, double u10, double u11)
+{
+    const double p1 = u01 * y.x, p2 = u01 * y.y, p3 = u10 * x.x, p4 = u10 * x.y;
+    x.x = fma(u00, x.x, p1);
+    x.y = fma(u00, x.y, p2);
+    y.x = fma(u11, y.x, p3);
+    y.y = fma(u11, y.y, p4);
+}
+
+// register swap that keeps both values in their own registers
+__device__ __forceinline__ void swap_inplace(double &x, double &y)
+{
+    asm("{\n\t.reg .f64 t;\n\tmov.f64 t, %0;\n\tmov.f64 %0, %1;\n\tmov.f64 %1, t;\n\t}" : "+d"(x), "+d"(y));
+}
+
 template <int K, int CODE, bool PRED>
 __device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint32_t mreg, uint32_t vreg)
 {
@@ -64,16 +96,13 @@ __device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint3
         const int i0 = ((p >> K) << (K + 1)) | (p & ((1 << K) - 1));
         const int i1 = i0 | (1 << K);
         if (PRED && (i0 & mreg) != vreg) continue;
-        const double2 x = a[i0], y = a[i1];
         if (CODE == OPC_XS) {
-            a[i0] = y;
-            a[i1] = x;
+            swap_inplace(a[i0].x, a[i1].x);
+            swap_inplace(a[i0].y, a[i1].y);
         } else if (CODE == OPC_U2R) {
-            a[i0] = make_double2(fma(u00.x, x.x, u01.x * y.x), fma(u00.x, x.y, u01.x * y.y));
-            a[i1] = make_double2(fma(u10.x, x.x, u11.x * y.x), fma(u10.x, x.y, u11.x * y.y));
+            u2r_inplace(a[i0], a[i1], u00.x, u01.x, u10.x, u11.x);
         } else {
-            a[i0] = cmac2(u00, x, u01, y);
-            a[i1] = cmac2(u10, x, u11, y);
+            u2_inplace(a[i0], a[i1], u00, u01, u10, u11);
         }
     }
 }
@@ -202,14 +231,13 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
         if (!tp) continue;
         const uint32_t mreg = op.mreg, vreg = op.vreg;
         if (code == OPC_PHASE) {
-            const double2 f = make_double2(op.m[0], op.m[1]);
-            if (mreg == 0) {
+            const double fr = op.m[0], fi = op.m[1];
 #pragma unroll
-                for (int i = 0; i < 16; i++) a[i] = cmul(f, a[i]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; i++)
-                    if ((i & mreg) == vreg) a[i] = cmul(f, a[i]);
+            for (int i = 0; i < 16; i++) {
+                if ((i & mreg) != vreg) continue;
+                const double p1 = -fi * a[i].y, p2 = fi * a[i].x;
+                a[i].x = fma(fr, a[i].x, p1);
+                a[i].y = fma(fr, a[i].y, p2);
             }
             continue;
         }
