@@ -207,6 +207,9 @@ typedef struct {
     double reduce_ms;
     double plan_ms;            /* host planning time */
     uint64_t pass_amp_bytes;   /* algorithmic bytes of the timed passes (32 B/amp/pass) */
+    uint64_t jit_launches;     /* passes run by a pass-specialised (NVRTC) kernel */
+    uint64_t jit_kernels;      /* specialised kernels in the process cache */
+    double jit_compile_ms;     /* total NVRTC + module-load time in this process */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);

@@ -39,7 +39,10 @@ class qsim_stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in ("gates", "flushes", "passes", "generic_launches", "perm_launches",
                                               "exchanges", "exchange_bytes", "kernel_launches", "relabels")] + \
                [(k, ctypes.c_double) for k in ("pass_ms", "generic_ms", "perm_ms", "exchange_ms", "reduce_ms",
-                                              "plan_ms")] + [("pass_amp_bytes", ctypes.c_uint64)]
+                                              "plan_ms")] + [("pass_amp_bytes", ctypes.c_uint64),
+                                                            ("jit_launches", ctypes.c_uint64),
+                                                            ("jit_kernels", ctypes.c_uint64),
+                                                            ("jit_compile_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -1,0 +1,381 @@
+// jit.cpp -- code generation + NVRTC compilation of pass-specialised kernels.
+// See jit.h.  The generated kernel is the k_pass of kernels.cu with the op
+// loop unrolled at generation time: register bits, predicates and shared-
+// memory re-layouts become constants, the CNOT/Toffoli register swap becomes
+// a renaming, and the matrices are read as constant-bank operands.
+#include "jit.h"
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <sstream>
+#include <thread>
+
+namespace qsb {
+
+namespace {
+
+int nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
+int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+struct Layout {
+    int n_out = 0, n_m = 0;
+    size_t off_out = 160, off_m = 0, bytes = 0;
+};
+
+Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_idx)
+{
+    Layout L;
+    out_idx.assign(st.ops.size(), -1);
+    m_idx.assign(st.ops.size(), -1);
+    for (size_t o = 0; o < st.ops.size(); o++) {
+        const KOp &op = st.ops[o];
+        if (op.code == OPC_TRANS) continue;
+        if (op.mout) out_idx[o] = L.n_out++;
+        if (op.code != OPC_XS) m_idx[o] = L.n_m++;
+    }
+    L.off_m = L.off_out + 16 * (size_t)std::max(1, L.n_out);
+    L.bytes = (L.off_m + 64 * (size_t)std::max(1, L.n_m) + 15) / 16 * 16;
+    return L;
+}
+
+}  // namespace
+
+JitPass jit_generate(const Step &st)
+{
+    std::vector<int> out_idx, m_idx;
+    Layout L = layout_of(st, out_idx, m_idx);
+    std::ostringstream s;
+    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long tpm[12]; "
+         "int ts[12]; unsigned long long out["
+      << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsim_pass(const __grid_constant__ JP P)\n{\n";
+    s << " extern __shared__ double2 sm[];\n";
+    s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    s << " unsigned long long base = blockIdx.x;\n";
+    s << "#pragma unroll\n for (int j = 0; j < 12; j++) { const int t = P.ts[j]; "
+         "base = ((base >> t) << (t + 1)) | (base & ((1ULL << t) - 1)); }\n";
+    s << " const unsigned long long gcta = P.rank_bits | base;\n";
+    s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
+    int reg[16];
+    for (int i = 0; i < 16; i++) reg[i] = i;
+    auto A = [&](int i) { return "a" + std::to_string(reg[i]); };
+    auto gaddr = [&](uint64_t c) {
+        std::ostringstream g;
+        g << "(unsigned long long)((lane & 3) << 1)";
+        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? P.tpm[" << nib(c, 4 + j) << "] : 0ULL)";
+        for (int j = 0; j < 3; j++) g << " | (((warp >> " << j << ") & 1) ? P.tpm[" << nib(c, 9 + j) << "] : 0ULL)";
+        return g.str();
+    };
+    auto roff = [&](uint64_t c, int j) {
+        std::ostringstream g;
+        g << "0ULL";
+        for (int b = 0; b < 3; b++)
+            if ((j >> b) & 1) g << " | P.tpm[" << nib(c, 1 + b) << "]";
+        return g.str();
+    };
+    uint64_t cur = st.pass.cfg0;
+    s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
+    for (int j = 0; j < 8; j++)
+        s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
+             "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
+          << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
+          << " = make_double2(x2, x3); }\n";
+    s << " }\n";
+    auto smem_z = [&](uint64_t c, const char *tag) {
+        s << "  const int zt" << tag << " = ";
+        for (int j = 0; j < 5; j++) s << "(((lane >> " << j << ") & 1) << " << nib(c, 4 + j) << ") | ";
+        for (int j = 0; j < 3; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, 9 + j) << ")" << (j < 2 ? " | " : ";\n");
+        s << "  const int zz" << tag << " = zt" << tag << " ^ (((zt" << tag << " >> 3) ^ (zt" << tag << " >> 6) ^ (zt"
+          << tag << " >> 9)) & 7);\n";
+    };
+    auto zreg = [&](uint64_t c, int i) {
+        int z = 0;
+        for (int b = 0; b < 4; b++)
+            if ((i >> b) & 1) z ^= swz_host(1 << nib(c, b));
+        return z;
+    };
+    for (size_t o = 0; o < st.ops.size(); o++) {
+        const KOp &op = st.ops[o];
+        if (op.code == OPC_TRANS) {
+            s << " {\n";
+            smem_z(cur, "a");
+            for (int i = 0; i < 16; i++) s << "  sm[zza ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
+            s << "  __syncthreads();\n";
+            cur = op.cfg;
+            smem_z(cur, "b");
+            for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzb ^ " << zreg(cur, i) << "];\n";
+            s << "  __syncthreads();\n }\n";
+            continue;
+        }
+        const bool plw = op.mlane || op.mwarp;  // thread-dependent predicate
+        const bool pout = op.mout != 0;         // CTA-uniform predicate
+        std::ostringstream pr;
+        pr << "true";
+        if (op.mlane) pr << " && ((lane & " << op.mlane << ") == " << op.vlane << ")";
+        if (op.mwarp) pr << " && ((warp & " << op.mwarp << ") == " << op.vwarp << ")";
+        if (pout) pr << " && ((gcta & P.out[" << out_idx[o] << "][0]) == P.out[" << out_idx[o] << "][1])";
+        const bool sel = plw || (pout && op.code == OPC_XS);  // select-based (no branch)
+        s << " { // op " << o << " code " << op.code << "\n";
+        if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
+        if (pout && !sel) s << "  if (tp) {\n";
+        const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
+        if (op.code == OPC_PHASE) {
+            for (int i = 0; i < 16; i++) {
+                if ((i & op.mreg) != op.vreg) continue;
+                const std::string v = A(i);
+                s << "  { const double p1 = -" << M << "[1] * " << v << ".y, p2 = " << M << "[1] * " << v << ".x; ";
+                if (sel)
+                    s << "const double nx = fma(" << M << "[0], " << v << ".x, p1), ny = fma(" << M << "[0], " << v
+                      << ".y, p2); " << v << ".x = tp ? nx : " << v << ".x; " << v << ".y = tp ? ny : " << v << ".y; }\n";
+                else
+                    s << v << ".x = fma(" << M << "[0], " << v << ".x, p1); " << v << ".y = fma(" << M << "[0], " << v
+                      << ".y, p2); }\n";
+            }
+        } else {
+            const int k = op.k;
+            for (int p = 0; p < 8; p++) {
+                const int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1)), i1 = i0 | (1 << k);
+                if ((i0 & (int)op.mreg) != (int)op.vreg) continue;
+                const std::string x = A(i0), y = A(i1);
+                if (op.code == OPC_XS) {
+                    if (sel)
+                        s << "  { const double2 t = " << x << "; " << x << ".x = tp ? " << y << ".x : " << x << ".x; "
+                          << x << ".y = tp ? " << y << ".y : " << x << ".y; " << y << ".x = tp ? t.x : " << y << ".x; "
+                          << y << ".y = tp ? t.y : " << y << ".y; }\n";
+                    else
+                        std::swap(reg[i0], reg[i1]);
+                    continue;
+                }
+                std::ostringstream pp;
+                if (op.code == OPC_U2R) {
+                    pp << "const double p1 = " << M << "[2] * " << y << ".x, p2 = " << M << "[2] * " << y << ".y, p3 = "
+                       << M << "[4] * " << x << ".x, p4 = " << M << "[4] * " << x << ".y; ";
+                } else {
+                    pp << "const double p1 = fma(-" << M << "[1], " << x << ".y, fma(" << M << "[2], " << y << ".x, -"
+                       << M << "[3] * " << y << ".y)); const double p2 = fma(" << M << "[1], " << x << ".x, fma(" << M
+                       << "[2], " << y << ".y, " << M << "[3] * " << y << ".x)); const double p3 = fma(" << M << "[4], "
+                       << x << ".x, fma(-" << M << "[5], " << x << ".y, -" << M << "[7] * " << y
+                       << ".y)); const double p4 = fma(" << M << "[4], " << x << ".y, fma(" << M << "[5], " << x
+                       << ".x, " << M << "[7] * " << y << ".x)); ";
+                }
+                s << "  { " << pp.str();
+                const char *dst[4] = {".x", ".y", ".x", ".y"};
+                const std::string xs[4] = {x, x, y, y};
+                const char *mm[4] = {"[0]", "[0]", "[6]", "[6]"};
+                const char *pv[4] = {"p1", "p2", "p3", "p4"};
+                if (sel) {
+                    for (int q = 0; q < 4; q++)
+                        s << "const double n" << q << " = fma(" << M << mm[q] << ", " << xs[q] << dst[q] << ", " << pv[q]
+                          << "); ";
+                    for (int q = 0; q < 4; q++)
+                        s << xs[q] << dst[q] << " = tp ? n" << q << " : " << xs[q] << dst[q] << "; ";
+                } else {
+                    for (int q = 0; q < 4; q++)
+                        s << xs[q] << dst[q] << " = fma(" << M << mm[q] << ", " << xs[q] << dst[q] << ", " << pv[q]
+                          << "); ";
+                }
+                s << "}\n";
+            }
+        }
+        if (pout && !sel) s << "  }\n";
+        s << " }\n";
+    }
+    s << " {\n  double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
+    for (int j = 0; j < 8; j++)
+        s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + (" << roff(cur, j) << ")), \"d\"("
+          << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
+          << ".y) : \"memory\");\n";
+    s << " }\n}\n";
+    JitPass jp;
+    jp.src = s.str();
+    jp.param_bytes = L.bytes;
+    return jp;
+}
+
+void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf)
+{
+    std::vector<int> out_idx, m_idx;
+    Layout L = layout_of(st, out_idx, m_idx);
+    buf.assign(L.bytes, 0);
+    uint8_t *b = buf.data();
+    std::memcpy(b + 0, &state, 8);
+    std::memcpy(b + 8, &rank_bits, 8);
+    for (int t = 0; t < kTileBits; t++) {
+        const uint64_t m = 1ULL << st.pass.tp[t];
+        std::memcpy(b + 16 + 8 * t, &m, 8);
+        std::memcpy(b + 112 + 4 * t, &st.pass.tile_sorted[t], 4);
+    }
+    for (size_t o = 0; o < st.ops.size(); o++) {
+        const KOp &op = st.ops[o];
+        if (out_idx[o] >= 0) {
+            std::memcpy(b + L.off_out + 16 * out_idx[o], &op.mout, 8);
+            std::memcpy(b + L.off_out + 16 * out_idx[o] + 8, &op.vout, 8);
+        }
+        if (m_idx[o] >= 0) std::memcpy(b + L.off_m + 64 * m_idx[o], op.m, 64);
+    }
+}
+
+// ------------------------------------------------------------- driver API
+// resolved at run time through cudart so the library loads on hosts without
+// a driver (the CPU test container)
+const Drv &drv()
+{
+    static Drv d = []() {
+        Drv x{};
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuModuleLoadData", (void **)&x.moduleLoadData, cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuModuleGetFunction", (void **)&x.moduleGetFunction, cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuFuncSetAttribute", (void **)&x.funcSetAttribute, cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuLaunchKernel", (void **)&x.launchKernel, cudaEnableDefault, &q);
+        return x;
+    }();
+    return d;
+}
+
+// ------------------------------------------------------------- compiling
+static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log)
+{
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "qsim_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+        log = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
+    nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+    if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        log.resize(n);
+        nvrtcGetProgramLog(prog, &log[0]);
+        nvrtcDestroyProgram(&prog);
+        return false;
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    cubin.resize(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    return true;
+}
+
+std::string jit_key(const Step &st)
+{
+    std::string k;
+    auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
+    put(st.pass.cfg0);
+    for (const KOp &op : st.ops) {
+        put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
+        put((uint64_t)op.mreg | ((uint64_t)op.vreg << 8) | ((uint64_t)op.mlane << 16) | ((uint64_t)op.vlane << 24) |
+            ((uint64_t)op.mwarp << 32) | ((uint64_t)op.vwarp << 40));
+        if (op.code == OPC_TRANS) put(op.cfg);
+    }
+    return k;
+}
+
+bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
+{
+    std::vector<std::string> keys, srcs;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        for (const Step *st : steps) {
+            std::string k = jit_key(*st);
+            if (fns_.count(k) || std::find(keys.begin(), keys.end(), k) != keys.end()) continue;
+            keys.push_back(k);
+        }
+    }
+    if (keys.empty()) return true;
+    for (const Step *st : steps) {
+        std::string k = jit_key(*st);
+        auto it = std::find(keys.begin(), keys.end(), k);
+        if (it != keys.end() && srcs.size() == (size_t)(it - keys.begin())) srcs.push_back(jit_generate(*st).src);
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::vector<char>> bins(srcs.size());
+    std::vector<std::string> logs(srcs.size());
+    std::vector<char> ok(srcs.size(), 0);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nthreads = std::min<size_t>(srcs.size(), hw);
+    std::vector<std::thread> th;
+    std::atomic_size_t next{0};
+    for (size_t w = 0; w < nthreads; w++)
+        th.emplace_back([&]() {
+            for (size_t i; (i = next++) < srcs.size();) ok[i] = nvrtc_compile(srcs[i], bins[i], logs[i]);
+        });
+    for (auto &t : th) t.join();
+    for (size_t i = 0; i < srcs.size(); i++) {
+        if (!ok[i]) {
+            err = "NVRTC: " + logs[i].substr(0, 2000);
+            return false;
+        }
+        CUmodule mod;
+        CUfunction fn;
+        const Drv &D = drv();
+        if (!D.moduleLoadData || !D.moduleGetFunction || !D.launchKernel) {
+            err = "CUDA driver entry points unavailable";
+            return false;
+        }
+        if (D.moduleLoadData(&mod, bins[i].data()) != CUDA_SUCCESS ||
+            D.moduleGetFunction(&fn, mod, "qsim_pass") != CUDA_SUCCESS) {
+            err = "cuModuleLoadData/cuModuleGetFunction failed";
+            return false;
+        }
+        D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, kTileAmps * 16);
+        std::lock_guard<std::mutex> g(mu_);
+        mods_.push_back(mod);
+        fns_[keys[i]] = fn;
+        compiled++;
+    }
+    compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return true;
+}
+
+bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms)
+{
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::string> keys, srcs;
+    for (const Step *st : steps) {
+        std::string k = jit_key(*st);
+        if (std::find(keys.begin(), keys.end(), k) != keys.end()) continue;
+        keys.push_back(k);
+        srcs.push_back(jit_generate(*st).src);
+    }
+    std::vector<std::vector<char>> bins(srcs.size());
+    std::vector<std::string> logs(srcs.size());
+    std::vector<char> ok(srcs.size(), 0);
+    std::atomic_size_t next{0};
+    std::vector<std::thread> th;
+    const size_t nt = std::min<size_t>(srcs.size(), std::max(1u, std::thread::hardware_concurrency()));
+    for (size_t w = 0; w < nt; w++)
+        th.emplace_back([&]() {
+            for (size_t i; (i = next++) < srcs.size();) ok[i] = nvrtc_compile(srcs[i], bins[i], logs[i]);
+        });
+    for (auto &t : th) t.join();
+    n = (int)srcs.size();
+    ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (size_t i = 0; i < srcs.size(); i++)
+        if (!ok[i]) {
+            err = logs[i].substr(0, 4000) + "\n--- source ---\n" + srcs[i].substr(0, 4000);
+            return false;
+        }
+    return true;
+}
+
+CUfunction JitCache::find(const std::string &key)
+{
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = fns_.find(key);
+    return it == fns_.end() ? nullptr : it->second;
+}
+
+size_t JitCache::size()
+{
+    std::lock_guard<std::mutex> g(mu_);
+    return fns_.size();
+}
+
+}  // namespace qsb

@@ -1,0 +1,66 @@
+// jit.h -- pass-specialised sm_100a kernels (the fast tier of k_pass).
+//
+// A fused pass's STRUCTURE (op codes, register bits, predicate masks, shared
+// memory re-layouts) is generated into CUDA source from our own template and
+// compiled with NVRTC for sm_100a; the per-pass DATA (matrices, phases,
+// tile bit positions, out-of-tile predicates) travels in the kernel
+// parameter block.  Structures repeat across passes/circuits, so compiled
+// kernels are cached by source text.  Arithmetic is the same expression
+// sequence as the interpreter k_pass, so both tiers give bitwise-identical
+// states.
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "plan.h"
+
+namespace qsb {
+
+struct Drv {
+    CUresult (*moduleLoadData)(CUmodule *, const void *);
+    CUresult (*moduleGetFunction)(CUfunction *, CUmodule, const char *);
+    CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+    CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void **, void **);
+};
+const Drv &drv();
+
+struct JitPass {
+    std::string src;     // generated source (cache key)
+    size_t param_bytes;  // size of the parameter block
+};
+
+// Generate the specialised kernel source for a pass step.
+JitPass jit_generate(const Step &st);
+// Pack the parameter block of a pass for one shard.
+void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf);
+
+// NVRTC-compile the specialised kernels of `steps` without loading them
+// (host-only check; n = distinct structures)
+bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms);
+
+// structural key of a pass (what the generated source depends on)
+std::string jit_key(const Step &st);
+
+class JitCache {
+public:
+    // generate + compile every pass structure not yet cached (NVRTC in
+    // parallel host threads); false + err on failure
+    bool compile(const std::vector<const Step *> &steps, std::string &err);
+    CUfunction find(const std::string &key);
+    size_t size();
+    double compile_ms = 0;
+    int compiled = 0;
+
+private:
+    std::mutex mu_;
+    std::unordered_map<std::string, CUfunction> fns_;
+    std::vector<CUmodule> mods_;
+};
+
+}  // namespace qsb

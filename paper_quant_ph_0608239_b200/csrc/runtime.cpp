@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/qsim.h"
+#include "jit.h"
 #include "kernels.h"
 #include "plan.h"
 
@@ -58,6 +59,7 @@ struct qsim_ctx_s {
     // options
     bool fusion = true, timing = false;
     int max_scan = 1 << 30;
+    int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
     // stats
@@ -104,6 +106,12 @@ struct qsim_ctx_s {
         }                                                                                     \
         (ctx)->stats.kernel_launches++;                                                       \
     } while (0)
+
+static JitCache &jit_cache()
+{
+    static JitCache *c = new JitCache();  // process-wide, one device per process
+    return *c;
+}
 
 static int ilog2(int P)
 {
@@ -476,15 +484,49 @@ static qsim_status flush(qsim_ctx c)
     c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     qsim_status st = upload_program(c, steps);
     if (st != QSIM_OK) return st;
+    std::vector<std::string> jkeys(steps.size());
+    if (c->jit) {
+        std::vector<const Step *> ps;
+        for (const Step &s : steps)
+            if (s.type == ST_PASS) ps.push_back(&s);
+        std::string err;
+        auto tj = std::chrono::steady_clock::now();
+        if (!jit_cache().compile(ps, err)) {
+            c->jit = 0;  // keep running on the interpreter tier, but say why
+            c->last_error = err;
+        }
+        c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj).count();
+        for (size_t i = 0; i < steps.size(); i++)
+            if (steps[i].type == ST_PASS) jkeys[i] = jit_key(steps[i]);
+    }
     const int M = c->M;
-    for (const Step &s : steps) {
+    std::vector<uint8_t> pbuf;
+    for (size_t si = 0; si < steps.size(); si++) {
+        const Step &s = steps[si];
         switch (s.type) {
         case ST_PASS: {
             RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
+            CUfunction fn = c->jit ? jit_cache().find(jkeys[si]) : nullptr;
             for (int i = 0; i < n_local(c); i++) {
-                PassDesc d = s.pass;
-                d.rank_bits = (uint64_t)local_ranks(c, i) << M;
-                launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream);
+                const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
+                if (fn) {
+                    jit_pack_params(s, c->shards[i], rb, pbuf);
+                    size_t sz = pbuf.size();
+                    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pbuf.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
+                                     CU_LAUNCH_PARAM_END};
+                    const unsigned smem = s.pass.use_smem ? kTileAmps * 16 : 0;
+                    CUresult cr = drv().launchKernel(fn, (unsigned)s.pass.n_inst, 1, 1, kPassThreads, 1, 1, smem,
+                                                 (CUstream)c->stream, nullptr, extra);
+                    if (cr != CUDA_SUCCESS) {
+                        c->poisoned = true;
+                        FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
+                    }
+                    c->stats.jit_launches++;
+                } else {
+                    PassDesc d = s.pass;
+                    d.rank_bits = rb;
+                    launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream);
+                }
                 LAUNCHED(c);
                 c->stats.passes++;
             }
@@ -973,6 +1015,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "max_scan") c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30);
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
+    else if (k == "jit") c->jit = value != 0;
     else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
     return QSIM_OK;
 }
@@ -984,6 +1027,8 @@ qsim_status qsim_get_stats(qsim_ctx c, qsim_stats *out)
     qsim_status s = collect_timing(c);
     if (s != QSIM_OK) return s;
     *out = c->stats;
+    out->jit_kernels = jit_cache().size();
+    out->jit_compile_ms = jit_cache().compile_ms;
     return QSIM_OK;
 }
 
@@ -1017,7 +1062,21 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     PlanOptions opt;
     opt.fusion = fusion != 0;
     P.plan(recs, opt, steps);
-    std::string js = init + plan_to_json(P, steps) + "}";
+    std::string jit_info;
+    if (fusion == 2) {  // also NVRTC-compile the pass-specialised kernels (host-only check)
+        std::vector<const Step *> ps;
+        for (const Step &s : steps)
+            if (s.type == ST_PASS) ps.push_back(&s);
+        std::string err;
+        int nk = 0;
+        double ms = 0;
+        bool ok = jit_compile_only(ps, err, nk, ms);
+        std::string e;
+        for (char ch : err) e += (ch == '"' || ch == '\\') ? ' ' : (ch == '\n' ? ' ' : ch);
+        jit_info = ",\"jit\":{\"ok\":" + std::string(ok ? "true" : "false") + ",\"kernels\":" + std::to_string(nk) +
+                   ",\"compile_ms\":" + std::to_string(ms) + ",\"error\":\"" + e + "\"}";
+    }
+    std::string js = init + plan_to_json(P, steps) + jit_info + "}";
     if (js.size() + 1 > buf_bytes) return QSIM_ERR_ARG;
     std::memcpy(buf, js.c_str(), js.size() + 1);
     return QSIM_OK;

@@ -73,10 +73,11 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
-def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: bool = True) -> str:
-    """Host-only planner introspection (no GPU needed)."""
+def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1) -> str:
+    """Host-only planner introspection (no GPU needed).  fusion=2 also
+    NVRTC-compiles the pass-specialised kernels (reported under "jit")."""
     arr, keep = pack_gates(gates)
-    cap = 1 << 16
+    cap = 1 << 26
     while True:
         buf = ctypes.create_string_buffer(cap)
         s = N.lib().qsim_plan_json(n, n_ranks, arr, len(gates), int(fusion), buf, cap)

@@ -127,3 +127,14 @@ def test_plan_controls_and_diagonals_on_global(pkg, oracle_mod):
               G.toffoli(12, 13, 0)]
     d = _check_plan(pkg, oracle_mod, n, P, 0, gates)
     assert not any(s["type"] == "exchange" for s in d["plan"]["steps"])
+
+
+def test_jit_kernels_compile_for_sm100a(pkg):
+    """The pass-specialised kernels generated for a circuit with every gate
+    kind (predicates on register/lane/warp/out-of-tile bits, swaps, phases,
+    re-layouts) compile with NVRTC for sm_100a (no GPU needed)."""
+    from tests.test_gpu_parity import kitchen_sink
+    gates = kitchen_sink(14, seed=3)
+    d = json.loads(_plan(pkg, 14, 2, gates, fusion=2))
+    assert d["jit"]["ok"], d["jit"]["error"]
+    assert d["jit"]["kernels"] >= 1

@@ -28,10 +28,11 @@ def P():
     return pkg
 
 
-def gpu_run(P, n, init, gates, ranks=1, fusion=True, transport=None):
+def gpu_run(P, n, init, gates, ranks=1, fusion=True, transport=None, jit=1):
     tp = transport or ("local" if ranks == 1 else "virtual")
     sim = P.QSim(n, n_ranks=ranks, transport=tp)
     sim.set_option("fusion", int(fusion))
+    sim.set_option("jit", int(jit))
     sim.init_basis(init)
     sim.run_circuit(gates)
     return sim
@@ -89,6 +90,20 @@ def test_every_gate_every_position(P, oracle_mod, n, fusion):
     gates = kitchen_sink(n, seed=n)
     sim = gpu_run(P, n, 5, gates, fusion=fusion)
     assert_parity(sim, oracle_run(oracle_mod, n, 5, gates), n)
+
+
+@pytest.mark.parametrize("n,ranks", [(13, 1), (16, 1), (15, 4)])
+def test_jit_tier_matches_interpreter_bitwise(P, oracle_mod, n, ranks):
+    """The NVRTC pass-specialised kernels and the interpreter k_pass apply the
+    same arithmetic: identical bits, and both match the oracle."""
+    gates = kitchen_sink(n, seed=7 * n) + C.random_brickwork(n, 4, seed=n)
+    s_int = gpu_run(P, n, 1, gates, ranks=ranks, jit=0)
+    s_jit = gpu_run(P, n, 1, gates, ranks=ranks, jit=1)
+    a_int, a_jit = s_int.get_amplitudes(), s_jit.get_amplitudes()
+    st = s_jit.stats()
+    assert st["jit_launches"] > 0 and s_int.stats()["jit_launches"] == 0
+    assert np.array_equal(a_int, a_jit)
+    assert_parity(s_jit, oracle_run(oracle_mod, n, 1, gates), n)
 
 
 @pytest.mark.parametrize("ranks,n", [(2, 14), (4, 15), (8, 16), (8, 12), (4, 9)])
