@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     link = ["g++", "-shared", "-o", LIB + ".tmp", *objs,
             "-L", os.path.join(CUDA, "lib64"), "-lcudart_static", "-lrt", "-ldl", "-lpthread",
             "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Wl,-rpath," + os.path.join(nccl, "lib"),
-            "-lnvrtc", "-Wl,-rpath," + os.path.join(CUDA, "lib64")]
+            "-ldl"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(" ".join(link) + "\n" + r.stdout + r.stderr)

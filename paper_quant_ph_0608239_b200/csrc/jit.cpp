@@ -6,6 +6,7 @@
 #include "jit.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -238,28 +239,72 @@ const Drv &drv()
 }
 
 // ------------------------------------------------------------- compiling
+// NVRTC of the CUDA 12.9 toolkit, loaded by absolute path: a process that
+// imported PyTorch already holds torch's own libnvrtc.so.12 (an older CUDA
+// whose ptxas rejects some sm_100a instructions), so the soname alone is not
+// enough to get the compiler this library was built with.
+struct Nvrtc {
+    nvrtcResult (*create)(nvrtcProgram *, const char *, const char *, int, const char *const *, const char *const *);
+    nvrtcResult (*compile)(nvrtcProgram, int, const char *const *);
+    nvrtcResult (*logSize)(nvrtcProgram, size_t *);
+    nvrtcResult (*log)(nvrtcProgram, char *);
+    nvrtcResult (*cubinSize)(nvrtcProgram, size_t *);
+    nvrtcResult (*cubin)(nvrtcProgram, char *);
+    nvrtcResult (*destroy)(nvrtcProgram *);
+    bool ok = false;
+};
+
+static const Nvrtc &nvrtc()
+{
+    static Nvrtc n = []() {
+        Nvrtc x{};
+        const char *env = getenv("CUDA_HOME");
+        std::string dir = env ? env : "/usr/local/cuda";
+        const char *names[] = {"/lib64/libnvrtc.so.12.9.86", "/lib64/libnvrtc.so.12", "/lib64/libnvrtc.so"};
+        void *h = nullptr;
+        for (const char *nm : names)
+            if ((h = dlopen((dir + nm).c_str(), RTLD_NOW | RTLD_LOCAL))) break;
+        if (!h) return x;
+        x.create = (decltype(x.create))dlsym(h, "nvrtcCreateProgram");
+        x.compile = (decltype(x.compile))dlsym(h, "nvrtcCompileProgram");
+        x.logSize = (decltype(x.logSize))dlsym(h, "nvrtcGetProgramLogSize");
+        x.log = (decltype(x.log))dlsym(h, "nvrtcGetProgramLog");
+        x.cubinSize = (decltype(x.cubinSize))dlsym(h, "nvrtcGetCUBINSize");
+        x.cubin = (decltype(x.cubin))dlsym(h, "nvrtcGetCUBIN");
+        x.destroy = (decltype(x.destroy))dlsym(h, "nvrtcDestroyProgram");
+        x.ok = x.create && x.compile && x.logSize && x.log && x.cubinSize && x.cubin && x.destroy;
+        return x;
+    }();
+    return n;
+}
+
 static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log)
 {
+    const Nvrtc &N = nvrtc();
+    if (!N.ok) {
+        log = "CUDA 12.9 NVRTC not found under $CUDA_HOME/lib64";
+        return false;
+    }
     nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, src.c_str(), "qsim_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    if (N.create(&prog, src.c_str(), "qsim_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
         log = "nvrtcCreateProgram failed";
         return false;
     }
-    const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
-    nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-diag-suppress=177"};
+    nvrtcResult r = N.compile(prog, 4, opts);
     if (r != NVRTC_SUCCESS) {
         size_t n = 0;
-        nvrtcGetProgramLogSize(prog, &n);
+        N.logSize(prog, &n);
         log.resize(n);
-        nvrtcGetProgramLog(prog, &log[0]);
-        nvrtcDestroyProgram(&prog);
+        N.log(prog, &log[0]);
+        N.destroy(&prog);
         return false;
     }
     size_t n = 0;
-    nvrtcGetCUBINSize(prog, &n);
+    N.cubinSize(prog, &n);
     cubin.resize(n);
-    nvrtcGetCUBIN(prog, cubin.data());
-    nvrtcDestroyProgram(&prog);
+    N.cubin(prog, cubin.data());
+    N.destroy(&prog);
     return true;
 }
 
