@@ -40,8 +40,14 @@ def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(d.get("sm_max_mhz", 1965.0))
+    return 6650.0, "fallback (B200_PROFILING.md)", 1965.0
+
+
+# FP64 ALU peak: 148 SMs x 64 FP64 FMA lanes/clk x 2 flop x max SM clock.
+# tools/fp64_peak.cu measured 34.1 TFLOP/s sustained on this pool's B200 (0.92 of it).
+FP64_FMA_PER_CLK_PER_SM = 64
+N_SM = 148
 
 
 class Clocks:
@@ -57,7 +63,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -145,7 +151,7 @@ def run_ours(args):
     n_o = len(gates)
     packed = pack_gates(gates)
     sim = QSim.distributed(n) if world > 1 else QSim(n)
-    sim.set_option("timing", 1)
+    sim.set_option("timing", 1)  # CUDA events around every pass launch (roofline)
     stream = sim.stream
 
     def step():
@@ -185,14 +191,18 @@ def run_ours(args):
     value = args.steps * n_o * float(1 << n) / (ms / 1e3)
 
     # ---- end-to-end through the public C-ABI with host buffers: the host
-    # gate array (qsim_gate[]) is marshalled + planned + uploaded every step
-    # and <Q_i> comes back to host memory; wall clock, max over ranks.
+    # gate array (qsim_gate[]) is validated, planned (plan cache off) and
+    # uploaded every step and <Q_i> comes back to host memory; wall clock,
+    # max over ranks.
+    sim.set_option("plan_cache", 0)
+    step()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     barrier()
     wall = time.perf_counter() - t0
+    sim.set_option("plan_cache", 1)
     tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tw, op=dist.ReduceOp.MAX)
@@ -201,9 +211,11 @@ def run_ours(args):
     import ctypes
     h2d = n_o * ctypes.sizeof(N.qsim_gate)
 
-    peak, peak_src = peaks()
+    hbm_peak, peak_src, sm_max = peaks()
     pass_ms = st["pass_ms"]
-    achieved = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
+    fp64_peak = 2.0 * FP64_FMA_PER_CLK_PER_SM * N_SM * sm_max * 1e6 / 1e12  # TFLOP/s
+    fp64_ach = (2.0 * st["pass_fp64_slots"] / (pass_ms / 1e3) / 1e12) if pass_ms > 0 else None
+    hbm_ach = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tp):
@@ -219,13 +231,19 @@ def run_ours(args):
                        "l2": "state %d MiB per GPU > 126 MB L2 (no flush needed)" % ((16 << (n - G)) >> 20)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n},
             "gpu_launches": int(st["kernel_launches"]),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_pass", "peak_source": peak_src,
+            "roofline": {"bound": "alu", "achieved": fp64_ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": (fp64_ach / fp64_peak) if fp64_ach else None, "traffic": traffic,
+                         "kernel": "qsim_pass (NVRTC pass-specialised k_pass)",
+                         "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x %.0f MHz" % sm_max,
                          "launches": int(st["passes"]), "kernel_ms": pass_ms,
-                         "kernel_share_of_step": pass_ms / ms if ms > 0 else None},
+                         "kernel_share_of_step": pass_ms / ms if ms > 0 else None,
+                         "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": (hbm_ach / hbm_peak) if hbm_ach else None, "peak_source": peak_src,
+                                 "bytes_per_launch": 32 << (n - G)}},
             "clocks": ck,
             "detail": {"passes_per_step": st["passes"] / args.steps, "plan_ms_per_step": st["plan_ms"] / args.steps,
+                       "jit_passes_per_step": st["jit_launches"] / args.steps,
+                       "plan_cache_hits": int(st["plan_cache_hits"]),
                        "exchanges_per_step": st["exchanges"] / args.steps,
                        "reduce_ms_per_step": st["reduce_ms"] / args.steps},
         }

@@ -210,6 +210,8 @@ typedef struct {
     uint64_t jit_launches;     /* passes run by a pass-specialised (NVRTC) kernel */
     uint64_t jit_kernels;      /* specialised kernels in the process cache */
     double jit_compile_ms;     /* total NVRTC + module-load time in this process */
+    double pass_fp64_slots;    /* algorithmic FP64 FMA-pipe instructions of the launched passes */
+    uint64_t plan_cache_hits;  /* flushes that reused a cached plan */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);

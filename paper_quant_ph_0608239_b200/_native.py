@@ -42,7 +42,9 @@ class qsim_stats(ctypes.Structure):
                                               "plan_ms")] + [("pass_amp_bytes", ctypes.c_uint64),
                                                             ("jit_launches", ctypes.c_uint64),
                                                             ("jit_kernels", ctypes.c_uint64),
-                                                            ("jit_compile_ms", ctypes.c_double)]
+                                                            ("jit_compile_ms", ctypes.c_double),
+                                                            ("pass_fp64_slots", ctypes.c_double),
+                                                            ("plan_cache_hits", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

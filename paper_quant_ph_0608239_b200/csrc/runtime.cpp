@@ -29,6 +29,25 @@ struct TimedRange {
 
 }  // namespace
 
+// Last flush's plan: resubmitting the same gate list from the same layout
+// (e.g. every step of a benchmark or a repeated circuit) skips planning,
+// code-generation keys and parameter packing.
+struct PlanCache {
+    bool valid = false;
+    bool with_init = false;
+    std::vector<GateRec> queue;
+    std::vector<int> phys_before, phys_init, phys_after;
+    std::vector<Step> steps;
+    std::vector<std::string> jkeys;
+    std::vector<std::vector<std::vector<uint8_t>>> params;  // [step][shard]
+};
+
+static bool same_gate(const GateRec &a, const GateRec &b)
+{
+    return a.kind == b.kind && a.target == b.target && a.controls == b.controls && a.targets == b.targets &&
+           std::memcmp(a.u, b.u, sizeof(a.u)) == 0 && a.perm == b.perm;
+}
+
 struct qsim_ctx_s {
     int n = 0, P = 1, G = 0, M = 0, rank = 0, transport = QSIM_TRANSPORT_LOCAL;
     std::vector<double2 *> shards;
@@ -43,6 +62,8 @@ struct qsim_ctx_s {
     bool initialized = false, init_pending = false;
     uint64_t init_index = 0;
     std::vector<GateRec> queue;
+    PlanCache pc;
+    bool plan_cache = true;
     // device program buffers
     KOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
@@ -106,6 +127,22 @@ struct qsim_ctx_s {
         }                                                                                     \
         (ctx)->stats.kernel_launches++;                                                       \
     } while (0)
+
+// algorithmic FP64 FMA-pipe instructions of one pass over a 2^M shard: per
+// touched amplitude 8 for a complex 2x2, 4 for a real 2x2, 4 for a phase,
+// 0 for an exact swap; the predicate bits (controls) halve the touched set
+static double pass_fp64_slots(const Step &s, int M)
+{
+    double tot = 0;
+    for (const KOp &op : s.ops) {
+        if (op.code == OPC_TRANS || op.code == OPC_XS) continue;
+        const int pb = __builtin_popcount(op.mreg) + __builtin_popcount(op.mlane) + __builtin_popcount(op.mwarp) +
+                       __builtin_popcountll(op.mout);
+        const double per = op.code == OPC_U2 ? 8.0 : 4.0;
+        tot += per * std::ldexp(1.0, M - pb);
+    }
+    return tot;
+}
 
 static JitCache &jit_cache()
 {
@@ -460,8 +497,21 @@ static qsim_status flush(qsim_ctx c)
     if (!c->init_pending && c->queue.empty()) return QSIM_OK;
     if (!c->init_pending && !c->initialized) FAIL(c, QSIM_ERR_STATE, "gates queued before qsim_init_basis");
     auto t0 = std::chrono::steady_clock::now();
+    PlanCache &pc = c->pc;
+    bool hit = c->plan_cache && pc.valid && pc.with_init == c->init_pending && pc.queue.size() == c->queue.size() &&
+               (c->init_pending || pc.phys_before == c->planner->phys_of);
+    for (size_t i = 0; hit && i < c->queue.size(); i++) hit = same_gate(pc.queue[i], c->queue[i]);
+    if (!hit) pc.valid = false;
+    const bool with_init = c->init_pending;
+    if (!hit) pc.phys_before = c->planner->phys_of;
     if (c->init_pending) {
-        c->planner->choose_initial_layout(c->queue);
+        if (hit) {
+            c->planner->phys_of = pc.phys_init;
+            for (int q = 0; q < c->n; q++) c->planner->qubit_at[pc.phys_init[q]] = q;
+        } else {
+            c->planner->choose_initial_layout(c->queue);
+            pc.phys_init = c->planner->phys_of;
+        }
         uint64_t phys = 0;
         for (int q = 0; q < c->n; q++)
             if ((c->init_index >> q) & 1) phys |= 1ULL << c->planner->phys_of[q];
@@ -474,18 +524,33 @@ static qsim_status flush(qsim_ctx c)
         c->init_pending = false;
         c->initialized = true;
     }
-    std::vector<Step> steps;
-    PlanOptions opt;
-    opt.fusion = c->fusion;
-    opt.max_scan = c->max_scan;
-    c->planner->plan(c->queue, opt, steps);
-    c->queue.clear();
+    if (hit) {
+        c->planner->phys_of = pc.phys_after;
+        for (int q = 0; q < c->n; q++) c->planner->qubit_at[pc.phys_after[q]] = q;
+        c->queue.clear();
+        c->stats.plan_cache_hits++;
+    } else {
+        std::vector<Step> steps;
+        PlanOptions opt;
+        opt.fusion = c->fusion;
+        opt.max_scan = c->max_scan;
+        c->planner->plan(c->queue, opt, steps);
+        pc.steps = std::move(steps);
+        pc.queue.swap(c->queue);
+        c->queue.clear();
+        pc.with_init = with_init;
+        pc.phys_after = c->planner->phys_of;
+        pc.jkeys.assign(pc.steps.size(), std::string());
+        pc.params.assign(pc.steps.size(), {});
+        pc.valid = true;
+    }
     c->stats.flushes++;
     c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<Step> &steps = pc.steps;
     qsim_status st = upload_program(c, steps);
     if (st != QSIM_OK) return st;
-    std::vector<std::string> jkeys(steps.size());
-    if (c->jit) {
+    std::vector<std::string> &jkeys = pc.jkeys;
+    if (c->jit && !hit) {
         std::vector<const Step *> ps;
         for (const Step &s : steps)
             if (s.type == ST_PASS) ps.push_back(&s);
@@ -500,7 +565,6 @@ static qsim_status flush(qsim_ctx c)
             if (steps[i].type == ST_PASS) jkeys[i] = jit_key(steps[i]);
     }
     const int M = c->M;
-    std::vector<uint8_t> pbuf;
     for (size_t si = 0; si < steps.size(); si++) {
         const Step &s = steps[si];
         switch (s.type) {
@@ -510,9 +574,11 @@ static qsim_status flush(qsim_ctx c)
             for (int i = 0; i < n_local(c); i++) {
                 const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
                 if (fn) {
-                    jit_pack_params(s, c->shards[i], rb, pbuf);
-                    size_t sz = pbuf.size();
-                    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pbuf.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
+                    auto &pp = pc.params[si];
+                    if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
+                    if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
+                    size_t sz = pp[i].size();
+                    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                                      CU_LAUNCH_PARAM_END};
                     const unsigned smem = s.pass.use_smem ? kTileAmps * 16 : 0;
                     CUresult cr = drv().launchKernel(fn, (unsigned)s.pass.n_inst, 1, 1, kPassThreads, 1, 1, smem,
@@ -529,6 +595,7 @@ static qsim_status flush(qsim_ctx c)
                 }
                 LAUNCHED(c);
                 c->stats.passes++;
+                c->stats.pass_fp64_slots += pass_fp64_slots(s, M);
             }
             break;
         }
@@ -1010,12 +1077,13 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     GUARD(c);
     if (!key) return QSIM_ERR_ARG;
     std::string k(key);
-    if (k == "fusion") c->fusion = value != 0;
+    if (k == "fusion") { c->fusion = value != 0; c->pc.valid = false; }
     else if (k == "timing") c->timing = value != 0;
-    else if (k == "max_scan") c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30);
+    else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
-    else if (k == "jit") c->jit = value != 0;
+    else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
+    else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }
     else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
     return QSIM_OK;
 }
