@@ -227,6 +227,15 @@ const char *qsim_last_error(qsim_ctx ctx);
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
                            int fusion, char *buf, size_t buf_bytes);
 
+/* Host-only exchange routing of a K-pair remap ("we first compute
+ * the ranks of the other MPI processes with which the MPI process has to
+ * communicate"): the remap swaps local bits l_i with nonlocal physical bits
+ * gpos[i]; chunk v of `rank` (the amplitudes whose l-bits equal v) goes to
+ * peers[v] (2^K entries), and *self_v is the chunk that stays.  Used by the
+ * NCCL exchange and by the CPU (gloo) tests of the sharded path. */
+qsim_status qsim_exchange_peers(int n_qubits, int n_ranks, int rank, const int *gpos, int K, int *peers,
+                                int *self_v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,7 +55,7 @@ EXPORTS = [
     "qsim_init_basis", "qsim_apply_1q", "qsim_apply_controlled", "qsim_apply_perm", "qsim_apply_swap",
     "qsim_remap", "qsim_run_circuit", "qsim_probabilities", "qsim_expectations", "qsim_measure",
     "qsim_get_amplitudes", "qsim_sync", "qsim_get_layout", "qsim_set_option", "qsim_get_stats",
-    "qsim_reset_stats", "qsim_status_str", "qsim_last_error", "qsim_plan_json",
+    "qsim_reset_stats", "qsim_status_str", "qsim_last_error", "qsim_plan_json", "qsim_exchange_peers",
 ]
 
 _lib = None
@@ -97,6 +97,7 @@ def lib():
         "qsim_status_str": ([st], ctypes.c_char_p),
         "qsim_last_error": ([ctx], ctypes.c_char_p),
         "qsim_plan_json": ([i, i, P(qsim_gate), ctypes.c_size_t, i, ctypes.c_char_p, ctypes.c_size_t], st),
+        "qsim_exchange_peers": ([i, i, i, P(i), i, P(i), P(i)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

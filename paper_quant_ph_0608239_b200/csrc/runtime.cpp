@@ -1109,6 +1109,20 @@ qsim_status qsim_reset_stats(qsim_ctx c)
     return QSIM_OK;
 }
 
+qsim_status qsim_exchange_peers(int n_qubits, int n_ranks, int rank, const int *gpos, int K, int *peers, int *self_v)
+{
+    if (n_ranks < 1 || (n_ranks & (n_ranks - 1)) || rank < 0 || rank >= n_ranks || K < 0 || K > 6 ||
+        (K && (!gpos || !peers)) || !self_v)
+        return QSIM_ERR_ARG;
+    const int M = n_qubits - ilog2(n_ranks);
+    std::vector<int> g(gpos, gpos + K);
+    for (int i = 0; i < K; i++)
+        if (g[i] < M || g[i] >= n_qubits) return QSIM_ERR_QUBIT_RANGE;
+    *self_v = (int)rank_sub((uint64_t)rank, g, M);
+    for (uint64_t v = 0; v < (1ULL << K); v++) peers[v] = (int)with_sub((uint64_t)rank, g, M, v);
+    return QSIM_OK;
+}
+
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates, int fusion, char *buf,
                            size_t buf_bytes)
 {

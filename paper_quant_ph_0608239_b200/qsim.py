@@ -89,6 +89,18 @@ def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1) -> str:
         raise QsimError(s, "qsim_plan_json")
 
 
+def exchange_peers(n: int, n_ranks: int, rank: int, gpos: Sequence[int]):
+    """Host-only routing of a K-pair remap: (peer rank per chunk value, own chunk value)."""
+    K = len(gpos)
+    g = (ctypes.c_int * max(1, K))(*gpos)
+    peers = (ctypes.c_int * (1 << K))()
+    selfv = ctypes.c_int()
+    s = N.lib().qsim_exchange_peers(n, n_ranks, rank, g, K, peers, ctypes.byref(selfv))
+    if s != 0:
+        raise QsimError(s, "qsim_exchange_peers")
+    return list(peers), selfv.value
+
+
 class QSim:
     """One context of the engine.
 
