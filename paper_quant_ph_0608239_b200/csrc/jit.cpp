@@ -25,8 +25,16 @@ int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
 struct Layout {
     int n_out = 0, n_m = 0;
-    size_t off_out = 160, off_m = 0, bytes = 0;
+    size_t off_out = 176, off_m = 0, bytes = 0;
 };
+
+// generator variants (env, for A/B experiments): minimum CTAs per SM and
+// persistent grid with L2 prefetch of the next tile
+int env_int(const char *k, int dflt)
+{
+    const char *v = getenv(k);
+    return v ? atoi(v) : dflt;
+}
 
 Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_idx)
 {
@@ -51,15 +59,21 @@ JitPass jit_generate(const Step &st)
     std::vector<int> out_idx, m_idx;
     Layout L = layout_of(st, out_idx, m_idx);
     std::ostringstream s;
-    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long tpm[12]; "
-         "int ts[12]; unsigned long long out["
+    const int minb = env_int("QSIM_JIT_MINB", 2), pf = env_int("QSIM_JIT_PREFETCH", 0);
+    const int loop = env_int("QSIM_JIT_PERSIST", 0) > 0;
+    s << "// minb=" << minb << " prefetch=" << pf << " loop=" << loop << "\n";
+    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
+         "unsigned long long pad; unsigned long long tpm[12]; int ts[12]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsim_pass(const __grid_constant__ JP P)\n{\n";
+    s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
+         "#pragma unroll\n for (int j = 0; j < 12; j++) { const int t = ts[j]; "
+         "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
     s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    s << " unsigned long long base = blockIdx.x;\n";
-    s << "#pragma unroll\n for (int j = 0; j < 12; j++) { const int t = P.ts[j]; "
-         "base = ((base >> t) << (t + 1)) | (base & ((1ULL << t) - 1)); }\n";
+    if (loop) s << " for (unsigned long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {\n";
+    else s << " { const unsigned long long inst = blockIdx.x;\n";
+    s << " const unsigned long long base = qdep(inst, P.ts);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     int reg[16];
@@ -86,6 +100,12 @@ JitPass jit_generate(const Step &st)
              "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
           << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
           << " = make_double2(x2, x3); }\n";
+    if (pf && loop) {
+        s << "  if ((lane & 3) == 0 && inst + gridDim.x < P.n_inst) {\n";
+        s << "   const double2 *q = P.st + qdep(inst + gridDim.x, P.ts) + (" << gaddr(cur) << ");\n";
+        for (int j = 0; j < 8; j++) s << "   asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(q + (" << roff(cur, j) << ")));\n";
+        s << "  }\n";
+    }
     s << " }\n";
     auto smem_z = [&](uint64_t c, const char *tag) {
         s << "  const int zt" << tag << " = ";
@@ -191,6 +211,8 @@ JitPass jit_generate(const Step &st)
         s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + (" << roff(cur, j) << ")), \"d\"("
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
+    s << " }\n";
+    if (loop) s << " __syncthreads();\n";
     s << " }\n}\n";
     JitPass jp;
     jp.src = s.str();
@@ -206,10 +228,11 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     uint8_t *b = buf.data();
     std::memcpy(b + 0, &state, 8);
     std::memcpy(b + 8, &rank_bits, 8);
+    std::memcpy(b + 16, &st.pass.n_inst, 8);
     for (int t = 0; t < kTileBits; t++) {
         const uint64_t m = 1ULL << st.pass.tp[t];
-        std::memcpy(b + 16 + 8 * t, &m, 8);
-        std::memcpy(b + 112 + 4 * t, &st.pass.tile_sorted[t], 4);
+        std::memcpy(b + 32 + 8 * t, &m, 8);
+        std::memcpy(b + 128 + 4 * t, &st.pass.tile_sorted[t], 4);
     }
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
@@ -312,6 +335,8 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
+    put((uint64_t)env_int("QSIM_JIT_MINB", 2) | ((uint64_t)env_int("QSIM_JIT_PREFETCH", 0) << 8) |
+        ((uint64_t)(env_int("QSIM_JIT_PERSIST", 0) > 0) << 16));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
@@ -379,12 +404,25 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
     return true;
 }
 
+static void dump_source(const std::string &src, size_t idx)
+{
+    const char *d = getenv("QSIM_JIT_DUMP");
+    if (!d) return;
+    std::string path = std::string(d) + "/qsim_pass_" + std::to_string(idx) + ".cu";
+    if (FILE *f = fopen(path.c_str(), "w")) {
+        fwrite(src.data(), 1, src.size(), f);
+        fclose(f);
+    }
+}
+
 bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms)
 {
     auto t0 = std::chrono::steady_clock::now();
     std::vector<std::string> keys, srcs;
-    for (const Step *st : steps) {
+    for (size_t i = 0; i < steps.size(); i++) {
+        const Step *st = steps[i];
         std::string k = jit_key(*st);
+        dump_source(jit_generate(*st).src, i);
         if (std::find(keys.begin(), keys.end(), k) != keys.end()) continue;
         keys.push_back(k);
         srcs.push_back(jit_generate(*st).src);
