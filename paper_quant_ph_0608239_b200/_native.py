@@ -6,7 +6,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqsim_b200.so")
+LIB_PATH = os.environ.get("QSIM_LIB") or os.path.join(HERE, "libqsim_b200.so")
 
 QSIM_MAX_CONTROLS = 8
 QSIM_MAX_PERM_TARGETS = 12

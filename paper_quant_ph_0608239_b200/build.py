@@ -44,7 +44,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     nccl = nccl_dir()
-    inc = ["-I", CSRC, "-I", INCLUDE, "-I", os.path.join(nccl, "include"), "-I", os.path.join(CUDA, "include")]
+    tile = os.environ.get("QSB_TILE_BITS")
+    defs = ["-DQSB_TILE_BITS=" + tile] if tile else []
+    inc = [*defs, "-I", CSRC, "-I", INCLUDE, "-I", os.path.join(nccl, "include"), "-I", os.path.join(CUDA, "include")]
     objs = []
     cmds = []
     for f in sorted(os.listdir(CSRC)):

@@ -16,15 +16,21 @@
 // moves the tile to another config through XOR-swizzled shared memory.
 // Load/store configs have r[0] = 0, l[0] = 1, l[1] = 2 (256-bit accesses of
 // amplitude pairs, whole 128-B lines per 4 lanes).
-// A config is packed in 12 nibbles: r0 r1 r2 r3 l0 l1 l2 l3 l4 w0 w1 w2.
+// A config is packed in nibbles: r0 r1 r2 r3 l0 l1 l2 l3 l4 w0 .. w(kWarpBits-1).
 #pragma once
 #include <cstdint>
 
 namespace qsb {
 
-constexpr int kTileBits = 12;
+#ifndef QSB_TILE_BITS
+#define QSB_TILE_BITS 12
+#endif
+constexpr int kTileBits = QSB_TILE_BITS;      // tile = 3 fixed low bits + 9 free bits (+ warp bits)
 constexpr int kTileAmps = 1 << kTileBits;
-constexpr int kPassThreads = 256;
+constexpr int kWarpBits = kTileBits - 9;      // 4 register bits + 5 lane bits + warp bits
+constexpr int kPassThreads = 32 << kWarpBits;
+constexpr int kPermTileBits = 12;             // k_perm tile (targets + low bits)
+constexpr int kPermTileAmps = 1 << kPermTileBits;
 constexpr int kAmpsPerThread = 16;
 // ops of one pass travel in the kernel parameter block (<= 32 KB on sm_100)
 constexpr int kMaxPassOps = 240;
@@ -84,8 +90,8 @@ struct PermDesc {
     int32_t t;           // target bits = tile-local bits 0..t-1 (register order)
     int32_t tile_bits;   // total tile bits (t + extras)
     int32_t perm_offset; // into the device perm-table array (uint32 entries)
-    int32_t tile_pos[kTileBits];    // physical position of tile-local bit b
-    int32_t tile_sorted[kTileBits]; // same positions sorted ascending
+    int32_t tile_pos[kPermTileBits];    // physical position of tile-local bit b
+    int32_t tile_sorted[kPermTileBits]; // same positions sorted ascending
 };
 
 }  // namespace qsb

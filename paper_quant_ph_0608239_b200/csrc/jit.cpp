@@ -23,9 +23,11 @@ namespace {
 int nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
 int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
+constexpr size_t kOffTpm = 32, kOffTs = kOffTpm + 8 * kTileBits;
+
 struct Layout {
     int n_out = 0, n_m = 0;
-    size_t off_out = 176, off_m = 0, bytes = 0;
+    size_t off_out = (kOffTs + 4 * kTileBits + 15) / 16 * 16, off_m = 0, bytes = 0;
 };
 
 // generator variants (env, for A/B experiments): minimum CTAs per SM and
@@ -59,16 +61,18 @@ JitPass jit_generate(const Step &st)
     std::vector<int> out_idx, m_idx;
     Layout L = layout_of(st, out_idx, m_idx);
     std::ostringstream s;
-    const int minb = env_int("QSIM_JIT_MINB", 2), pf = env_int("QSIM_JIT_PREFETCH", 0);
+    const int minb = env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2), pf = env_int("QSIM_JIT_PREFETCH", 0);
     const int loop = env_int("QSIM_JIT_PERSIST", 0) > 0;
     s << "// minb=" << minb << " prefetch=" << pf << " loop=" << loop << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
-         "unsigned long long pad; unsigned long long tpm[12]; int ts[12]; unsigned long long out["
+         "unsigned long long pad; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
+      << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
-         "#pragma unroll\n for (int j = 0; j < 12; j++) { const int t = ts[j]; "
+         "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
          "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads << ", " << minb
+      << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
     s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
     if (loop) s << " for (unsigned long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {\n";
@@ -83,7 +87,7 @@ JitPass jit_generate(const Step &st)
         std::ostringstream g;
         g << "(unsigned long long)((lane & 3) << 1)";
         for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? P.tpm[" << nib(c, 4 + j) << "] : 0ULL)";
-        for (int j = 0; j < 3; j++) g << " | (((warp >> " << j << ") & 1) ? P.tpm[" << nib(c, 9 + j) << "] : 0ULL)";
+        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? P.tpm[" << nib(c, 9 + j) << "] : 0ULL)";
         return g.str();
     };
     auto roff = [&](uint64_t c, int j) {
@@ -110,7 +114,8 @@ JitPass jit_generate(const Step &st)
     auto smem_z = [&](uint64_t c, const char *tag) {
         s << "  const int zt" << tag << " = ";
         for (int j = 0; j < 5; j++) s << "(((lane >> " << j << ") & 1) << " << nib(c, 4 + j) << ") | ";
-        for (int j = 0; j < 3; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, 9 + j) << ")" << (j < 2 ? " | " : ";\n");
+        for (int j = 0; j < kWarpBits; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, 9 + j) << ") | ";
+        s << "0;\n";
         s << "  const int zz" << tag << " = zt" << tag << " ^ (((zt" << tag << " >> 3) ^ (zt" << tag << " >> 6) ^ (zt"
           << tag << " >> 9)) & 7);\n";
     };
@@ -231,8 +236,8 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     std::memcpy(b + 16, &st.pass.n_inst, 8);
     for (int t = 0; t < kTileBits; t++) {
         const uint64_t m = 1ULL << st.pass.tp[t];
-        std::memcpy(b + 32 + 8 * t, &m, 8);
-        std::memcpy(b + 128 + 4 * t, &st.pass.tile_sorted[t], 4);
+        std::memcpy(b + kOffTpm + 8 * t, &m, 8);
+        std::memcpy(b + kOffTs + 4 * t, &st.pass.tile_sorted[t], 4);
     }
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
@@ -335,7 +340,7 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", 2) | ((uint64_t)env_int("QSIM_JIT_PREFETCH", 0) << 8) |
+    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2) | ((uint64_t)env_int("QSIM_JIT_PREFETCH", 0) << 8) |
         ((uint64_t)(env_int("QSIM_JIT_PERSIST", 0) > 0) << 16));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {

@@ -141,7 +141,7 @@ __device__ __forceinline__ void smem_coords(uint64_t c, int lane, int warp, int 
 #pragma unroll
     for (int j = 0; j < 5; j++) st |= ((lane >> j) & 1) << cfg_nib(c, 4 + j);
 #pragma unroll
-    for (int j = 0; j < 3; j++) st |= ((warp >> j) & 1) << cfg_nib(c, 9 + j);
+    for (int j = 0; j < kWarpBits; j++) st |= ((warp >> j) & 1) << cfg_nib(c, 9 + j);
     zt = swz(st);
 #pragma unroll
     for (int j = 0; j < 4; j++) zr[j] = swz(1 << cfg_nib(c, j));
@@ -174,7 +174,7 @@ __device__ __forceinline__ void global_coords(const PassDesc &d, uint64_t c, int
 #pragma unroll
     for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << d.tp[cfg_nib(c, 4 + j)];
 #pragma unroll
-    for (int j = 0; j < 3; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, 9 + j)];
+    for (int j = 0; j < kWarpBits; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, 9 + j)];
     g1 = 1ULL << d.tp[cfg_nib(c, 1)];
     g2 = 1ULL << d.tp[cfg_nib(c, 2)];
     g3 = 1ULL << d.tp[cfg_nib(c, 3)];
@@ -283,14 +283,15 @@ static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cud
 
 void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s)
 {
-    if (variant == 1) launch_pass_minb<1>(d, ops, st, s);
-    else launch_pass_minb<2>(d, ops, st, s);
+    constexpr int kMinB = 8192 / kTileAmps;  // 2 CTAs of 256 threads, or 4 of 128 (<= 128 registers)
+    if (variant == 1) launch_pass_minb<kMinB / 2>(d, ops, st, s);
+    else launch_pass_minb<kMinB>(d, ops, st, s);
 }
 
 int pass_regs_per_thread()
 {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, (k_pass<kMaxPassOps, 1>)) != cudaSuccess) return -1;
+    if (cudaFuncGetAttributes(&fa, (k_pass<kMaxPassOps, 8192 / kTileAmps>)) != cudaSuccess) return -1;
     return fa.numRegs;
 }
 
@@ -382,7 +383,7 @@ void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaS
 {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileAmps * (int)sizeof(double2));
+        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPermTileAmps * (int)sizeof(double2));
         attr = true;
     }
     k_perm<<<(unsigned)d.n_inst, 256, (1 << d.tile_bits) * (int)sizeof(double2), s>>>(d, st, perm_tab);

@@ -121,12 +121,13 @@ static void set_u2_code(const GateRec &g, POp &p)
 namespace {
 // thread-coordinate assignment of the 12 tile-local bits (see engine.h)
 struct Cfg {
-    int r[4], l[5], w[3];
+    int r[4], l[5], w[kWarpBits];
     uint64_t pack() const
     {
         uint64_t c = 0;
-        int v[12] = {r[0], r[1], r[2], r[3], l[0], l[1], l[2], l[3], l[4], w[0], w[1], w[2]};
-        for (int j = 0; j < 12; j++) c |= (uint64_t)v[j] << (4 * j);
+        for (int j = 0; j < 4; j++) c |= (uint64_t)r[j] << (4 * j);
+        for (int j = 0; j < 5; j++) c |= (uint64_t)l[j] << (4 * (4 + j));
+        for (int j = 0; j < kWarpBits; j++) c |= (uint64_t)w[j] << (4 * (9 + j));
         return c;
     }
     bool store_ok() const { return r[0] == 0 && l[0] == 1 && l[1] == 2; }
@@ -136,7 +137,7 @@ struct Cfg {
             if (r[j] == t) return ROLE_REG;
         for (j = 0; j < 5; j++)
             if (l[j] == t) return ROLE_LANE;
-        for (j = 0; j < 3; j++)
+        for (j = 0; j < kWarpBits; j++)
             if (w[j] == t) return ROLE_WARP;
         j = -1;
         return -1;
@@ -331,7 +332,7 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
         int t = phys_of[g.target];
         if (t >= M) { block(); continue; }
         if (!in_tile[t]) {
-            if ((int)freeb.size() >= 9) { block(); continue; }
+            if ((int)freeb.size() >= kTileBits - 3) { block(); continue; }
             in_tile[t] = true;
             freeb.push_back(t);
         }
@@ -350,7 +351,7 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
             order.push_back(p.t);
     for (int b : freeb)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
-    for (int p = 3; (int)order.size() < 9 && p < M; p++)
+    for (int p = 3; (int)order.size() < kTileBits - 3 && p < M; p++)
         if (!in_tile[p]) { in_tile[p] = true; order.push_back(p); }
 
     Step st;
@@ -359,7 +360,7 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     int tl_of[64];
     for (int b = 0; b < 64; b++) tl_of[b] = -1;
     for (int t = 0; t < 3; t++) { d.tp[t] = t; tl_of[t] = t; }
-    for (int j = 0; j < 9; j++) { d.tp[3 + j] = order[j]; tl_of[order[j]] = 3 + j; }
+    for (int j = 0; j < kTileBits - 3; j++) { d.tp[3 + j] = order[j]; tl_of[order[j]] = 3 + j; }
     uint64_t cfg0 = 0;
     lower_pass(pops, tl_of, st, cfg0);
     d.cfg0 = cfg0;

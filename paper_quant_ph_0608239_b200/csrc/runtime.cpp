@@ -457,7 +457,7 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
 {
     PermDesc d{};
     const int M = c->M, t = (int)s.ptargets.size();
-    int tb = std::min(kTileBits, M);
+    int tb = std::min(kPermTileBits, M);
     if (tb < t) tb = t;
     d.M = M;
     d.t = t;
@@ -468,7 +468,7 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     int nb = t;
     for (int p = 0; p < M && nb < tb; p++)
         if (!used[p]) { d.tile_pos[nb++] = p; used[p] = true; }
-    int srt[kTileBits];
+    int srt[kPermTileBits];
     for (int i = 0; i < tb; i++) srt[i] = d.tile_pos[i];
     std::sort(srt, srt + tb);
     for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
