@@ -27,7 +27,7 @@ constexpr size_t kOffTpm = 32, kOffTs = kOffTpm + 8 * kTileBits;
 
 struct Layout {
     int n_out = 0, n_m = 0;
-    size_t off_out = (kOffTs + 4 * kTileBits + 15) / 16 * 16, off_m = 0, bytes = 0;
+    size_t off_out = (kOffTs + 4 * kTileBits + 7) / 8 * 8, off_m = 0, bytes = 0;  // natural u64 alignment
 };
 
 // generator variants (env, for A/B experiments): minimum CTAs per SM and
