@@ -29,7 +29,8 @@ constexpr int kTileBits = QSB_TILE_BITS;      // tile = 3 fixed low bits + 9 fre
 constexpr int kTileAmps = 1 << kTileBits;
 constexpr int kWarpBits = kTileBits - 9;      // 4 register bits + 5 lane bits + warp bits
 constexpr int kPassThreads = 32 << kWarpBits;
-constexpr int kPermTileBits = 12;             // k_perm tile (targets + low bits)
+constexpr int kPermTileBits = 12;
+constexpr int kPhaseRunMin = 4;             // k_perm tile (targets + low bits)
 constexpr int kPermTileAmps = 1 << kPermTileBits;
 constexpr int kAmpsPerThread = 16;
 // ops of one pass travel in the kernel parameter block (<= 32 KB on sm_100)
@@ -40,7 +41,14 @@ enum OpCode : int32_t {
     OPC_U2R = 1,    // real 2x2 (imaginary parts zero), e.g. Hadamard
     OPC_XS = 2,     // exact [[0,1],[1,0]]: conditional swap (CNOT/Toffoli target)
     OPC_PHASE = 3,  // multiply by f = m[0] + i m[1] where the predicate holds
-    OPC_TRANS = 4   // re-layout the tile to config `cfg` through shared memory
+    OPC_TRANS = 4,  // re-layout the tile to config `cfg` through shared memory
+    // A run of >= kPhaseRunMin consecutive phases: OPC_PHASE_ACC ops add their
+    // angle (cfg = round(phi / 2pi * 2^64), exact mod 2pi) to per-register
+    // integer accumulators; OPC_PHASE_FLUSH multiplies each amplitude once by
+    // e^{i theta} (JIT tier).  The interpreter applies OPC_PHASE_ACC like
+    // OPC_PHASE (same m[0], m[1]) and ignores OPC_PHASE_FLUSH.
+    OPC_PHASE_ACC = 5,
+    OPC_PHASE_FLUSH = 6
 };
 
 enum Role : int32_t { ROLE_REG = 0, ROLE_LANE = 1, ROLE_WARP = 2, ROLE_OUT = 3 };

@@ -45,7 +45,7 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
     m_idx.assign(st.ops.size(), -1);
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
-        if (op.code == OPC_TRANS) continue;
+        if (op.code == OPC_TRANS || op.code == OPC_PHASE_FLUSH) continue;
         if (op.mout) out_idx[o] = L.n_out++;
         if (op.code != OPC_XS) m_idx[o] = L.n_m++;
     }
@@ -125,6 +125,7 @@ JitPass jit_generate(const Step &st)
             if ((i >> b) & 1) z ^= swz_host(1 << nib(c, b));
         return z;
     };
+    bool acc_used[16] = {false}, in_run = false;
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
@@ -138,6 +139,22 @@ JitPass jit_generate(const Step &st)
             s << "  __syncthreads();\n }\n";
             continue;
         }
+        if (op.code == OPC_PHASE_FLUSH) {
+            for (int v = 0; v < 16; v++)
+                if (acc_used[v])
+                    s << "  { double sn, cs; sincospi((double)th" << v << " * 0x1p-63, &sn, &cs); const double p1 = -sn * a"
+                      << v << ".y, p2 = sn * a" << v << ".x; a" << v << ".x = fma(cs, a" << v << ".x, p1); a" << v
+                      << ".y = fma(cs, a" << v << ".y, p2); }\n";
+            s << " }\n";
+            in_run = false;
+            continue;
+        }
+        if (op.code == OPC_PHASE_ACC && !in_run) {
+            s << " { unsigned long long th0 = 0, th1 = 0, th2 = 0, th3 = 0, th4 = 0, th5 = 0, th6 = 0, th7 = 0, th8 = 0, "
+                 "th9 = 0, th10 = 0, th11 = 0, th12 = 0, th13 = 0, th14 = 0, th15 = 0;\n";
+            for (int v = 0; v < 16; v++) acc_used[v] = false;
+            in_run = true;
+        }
         const bool plw = op.mlane || op.mwarp;  // thread-dependent predicate
         const bool pout = op.mout != 0;         // CTA-uniform predicate
         std::ostringstream pr;
@@ -150,7 +167,15 @@ JitPass jit_generate(const Step &st)
         if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
         if (pout && !sel) s << "  if (tp) {\n";
         const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
-        if (op.code == OPC_PHASE) {
+        if (op.code == OPC_PHASE_ACC) {
+            s << "  const unsigned long long K = " << (sel ? "tp ? " : "") << "(unsigned long long)__double_as_longlong("
+              << M << "[2])" << (sel ? " : 0ULL" : "") << ";\n";
+            for (int i = 0; i < 16; i++) {
+                if ((i & op.mreg) != op.vreg) continue;
+                s << "  th" << reg[i] << " += K;\n";
+                acc_used[reg[i]] = true;
+            }
+        } else if (op.code == OPC_PHASE) {
             for (int i = 0; i < 16; i++) {
                 if ((i & op.mreg) != op.vreg) continue;
                 const std::string v = A(i);
@@ -245,7 +270,10 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             std::memcpy(b + L.off_out + 16 * out_idx[o], &op.mout, 8);
             std::memcpy(b + L.off_out + 16 * out_idx[o] + 8, &op.vout, 8);
         }
-        if (m_idx[o] >= 0) std::memcpy(b + L.off_m + 64 * m_idx[o], op.m, 64);
+        if (m_idx[o] >= 0) {
+            std::memcpy(b + L.off_m + 64 * m_idx[o], op.m, 64);
+            if (op.code == OPC_PHASE_ACC) std::memcpy(b + L.off_m + 64 * m_idx[o] + 16, &op.cfg, 8);  // angle
+        }
     }
 }
 

@@ -226,11 +226,12 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
             __syncthreads();
             continue;
         }
+        if (code == OPC_PHASE_FLUSH) continue;
         const bool tp = ((lane & op.mlane) == op.vlane) && ((warp & op.mwarp) == op.vwarp) &&
                         ((gcta & op.mout) == op.vout);
         if (!tp) continue;
         const uint32_t mreg = op.mreg, vreg = op.vreg;
-        if (code == OPC_PHASE) {
+        if (code == OPC_PHASE || code == OPC_PHASE_ACC) {
             const double fr = op.m[0], fi = op.m[1];
 #pragma unroll
             for (int i = 0; i < 16; i++) {

@@ -269,6 +269,30 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         done[pick] = 1;
         left--;
     }
+    // mark runs of consecutive phases for angle accumulation (JIT tier)
+    for (size_t a = 0; a < st.ops.size();) {
+        size_t b = a;
+        while (b < st.ops.size() && st.ops[b].code == OPC_PHASE) b++;
+        if (b - a >= (size_t)kPhaseRunMin) {
+            for (size_t o = a; o < b; o++) {
+                KOp &op = st.ops[o];
+                op.code = OPC_PHASE_ACC;
+                double t = std::atan2(op.m[1], op.m[0]) / (2.0 * M_PI);  // turns in (-1/2, 1/2]
+                if (t < 0) t += 1.0;
+                const long double scaled = (long double)t * 18446744073709551616.0L;
+                op.cfg = scaled >= 18446744073709551615.0L ? 0 : (uint64_t)(scaled + 0.5L);
+            }
+            KOp fl{};
+            fl.code = OPC_PHASE_FLUSH;
+            st.ops.insert(st.ops.begin() + b, fl);
+            st.op_gate.insert(st.op_gate.begin() + b, -1);
+            st.op_t.insert(st.op_t.begin() + b, -1);
+            st.op_cm.insert(st.op_cm.begin() + b, 0);
+            st.op_cv.insert(st.op_cv.begin() + b, 0);
+            b++;
+        }
+        a = b == a ? a + 1 : b;
+    }
     if (!cfg.store_ok()) {
         std::vector<int> r2;
         for (int k = 0; k < 4; k++)

@@ -135,7 +135,7 @@ static double pass_fp64_slots(const Step &s, int M)
 {
     double tot = 0;
     for (const KOp &op : s.ops) {
-        if (op.code == OPC_TRANS || op.code == OPC_XS) continue;
+        if (op.code == OPC_TRANS || op.code == OPC_XS || op.code == OPC_PHASE_FLUSH) continue;
         const int pb = __builtin_popcount(op.mreg) + __builtin_popcount(op.mlane) + __builtin_popcount(op.mwarp) +
                        __builtin_popcountll(op.mout);
         const double per = op.code == OPC_U2 ? 8.0 : 4.0;

@@ -10,8 +10,10 @@ import numpy as np
 
 
 def _apply(psi, idx, code, t, cm, cv, m):
+    if code == 6:  # phase-run flush marker
+        return
     sel = (idx & cm) == cv
-    if code == 3:  # PHASE
+    if code in (3, 5):  # PHASE / PHASE_ACC
         psi[sel] *= complex(m[0], m[1])
         return
     tb = 1 << t
@@ -44,7 +46,7 @@ def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
         ty = st["type"]
         if ty == "pass":
             for op in st["ops"]:
-                if op["code"] == 4:
+                if op["code"] in (4, 6):
                     continue
                 _apply(psi, idx, op["code"], op["t"], op["cm"], op["cv"], op["m"])
         elif ty == "generic":

@@ -27,8 +27,10 @@ def _free_port():
 
 
 def _apply(shard, full, code, t, cm, cv, m):
+    if code == 6:
+        return
     sel = (full & cm) == cv
-    if code == 3:
+    if code in (3, 5):
         shard[sel] *= complex(m[0], m[1])
         return
     tb = 1 << t
@@ -77,7 +79,7 @@ def _worker(rank, world, port, case, out_q):
             ty = st["type"]
             if ty == "pass":
                 for op in st["ops"]:
-                    if op["code"] != 4:
+                    if op["code"] not in (4, 6):
                         _apply(shard, full, op["code"], op["t"], op["cm"], op["cv"], op["m"])
             elif ty == "generic":
                 _apply(shard, full, st["code"], st["t"], st["cm"], st["cv"], st["m"])
