@@ -98,6 +98,7 @@ struct PermDesc {
     int32_t t;           // target bits = tile-local bits 0..t-1 (register order)
     int32_t tile_bits;   // total tile bits (t + extras)
     int32_t perm_offset; // into the device perm-table array (uint32 entries)
+    int32_t contiguous;  // tile_pos[b] == b for all b (offset == tile index)
     int32_t tile_pos[kPermTileBits];    // physical position of tile-local bit b
     int32_t tile_sorted[kPermTileBits]; // same positions sorted ascending
 };

@@ -370,13 +370,34 @@ __global__ void __launch_bounds__(256) k_perm(const __grid_constant__ PermDesc d
     for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
     if (((d.rank_bits | base) & d.m_ctrl_out) != d.v_ctrl_out) return;
     const uint32_t E = 1u << d.tile_bits, T = (1u << d.t) - 1;
+    const uint32_t *perm = perm_tab + d.perm_offset;
+    if (d.contiguous) {
+        // tile = the low tile_bits physical bits in order (the usual case: the
+        // initial layout puts permutation targets lowest): offset == index
+        const double2 *src = st + base;
+        for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
+            double2 x0, x1;
+            ld256(src + e, x0, x1);
+            sm[e] = x0;
+            sm[e + 1] = x1;
+        }
+        __syncthreads();
+        // gather with the inverse permutation: coalesced 256-bit stores; pairs
+        // (e, e+1) differ in target bit 0 only, so they share the control test
+        double2 *dst = st + base;
+        for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
+            if ((e & d.m_ctrl_tile) != d.v_ctrl_tile) continue;
+            const double2 y0 = sm[(e & ~T) | __ldg(perm + (e & T))];
+            const double2 y1 = sm[((e + 1) & ~T) | __ldg(perm + ((e + 1) & T))];
+            st256(dst + e, y0, y1);
+        }
+        return;
+    }
     for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) sm[e] = st[base + dep_tile(e, d.tile_pos, d.tile_bits)];
     __syncthreads();
-    const uint32_t *perm = perm_tab + d.perm_offset;
     for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
         if ((e & d.m_ctrl_tile) != d.v_ctrl_tile) continue;
-        const uint32_t dst = (e & ~T) | perm[e & T];
-        st[base + dep_tile(dst, d.tile_pos, d.tile_bits)] = sm[e];
+        st[base + dep_tile(e, d.tile_pos, d.tile_bits)] = sm[(e & ~T) | perm[e & T]];
     }
 }
 

@@ -439,7 +439,8 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
     size_t p = 0;
     for (Step &s : steps) {
         if (s.type == ST_PERM) {
-            std::memcpy(c->h_perm + p, s.perm.data(), s.perm.size() * sizeof(uint32_t));
+            // k_perm gathers: out[w] = in[perm^-1(w)]
+            for (size_t w = 0; w < s.perm.size(); w++) c->h_perm[p + s.perm[w]] = (uint32_t)w;
             s.t = (int)p;  // perm offset
             p += s.perm.size();
         }
@@ -473,6 +474,9 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     std::sort(srt, srt + tb);
     for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
     d.n_inst = 1ULL << (M - tb);
+    d.contiguous = 1;
+    for (int i = 0; i < tb; i++)
+        if (d.tile_pos[i] != i) d.contiguous = 0;
     for (int b = 0; b < 64; b++) {
         if (!((s.cm >> b) & 1)) continue;
         int tl = -1;
