@@ -10,6 +10,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -65,12 +66,22 @@ JitPass jit_generate(const Step &st)
     const int loop = env_int("QSIM_JIT_PERSIST", 0) > 0;
     s << "// minb=" << minb << " prefetch=" << pf << " loop=" << loop << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
-         "unsigned long long pad; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
+         "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
          "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
          "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
+    // e^{2 pi i t / 2^64}: table of the top 8 bits x Taylor series of the rest (|x| < 2pi/256)
+    s << "__device__ __forceinline__ double2 qexp(unsigned long long t, const double2 *tab)\n{\n"
+         " const double2 b = __ldg(tab + (t >> 56));\n"
+         " const double x = (double)(t & 0x00FFFFFFFFFFFFFFULL) * 3.4061215800865545e-19;\n"  // 2pi / 2^64
+         " const double x2 = x * x;\n"
+         " const double c = fma(x2, fma(x2, fma(x2, fma(x2, 2.48015873015873e-05, -1.3888888888888889e-03), "
+         "4.1666666666666664e-02), -0.5), 1.0);\n"
+         " const double s = x * fma(x2, fma(x2, fma(x2, fma(x2, 2.7557319223985893e-06, -1.9841269841269841e-04), "
+         "8.3333333333333332e-03), -1.6666666666666666e-01), 1.0);\n"
+         " return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));\n}\n";
     s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads << ", " << minb
       << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
@@ -142,9 +153,9 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_PHASE_FLUSH) {
             for (int v = 0; v < 16; v++)
                 if (acc_used[v])
-                    s << "  { double sn, cs; sincospi((double)th" << v << " * 0x1p-63, &sn, &cs); const double p1 = -sn * a"
-                      << v << ".y, p2 = sn * a" << v << ".x; a" << v << ".x = fma(cs, a" << v << ".x, p1); a" << v
-                      << ".y = fma(cs, a" << v << ".y, p2); }\n";
+                    s << "  { const double2 e = qexp(th" << v << ", P.ptab); const double p1 = -e.y * a" << v
+                      << ".y, p2 = e.y * a" << v << ".x; a" << v << ".x = fma(e.x, a" << v << ".x, p1); a" << v
+                      << ".y = fma(e.x, a" << v << ".y, p2); }\n";
             s << " }\n";
             in_run = false;
             continue;
@@ -259,6 +270,8 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     std::memcpy(b + 0, &state, 8);
     std::memcpy(b + 8, &rank_bits, 8);
     std::memcpy(b + 16, &st.pass.n_inst, 8);
+    const void *tab = jit_phase_table();
+    std::memcpy(b + 24, &tab, 8);
     for (int t = 0; t < kTileBits; t++) {
         const uint64_t m = 1ULL << st.pass.tp[t];
         std::memcpy(b + kOffTpm + 8 * t, &m, 8);
@@ -275,6 +288,26 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             if (op.code == OPC_PHASE_ACC) std::memcpy(b + L.off_m + 64 * m_idx[o] + 16, &op.cfg, 8);  // angle
         }
     }
+}
+
+// e^{2 pi i k / 256}, k < 256 (device, one per process)
+const void *jit_phase_table()
+{
+    static void *d = []() -> void * {
+        double h[512];
+        for (int k = 0; k < 256; k++) {
+            const long double a = 2.0L * 3.14159265358979323846264338327950288L * k / 256.0L;
+            h[2 * k] = (double)cosl(a);
+            h[2 * k + 1] = (double)sinl(a);
+        }
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(h)) != cudaSuccess || cudaMemcpy(p, h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return p;
+    }();
+    return d;
 }
 
 // ------------------------------------------------------------- driver API

@@ -29,6 +29,8 @@ struct Drv {
                              CUstream, void **, void **);
 };
 const Drv &drv();
+// device table of e^{2 pi i k/256} used by the phase-run flush
+const void *jit_phase_table();
 
 struct JitPass {
     std::string src;     // generated source (cache key)

@@ -274,7 +274,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         size_t b = a;
         while (b < st.ops.size() && st.ops[b].code == OPC_PHASE) b++;
         // cost model (FP64-pipe ops per thread): direct = 4 per touched register per
-        // op; accumulated = integer adds + one sincospi (~45) + cmul per touched register
+        // op; accumulated = integer adds + one e^{i theta} (~20) + cmul per touched register
         double direct = 0;
         uint32_t touched = 0;
         for (size_t o = a; o < b; o++) {
@@ -282,7 +282,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             for (uint32_t i = 0; i < 16; i++)
                 if ((i & op.mreg) == op.vreg) { direct += 4; touched |= 1u << i; }
         }
-        const double acc = 50.0 * __builtin_popcount(touched);
+        const double acc = 24.0 * __builtin_popcount(touched);  // table x Taylor flush (jit.cpp qexp)
         if (b - a >= (size_t)kPhaseRunMin && acc < 0.8 * direct) {
             for (size_t o = a; o < b; o++) {
                 KOp &op = st.ops[o];
