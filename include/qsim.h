@@ -221,11 +221,13 @@ const char *qsim_status_str(qsim_status s);
 const char *qsim_last_error(qsim_ctx ctx);
 
 /* Host-only planner introspection (no GPU needed): plan `gates` for an
- * n-qubit state over P shards starting from the identity sigma and write a
- * JSON description of the steps (passes, perms, exchanges, relabels) into
- * buf.  Returns QSIM_ERR_ARG if buf is too small. */
+ * n-qubit state over P shards (initial sigma by look-ahead) and write a JSON
+ * description of the steps (passes, perms, exchanges, pairwise combines,
+ * relabels) into buf.  flags: bits 0-1 = fusion (0 off, 1 on, 2 on + NVRTC-
+ * compile the pass kernels as a host-only check); bits 4-5 = global policy
+ * + 1 (0 = default auto).  Returns QSIM_ERR_ARG if buf is too small. */
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
-                           int fusion, char *buf, size_t buf_bytes);
+                           int flags, char *buf, size_t buf_bytes);
 
 /* Host-only exchange routing of a K-pair remap ("we first compute
  * the ranks of the other MPI processes with which the MPI process has to

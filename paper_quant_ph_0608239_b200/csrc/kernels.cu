@@ -683,6 +683,53 @@ __global__ void k_pack(double2 *__restrict__ shard, double2 *__restrict__ buf, u
     }
 }
 
+// pairwise global-target gate (virtual shards): A holds the partner with the
+// target bit 0, B with the bit 1; both are updated from both (1x traffic)
+__global__ void k_pair_gate(double2 *__restrict__ A, double2 *__restrict__ B, uint64_t count, uint64_t mloc,
+                            uint64_t vloc, int xs, U8 u)
+{
+    const double2 u00 = make_double2(u.m[0], u.m[1]), u01 = make_double2(u.m[2], u.m[3]);
+    const double2 u10 = make_double2(u.m[4], u.m[5]), u11 = make_double2(u.m[6], u.m[7]);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        if ((i & mloc) != vloc) continue;
+        const double2 a = A[i], b = B[i];
+        if (xs) {
+            A[i] = b;
+            B[i] = a;
+        } else {
+            A[i] = cmac2(u00, a, u01, b);
+            B[i] = cmac2(u10, a, u11, b);
+        }
+    }
+}
+
+// pairwise over NCCL: own <- c0*own + c1*other (self_first) or c0*other + c1*own
+__global__ void k_pair_combine(double2 *__restrict__ own, const double2 *__restrict__ other, uint64_t off,
+                               uint64_t count, uint64_t mloc, uint64_t vloc, double2 c0, double2 c1, int self_first)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (((off + i) & mloc) != vloc) continue;
+        own[i] = self_first ? cmac2(c0, own[i], c1, other[i]) : cmac2(c0, other[i], c1, own[i]);
+    }
+}
+
+void launch_pair_gate(double2 *A, double2 *B, int M, uint64_t mloc, uint64_t vloc, int xs, const double *m,
+                      cudaStream_t s)
+{
+    U8 u;
+    for (int k = 0; k < 8; k++) u.m[k] = m[k];
+    const uint64_t n = 1ULL << M;
+    k_pair_gate<<<grid_for(n, 256), 256, 0, s>>>(A, B, n, mloc, vloc, xs, u);
+}
+
+void launch_pair_combine(double2 *own, const double2 *other, uint64_t off, uint64_t count, uint64_t mloc,
+                         uint64_t vloc, const double *c0, const double *c1, int self_first, cudaStream_t s)
+{
+    k_pair_combine<<<grid_for(count, 256), 256, 0, s>>>(own, other, off, count, mloc, vloc,
+                                                      make_double2(c0[0], c0[1]), make_double2(c1[0], c1[1]),
+                                                      self_first);
+}
+
 static LPos make_lpos(int K, const int *lpos, uint64_t c, uint64_t *off)
 {
     LPos L{};

@@ -39,6 +39,10 @@ void launch_swap_blocks(double2 *A, double2 *B, int M, int K, const int *lpos, u
                         cudaStream_t s);
 void launch_pack(const double2 *shard, double2 *buf, int M, int K, const int *lpos, uint64_t c, uint64_t first,
                  uint64_t count, int unpack, cudaStream_t s);
+void launch_pair_gate(double2 *A, double2 *B, int M, uint64_t mloc, uint64_t vloc, int xs, const double *m,
+                      cudaStream_t s);
+void launch_pair_combine(double2 *own, const double2 *other, uint64_t off, uint64_t count, uint64_t mloc,
+                         uint64_t vloc, const double *c0, const double *c1, int self_first, cudaStream_t s);
 int pass_regs_per_thread();
 
 }  // namespace qsb

@@ -501,6 +501,32 @@ void Planner::emit_exchange(const std::vector<GateRec> &gates, const std::vector
     out.push_back(std::move(s));
 }
 
+// Auto policy: a remap moves half a shard per direction and makes the qubit
+// local for every later gate; a pairwise combine moves a whole shard and keeps
+// sigma.  Pairwise pays off only for an isolated gate on a global qubit when
+// every local qubit a remap could evict is itself needed within the window
+// (the remap would have to be undone right away).
+bool Planner::prefer_pairwise(const std::vector<GateRec> &gates, const std::vector<char> &done, size_t first) const
+{
+    const GateRec &g = gates[first];
+    const int q = g.target;
+    const size_t window = (size_t)4 * n + 8;
+    size_t seen = 0;
+    int uses = 0;
+    uint64_t needed = 0;  // local qubits used non-diagonally in the window
+    for (size_t i = first; i < gates.size() && seen < window; i++) {
+        if (done[i]) continue;
+        seen++;
+        if ((gates[i].qN >> q) & 1) uses++;
+        needed |= gates[i].qN;
+    }
+    if (uses > 1) return false;
+    const int lo = M >= kTileBits ? 3 : 0;
+    for (int p = lo; p < M; p++)
+        if (!((needed >> qubit_at[p]) & 1)) return false;  // a free victim exists
+    return true;
+}
+
 void Planner::remap(const std::vector<int> &local_q, const std::vector<int> &global_q, std::vector<Step> &out)
 {
     Step s;
@@ -536,7 +562,22 @@ void Planner::plan(const std::vector<GateRec> &gates, const PlanOptions &opt, st
         for (int q = 0; q < n; q++)
             if (((g.qN >> q) & 1) && phys_of[q] >= M) global_target = true;
         if (global_target) {
-            emit_exchange(gates, done, first, out);
+            const bool pw = g.kind == GK_U2 && (opt.global_policy == GP_PAIRWISE ||
+                                                (opt.global_policy == GP_AUTO && prefer_pairwise(gates, done, first)));
+            if (pw) {
+                Step s;
+                s.type = ST_PAIRWISE;
+                s.code = g.cls == CLS_XS ? OPC_XS : g.cls == CLS_REAL ? OPC_U2R : OPC_U2;
+                s.t = phys_of[g.target];
+                for (int c : g.controls) s.cm |= bit(phys_of[c]);
+                s.cv = s.cm;
+                for (int k = 0; k < 8; k++) s.m[k] = g.u[k];
+                s.gate_id = g.id;
+                out.push_back(s);
+                done[first] = 1;
+            } else {
+                emit_exchange(gates, done, first, out);
+            }
             continue;
         }
         if (g.kind == GK_PERM) {
@@ -607,6 +648,12 @@ std::string plan_to_json(const Planner &P, const std::vector<Step> &steps)
             break;
         case ST_RELABEL:
             o << "{\"type\":\"relabel\",\"a\":" << st.ra << ",\"b\":" << st.rb << "}";
+            break;
+        case ST_PAIRWISE:
+            o << "{\"type\":\"pairwise\",\"gate\":" << st.gate_id << ",\"code\":" << st.code << ",\"t\":" << st.t
+              << ",\"cm\":" << st.cm << ",\"cv\":" << st.cv << ",\"m\":[";
+            for (int j = 0; j < 8; j++) o << (j ? "," : "") << st.m[j];
+            o << "]}";
             break;
         }
     }

@@ -28,7 +28,11 @@ struct GateRec {
 
 void classify(GateRec &g);  // sets cls, qN, qD
 
-enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5 };
+enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5, ST_PAIRWISE = 6 };
+
+// global-target policy: remap (K-pair interchange),
+// pairwise (partner shards combine, sigma unchanged), or auto
+enum GlobalPolicy { GP_REMAP = 0, GP_PAIRWISE = 1, GP_AUTO = 2 };
 
 struct Step {
     int type = ST_PASS;
@@ -39,6 +43,7 @@ struct Step {
     std::vector<int> op_t;        // physical target of each op (-1: PHASE/TRANS)
     std::vector<uint64_t> op_cm, op_cv;  // full-index predicate of each op (for introspection)
     // ST_GENERIC: one U2 on physical target t, controls (full-index mask/val)
+    // ST_PAIRWISE: one U2 on GLOBAL physical target t (partner shards combine)
     // ST_PHASE  : multiply by f where (full & mask) == val
     int code = OPC_U2;
     int t = -1;
@@ -57,6 +62,7 @@ struct Step {
 struct PlanOptions {
     bool fusion = true;
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
+    int global_policy = GP_AUTO;
 };
 
 class Planner {
@@ -74,6 +80,7 @@ public:
     void remap(const std::vector<int> &local_q, const std::vector<int> &global_q, std::vector<Step> &out);
 
 private:
+    bool prefer_pairwise(const std::vector<GateRec> &gates, const std::vector<char> &done, size_t first) const;
     void emit_exchange(const std::vector<GateRec> &gates, const std::vector<char> &done, size_t first,
                        std::vector<Step> &out);
     void build_pass(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,

@@ -81,6 +81,7 @@ struct qsim_ctx_s {
     bool fusion = true, timing = false;
     int max_scan = 1 << 30;
     int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
+    int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
     // stats
@@ -424,6 +425,52 @@ static qsim_status exec_exchange(qsim_ctx c, const Step &s)
     return QSIM_OK;
 }
 
+// pairwise handling of a gate on a global target: the two ranks
+// that differ only in the target bit combine their shards; sigma unchanged
+static qsim_status exec_pairwise(qsim_ctx c, const Step &s)
+{
+    const int M = c->M;
+    const uint64_t gbit = 1ULL << (s.t - M);
+    const uint64_t lmask = (1ULL << M) - 1;
+    const uint64_t mloc = s.cm & lmask, vloc = s.cv & lmask, mhi = s.cm & ~lmask, vhi = s.cv & ~lmask;
+    RangeGuard rg(c, 3, 0);
+    c->stats.exchanges++;
+    if (c->transport == QSIM_TRANSPORT_VIRTUAL) {
+        for (uint64_t r = 0; r < (uint64_t)c->P; r++) {
+            if (r & gbit) continue;
+            if (((r << M) & mhi) != vhi) continue;  // controls on global qubits (never the target)
+            launch_pair_gate(c->shards[r], c->shards[r | gbit], M, mloc, vloc, s.code == OPC_XS, s.m, c->stream);
+            LAUNCHED(c);
+        }
+        c->stats.exchange_bytes += (uint64_t)c->P * (16ULL << M);
+        return QSIM_OK;
+    }
+    if (c->transport != QSIM_TRANSPORT_NCCL) FAIL(c, QSIM_ERR_STATE, "pairwise step without a multi-shard transport");
+    const uint64_t r = (uint64_t)c->rank;
+    if (((r << M) & mhi) != vhi) return QSIM_OK;  // the partner skips too (same control bits)
+    const int peer = (int)(r ^ gbit);
+    const bool hi = (r & gbit) != 0;
+    static const double xs_m[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+    const double *m = s.code == OPC_XS ? xs_m : s.m;
+    // self_first: bit 0 -> own' = u00 own + u01 other; bit 1 -> own' = u10 other + u11 own
+    const double *c0 = hi ? m + 4 : m + 0, *c1 = hi ? m + 6 : m + 2;
+    const uint64_t shard = 1ULL << M, scratch_amps = c->scratch_bytes / sizeof(double2);
+    uint64_t piece = shard;
+    const uint64_t limit_amps = (uint64_t)c->chunk_mb * (1ULL << 20) / sizeof(double2);
+    while (piece > 1 && (piece > scratch_amps || piece > limit_amps)) piece >>= 1;
+    if (piece > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for a pairwise exchange");
+    for (uint64_t off = 0; off < shard; off += piece) {
+        CKN(c, ncclGroupStart());
+        CKN(c, ncclSend(c->shards[0] + off, piece * 2, ncclDouble, peer, c->comm, c->stream));
+        CKN(c, ncclRecv(c->scratch, piece * 2, ncclDouble, peer, c->comm, c->stream));
+        CKN(c, ncclGroupEnd());
+        launch_pair_combine(c->shards[0] + off, c->scratch, off, piece, mloc, vloc, c0, c1, !hi, c->stream);
+        LAUNCHED(c);
+    }
+    c->stats.exchange_bytes += 16ULL << M;
+    return QSIM_OK;
+}
+
 // ------------------------------------------------------------ flush
 static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 {
@@ -538,6 +585,7 @@ static qsim_status flush(qsim_ctx c)
         PlanOptions opt;
         opt.fusion = c->fusion;
         opt.max_scan = c->max_scan;
+        opt.global_policy = c->global_policy;
         c->planner->plan(c->queue, opt, steps);
         pc.steps = std::move(steps);
         pc.queue.swap(c->queue);
@@ -628,6 +676,9 @@ static qsim_status flush(qsim_ctx c)
             break;
         case ST_RELABEL:
             c->stats.relabels++;
+            break;
+        case ST_PAIRWISE:
+            if ((st = exec_pairwise(c, s)) != QSIM_OK) return st;
             break;
         }
     }
@@ -1091,6 +1142,11 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
     else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
     else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }
+    else if (k == "global_policy") {
+        if (value < 0 || value > 2) FAIL(c, QSIM_ERR_ARG, "global_policy must be 0 (remap), 1 (pairwise) or 2 (auto)");
+        c->global_policy = (int)value;
+        c->pc.valid = false;
+    }
     else FAIL(c, QSIM_ERR_ARG, "unknown option '%s'", key);
     return QSIM_OK;
 }
@@ -1149,10 +1205,11 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     init += "],\"plan\":";
     std::vector<Step> steps;
     PlanOptions opt;
-    opt.fusion = fusion != 0;
+    opt.fusion = (fusion & 3) != 0;
+    opt.global_policy = (fusion >> 4) & 3 ? ((fusion >> 4) & 3) - 1 : GP_AUTO;
     P.plan(recs, opt, steps);
     std::string jit_info;
-    if (fusion == 2) {  // also NVRTC-compile the pass-specialised kernels (host-only check)
+    if ((fusion & 3) == 2) {  // also NVRTC-compile the pass-specialised kernels (host-only check)
         std::vector<const Step *> ps;
         for (const Step &s : steps)
             if (s.type == ST_PASS) ps.push_back(&s);

@@ -73,14 +73,19 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
-def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1) -> str:
+GLOBAL_POLICY = {"remap": 0, "pairwise": 1, "auto": 2}
+
+
+def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1, policy: Optional[str] = None) -> str:
     """Host-only planner introspection (no GPU needed).  fusion=2 also
-    NVRTC-compiles the pass-specialised kernels (reported under "jit")."""
+    NVRTC-compiles the pass-specialised kernels (reported under "jit");
+    policy: global-target policy ("remap" | "pairwise" | "auto")."""
     arr, keep = pack_gates(gates)
+    flags = int(fusion) | (((GLOBAL_POLICY[policy] + 1) << 4) if policy else 0)
     cap = 1 << 26
     while True:
         buf = ctypes.create_string_buffer(cap)
-        s = N.lib().qsim_plan_json(n, n_ranks, arr, len(gates), int(fusion), buf, cap)
+        s = N.lib().qsim_plan_json(n, n_ranks, arr, len(gates), flags, buf, cap)
         if s == 0:
             return buf.value.decode()
         if s == 1 and cap < (1 << 30):

@@ -77,6 +77,8 @@ def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
             psi = new
         elif ty == "relabel":
             pass
+        elif ty == "pairwise":  # a gate on a nonlocal bit: in one array it is just that bit
+            _apply(psi, idx, st["code"], st["t"], st["cm"], st["cv"], st["m"])
         else:
             raise ValueError(ty)
     fin = plan["final_phys_of"]

@@ -47,8 +47,8 @@ def test_status_strings(pkg):
         assert lib.qsim_status_str(i).decode() == nme
 
 
-def _plan(pkg, n, P, gates, fusion=True):
-    return pkg.plan_json(n, P, gates, fusion)
+def _plan(pkg, n, P, gates, fusion=True, policy=None):
+    return pkg.plan_json(n, P, gates, fusion, policy)
 
 
 def test_validation_codes(pkg):
@@ -67,8 +67,8 @@ def test_validation_codes(pkg):
         assert e.value.status == code
 
 
-def _check_plan(pkg, oracle_mod, n, P, init, gates, fusion=True):
-    js = _plan(pkg, n, P, gates, fusion)
+def _check_plan(pkg, oracle_mod, n, P, init, gates, fusion=True, policy=None):
+    js = _plan(pkg, n, P, gates, fusion, policy)
     got = run_plan(js, n, init, gates)
     o = oracle_mod.Oracle(n)
     o.init_basis(init)
@@ -138,3 +138,29 @@ def test_jit_kernels_compile_for_sm100a(pkg):
     d = json.loads(_plan(pkg, 14, 2, gates, fusion=2))
     assert d["jit"]["ok"], d["jit"]["error"]
     assert d["jit"]["kernels"] >= 1
+
+
+@pytest.mark.parametrize("policy", ["remap", "pairwise", "auto"])
+def test_plan_global_policies(pkg, oracle_mod, policy):
+    """Gates on nonlocal qubits by K-pair remap or by pairwise
+    combine of partner shards; both give the oracle's state."""
+    for P, n in ((2, 13), (4, 14), (8, 15)):
+        gates = C.random_chain(n, 2, seed=P, sweep=True)
+        d = _check_plan(pkg, oracle_mod, n, P, 3, gates, policy=policy)
+        types = {s["type"] for s in d["plan"]["steps"]}
+        if policy == "pairwise":
+            assert "pairwise" in types
+        if policy == "remap":
+            assert "pairwise" not in types and "exchange" in types
+
+
+def test_auto_policy_picks_pairwise_when_remap_would_thrash(pkg, oracle_mod):
+    """One gate on the nonlocal qubit while every local qubit keeps being
+    used: the auto policy combines partner shards instead of remapping."""
+    n, P = 13, 2
+    rng = G.SplitMix64(9)
+    layer = lambda: [G.one_q(q, G.haar_u2(rng)) for q in range(12)]  # noqa: E731
+    gates = layer() + [G.one_q(12, G.haar_u2(rng))] + [G.cnot(12, q) for q in range(12)] + layer() + layer()
+    d = _check_plan(pkg, oracle_mod, n, P, 0, gates, policy="auto")
+    types = [s["type"] for s in d["plan"]["steps"]]
+    assert "pairwise" in types and "exchange" not in types

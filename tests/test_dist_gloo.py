@@ -54,7 +54,7 @@ def _chunk_index(M, lpos, v):
     return idx[sel]
 
 
-def _worker(rank, world, port, case, out_q):
+def _worker(rank, world, port, case, out_q, policy=None):
     import torch
     import torch.distributed as dist
     import sys
@@ -65,7 +65,7 @@ def _worker(rank, world, port, case, out_q):
         import paper_quant_ph_0608239_b200 as P
         from workloads import circuits as C
         n, init, gates, qs = case()
-        plan = json.loads(P.plan_json(n, world, gates))
+        plan = json.loads(P.plan_json(n, world, gates, policy=policy))
         G = (world - 1).bit_length()
         M = n - G
         phys0 = plan["initial_phys_of"]
@@ -117,6 +117,27 @@ def _worker(rank, world, port, case, out_q):
                 for v, (ci, recv, _) in bufs.items():
                     shard[ci] = recv.numpy().view(np.complex128)
                 n_ex += 1
+            elif ty == "pairwise":
+                gb = 1 << (st["t"] - M)
+                peer = rank ^ gb
+                lm = (1 << M) - 1
+                if ((rank << M) & st["cm"] & ~lm) == (st["cv"] & ~lm):
+                    send = torch.from_numpy(shard.view(np.float64).copy())
+                    recv = torch.empty_like(send)
+                    reqs = [dist.isend(send, peer), dist.irecv(recv, peer)]
+                    for r_ in reqs:
+                        r_.wait()
+                    other = recv.numpy().view(np.complex128)
+                    m = st["m"]
+                    u = [complex(m[0], m[1]), complex(m[2], m[3]), complex(m[4], m[5]), complex(m[6], m[7])]
+                    if st["code"] == 2:
+                        u = [0, 1, 1, 0]
+                    sel = (np.arange(1 << M) & st["cm"] & lm) == (st["cv"] & lm)
+                    if rank & gb:
+                        shard[sel] = u[2] * other[sel] + u[3] * shard[sel]
+                    else:
+                        shard[sel] = u[0] * shard[sel] + u[1] * other[sel]
+                n_ex += 1
         # gather the state (logical order) and reduce a marginal like qsim_probabilities
         allsh = [torch.empty(2 << M, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(allsh, torch.from_numpy(shard.view(np.float64).copy()))
@@ -164,12 +185,14 @@ def _case_qft():
     return 13, w.init, w.gates, [12, 11]
 
 
-@pytest.mark.parametrize("world,case", [(2, _case_brickwork), (2, _case_shor), (2, _case_qft), (4, _case_chain4)])
-def test_sharded_path_gloo(oracle_mod, world, case):
+@pytest.mark.parametrize("world,case,policy", [(2, _case_brickwork, None), (2, _case_shor, None), (2, _case_qft, None),
+                                               (4, _case_chain4, None), (2, _case_brickwork, "pairwise"),
+                                               (4, _case_chain4, "pairwise")])
+def test_sharded_path_gloo(oracle_mod, world, case, policy):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, policy)) for r in range(world)]
     for p in procs:
         p.start()
     logical, prob, n_ex = q.get(timeout=300)

@@ -123,6 +123,17 @@ def test_every_gate_sharded_virtual(P, oracle_mod, ranks, n):
     assert st["exchanges"] > 0
 
 
+@pytest.mark.parametrize("policy,ranks,n", [(1, 2, 14), (1, 8, 16), (1, 4, 9), (2, 8, 15)])
+def test_global_policy_pairwise_virtual(P, oracle_mod, policy, ranks, n):
+    """Pairwise combine of partner shards for gates on nonlocal qubits."""
+    gates = kitchen_sink(n, seed=200 + n) + C.random_chain(n, 1, seed=n, sweep=True)
+    sim = P.QSim(n, n_ranks=ranks, transport="virtual")
+    sim.set_option("global_policy", policy)
+    sim.init_basis(2)
+    sim.run_circuit(gates)
+    assert_parity(sim, oracle_run(oracle_mod, n, 2, gates), n)
+
+
 def test_tiny_states(P, oracle_mod):
     for n, ranks in [(1, 1), (2, 1), (2, 2), (3, 4), (5, 1)]:
         gates = [G.one_q(q, G.haar_u2(G.SplitMix64(q))) for q in range(n)]
