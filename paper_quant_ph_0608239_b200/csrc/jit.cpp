@@ -69,9 +69,11 @@ JitPass jit_generate(const Step &st)
          "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
+    // (the volatile move keeps ptxas from hoisting the 12 loop-invariant masks
+    // of the persistent variant into long-lived registers)
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
-         "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
-         "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
+         "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { int t; asm volatile(\"mov.b32 %0, %1;\" : "
+         "\"=r\"(t) : \"r\"(ts[j])); b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
     // e^{2 pi i t / 2^64}: table of the top 8 bits x Taylor series of the rest (|x| < 2pi/256)
     s << "__device__ __forceinline__ double2 qexp(unsigned long long t, const double2 *tab)\n{\n"
          " const double2 b = __ldg(tab + (t >> 56));\n"
@@ -85,9 +87,16 @@ JitPass jit_generate(const Step &st)
     s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads << ", " << minb
       << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
-    s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    if (loop) s << " for (unsigned long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {\n";
-    else s << " { const unsigned long long inst = blockIdx.x;\n";
+    if (loop) {
+        // lane/warp re-read every iteration (asm volatile) so ptxas cannot hoist the
+        // per-config address terms out of the loop and raise register pressure
+        s << " for (unsigned long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {\n";
+        s << " int tid_; asm volatile(\"mov.u32 %0, %%tid.x;\" : \"=r\"(tid_));\n";
+        s << " const int lane = tid_ & 31, warp = tid_ >> 5;\n";
+    } else {
+        s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+        s << " { const unsigned long long inst = blockIdx.x;\n";
+    }
     s << " const unsigned long long base = qdep(inst, P.ts);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";

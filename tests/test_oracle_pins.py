@@ -344,3 +344,27 @@ def test_sampler_rule(oracle_mod):
     out, _ = sample_from(np.full(8, 1 / 8), 3, 1, 80000)
     freq = np.bincount(out.astype(np.int64), minlength=8) / 80000
     assert np.max(np.abs(freq - 1 / 8)) < 0.01
+
+
+def test_paper_adder_op_counts():
+    """N_O of the paper's adder benchmarks (Tables IV-VIII)
+    decomposes as 2 x (one-bits) + QFT + adds + inverse QFT (V4)."""
+    for name, (m, values, n_o) in C.PAPER_ADDERS.items():
+        w = C.paper_adder(name)
+        assert len(w.gates) == n_o, name
+        assert w.n == m * len(values)
+    assert C.paper_adder("3-11QBA").meta["expect_sum"] == 2047     # P:1293 caption values
+    assert C.paper_adder("2-17QBA").meta["expect_sum"] == 131071
+
+
+def test_paper_adder_small_instance(oracle_mod):
+    """Same construction (doubled loading gates + QFT adder) on 3 x 4-qubit
+    registers: the sum register holds the sum mod 16 with probability 1."""
+    regs = [list(range(0, 4)), list(range(4, 8)), list(range(8, 12))]
+    vals = (5, 9, 14)
+    gates = C.load_register_bits(regs, vals) + C.qft_adder(regs)
+    o = oracle_mod.Oracle(12)
+    o.init_basis(0)
+    o.run(gates)
+    assert o.probabilities(regs[2])[sum(vals) % 16] >= 1 - 1e-12
+    assert o.probabilities(regs[0])[5] >= 1 - 1e-12

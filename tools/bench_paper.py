@@ -1,0 +1,75 @@
+"""The paper's own benchmarks (Tables IV-VIII) on one B200.
+
+t_E as the paper defines it: gates + measuring every qubit (<Q_i>),
+here also including the state initialisation.  33 qubits = 128 GiB is the
+largest state one 180-GB B200 holds; 34-36 qubits need 2-8 GPUs.  Each run is
+checked: H-on-all must give <Q_i> = 1/2 and norm 1; an adder must leave the
+sum register at sum mod 2^m with probability 1 ("very easy to check").
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_quant_ph_0608239_b200 import QSim, pack_gates  # noqa: E402
+from workloads import circuits as C  # noqa: E402
+
+# best printed t_E [s] of each row (machine, processes), BASELINE.md / P:1285-1390
+PAPER = {("H-all", 27): ("Cray X1E", 4, 12), ("H-all", 28): ("BG/L", 16, 43), ("H-all", 29): ("Cray X1E", 8, 26),
+         ("H-all", 30): ("BG/L", 64, 52), ("H-all", 31): ("BG/L", 128, 58), ("H-all", 32): ("BG/L", 256, 70),
+         ("H-all", 33): ("BG/L", 512, 79), ("3-11QBA", 33): ("SR11000/J1", 128, 586)}
+
+
+def run(w, check):
+    sim = QSim(w.n)
+    sim.set_option("timing", 1)
+    packed = pack_gates(w.gates)
+    # warm-up (plans + JIT-compiles), then the timed run
+    sim.init_basis(w.init); sim.run_circuit(w.gates, packed=packed); ex = sim.expectations()
+    torch.cuda.synchronize()
+    sim.reset_stats()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(sim.stream)
+    sim.init_basis(w.init); sim.run_circuit(w.gates, packed=packed); ex = sim.expectations()
+    e1.record(sim.stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    ok, detail = check(sim, ex)
+    st = sim.stats()
+    key = (w.name, w.n)
+    paper = PAPER.get(key)
+    out = {"workload": w.name, "L": w.n, "N_O": len(w.gates), "t_E_s": ms / 1e3, "wall_s": wall,
+           "agu_per_s": len(w.gates) * 2.0 ** w.n / (ms / 1e3), "passes": st["passes"],
+           "check": ok, "detail": detail}
+    if paper:
+        out["paper_best"] = {"machine": paper[0], "processes": paper[1], "t_E_s": paper[2],
+                             "speedup": paper[2] / (ms / 1e3)}
+    print(json.dumps(out), flush=True)
+    sim.close()
+    torch.cuda.empty_cache()
+
+
+def check_h(sim, ex):
+    return bool(np.max(np.abs(ex - 0.5)) < 1e-12 and abs(sim.norm() - 1) < 1e-12), \
+        {"max_dev_Q": float(np.max(np.abs(ex - 0.5)))}
+
+
+def check_adder(w):
+    def f(sim, ex):
+        p = sim.probabilities(w.meta["sum_register"])
+        return bool(p[w.meta["expect_sum"]] >= 1 - 1e-12), {"p_sum": float(p[w.meta["expect_sum"]]),
+                                                           "expect": w.meta["expect_sum"]}
+    return f
+
+
+Ls = [int(x) for x in sys.argv[1:]] or list(range(27, 34))
+for L in Ls:
+    run(C.h_on_all(L), check_h)
+w = C.paper_adder("3-11QBA")
+run(w, check_adder(w))

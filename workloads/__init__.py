@@ -15,4 +15,5 @@ from .circuits import (  # noqa: F401
     qft_ladder, inverse_qft_ladder, qft_adder, random_brickwork, random_chain,
     shor_order_finding, shor_base, qft_basis, config1_adder, config2_random,
     config3_shor, config4_qft, config5_random36, count_ops, multiplicative_order,
+    paper_adder, h_on_all, PAPER_ADDERS, load_register_bits,
 )

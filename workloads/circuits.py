@@ -200,3 +200,51 @@ def count_ops(gates: Sequence[Gate]) -> Dict[str, int]:
         c[{G_1Q: "1q", G_CTRL: "ctrl", G_PERM: "perm", G_SWAP: "swap"}[g.kind]] += 1
     c["total"] = len(gates)
     return c
+
+
+# ---------------------------------------------------------------------------
+# The paper's own benchmark workloads (Tables IV-IX)
+# ---------------------------------------------------------------------------
+PAPER_ADDERS = {
+    # name: (register width m, register values); N_O as printed (V4)
+    "3-11QBA": (11, (292, 585, 1170), 286),    # 33 qubits
+    "2-17QBA": (17, (26214, 104857), 493),     # 34 qubits
+    "5-7QBA": (7, (7, 9, 19, 35, 65), 194),    # 35 qubits
+    "3-12QBA": (12, (781, 1054, 3296), 342),   # 36 qubits
+}
+
+
+def load_register_bits(regs, values):
+    """Put numbers in the registers with the doubled gates XX, YY, X-bar X-bar,
+    Y-bar Y-bar: each loads |1> up to a phase and
+    counts as 2 operations.  The four kinds are cycled over the one-bits."""
+    from .gates import X, XBAR, Y, YBAR
+    kinds = (X, Y, XBAR, YBAR)
+    out, k = [], 0
+    for reg, val in zip(regs, values):
+        for b, q in enumerate(reg):
+            if (val >> b) & 1:
+                u = kinds[k % 4]
+                out += [one_q(q, u), one_q(q, u)]
+                k += 1
+    return out
+
+
+def paper_adder(name: str) -> Workload:
+    """n-mQBA of the paper: load the registers from |0..0>, QFT the last
+    register, add the others into it with controlled phases, inverse QFT
+    (Fig. adder caption).  Expect the last register to hold
+    sum mod 2^m with probability 1."""
+    m, values, n_o = PAPER_ADDERS[name]
+    regs = [list(range(i * m, (i + 1) * m)) for i in range(len(values))]
+    gates = load_register_bits(regs, values) + qft_adder(regs)
+    expect = sum(values) % (1 << m)
+    return Workload(name, m * len(values), 0, gates,
+                    {"m": m, "values": values, "expect_sum": expect, "n_o_paper": n_o, "sum_register": regs[-1]})
+
+
+def h_on_all(L: int) -> Workload:
+    """The scaling test: a Hadamard on every qubit ("H" rows of
+    Tables IV-IX, N_O = L)."""
+    from .gates import H as HD
+    return Workload("H-all", L, 0, [one_q(q, HD) for q in range(L)], {})
