@@ -164,3 +164,27 @@ def test_auto_policy_picks_pairwise_when_remap_would_thrash(pkg, oracle_mod):
     d = _check_plan(pkg, oracle_mod, n, P, 0, gates, policy="auto")
     types = [s["type"] for s in d["plan"]["steps"]]
     assert "pairwise" in types and "exchange" not in types
+
+
+def _build_c_client(pkg, tmp_path):
+    import subprocess
+    exe = str(tmp_path / "abi_client")
+    libdir = os.path.dirname(pkg.LIB_PATH)
+    subprocess.check_call(["gcc", "-std=c11", "-O1", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_client.c"), "-o", exe,
+                           "-L", libdir, "-l:libqsim_b200.so", "-Wl,-rpath," + libdir, "-lm"])
+    return exe
+
+
+def test_c_client_compiles_and_links(pkg, tmp_path):
+    """A plain C program builds against include/qsim.h + libqsim_b200.so."""
+    assert os.path.exists(_build_c_client(pkg, tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_client_runs(pkg, tmp_path):
+    """The same C program runs the engine with no Python/torch involvement."""
+    import subprocess
+    r = subprocess.run([_build_c_client(pkg, tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr + r.stdout
+    assert "abi_client ok" in r.stdout
