@@ -358,3 +358,29 @@ def test_errors_leave_state_untouched(P):
     with pytest.raises(QsimError) as e:
         s2.norm()
     assert e.value.name == "QSIM_ERR_STATE"
+
+
+def test_nccl_transport_single_rank(P, oracle_mod):
+    """The NCCL transport end to end on one GPU (world size 1): unique id from
+    qsim_get_unique_id broadcast over torch.distributed, ncclCommInitRank,
+    then the usual parity.  (Multi-rank NCCL needs several GPUs; its host
+    logic is covered by tests/test_dist_gloo.py.)"""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        n = 15
+        gates = kitchen_sink(n, seed=5)
+        sim = P.QSim.distributed(n)
+        sim.init_basis(9)
+        sim.run_circuit(gates)
+        o = oracle_run(oracle_mod, n, 9, gates)
+        assert_parity(sim, o, n)
+        assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-13
+        sim.close()
+    finally:
+        dist.destroy_process_group()
