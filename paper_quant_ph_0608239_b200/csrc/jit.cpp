@@ -31,8 +31,9 @@ struct Layout {
     size_t off_out = (kOffTs + 4 * kTileBits + 7) / 8 * 8, off_m = 0, bytes = 0;  // natural u64 alignment
 };
 
-// generator variants (env, for A/B experiments): minimum CTAs per SM and
-// persistent grid with L2 prefetch of the next tile
+// generator variant (env, for A/B experiments): minimum CTAs per SM.  A
+// persistent grid with L2 prefetch of the next tile and 1 or 3 CTAs/SM were
+// measured slower on config 2 (register spills / occupancy).
 int env_int(const char *k, int dflt)
 {
     const char *v = getenv(k);
@@ -62,18 +63,15 @@ JitPass jit_generate(const Step &st)
     std::vector<int> out_idx, m_idx;
     Layout L = layout_of(st, out_idx, m_idx);
     std::ostringstream s;
-    const int minb = env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2), pf = env_int("QSIM_JIT_PREFETCH", 0);
-    const int loop = env_int("QSIM_JIT_PERSIST", 0) > 0;
-    s << "// minb=" << minb << " prefetch=" << pf << " loop=" << loop << "\n";
+    const int minb = env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2);  // CTAs per SM (register cap)
+    s << "// minb=" << minb << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
          "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
-    // (the volatile move keeps ptxas from hoisting the 12 loop-invariant masks
-    // of the persistent variant into long-lived registers)
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
-         "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { int t; asm volatile(\"mov.b32 %0, %1;\" : "
-         "\"=r\"(t) : \"r\"(ts[j])); b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
+         "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
+         "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
     // e^{2 pi i t / 2^64}: table of the top 8 bits x Taylor series of the rest (|x| < 2pi/256)
     s << "__device__ __forceinline__ double2 qexp(unsigned long long t, const double2 *tab)\n{\n"
          " const double2 b = __ldg(tab + (t >> 56));\n"
@@ -87,16 +85,8 @@ JitPass jit_generate(const Step &st)
     s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads << ", " << minb
       << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
-    if (loop) {
-        // lane/warp re-read every iteration (asm volatile) so ptxas cannot hoist the
-        // per-config address terms out of the loop and raise register pressure
-        s << " for (unsigned long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {\n";
-        s << " int tid_; asm volatile(\"mov.u32 %0, %%tid.x;\" : \"=r\"(tid_));\n";
-        s << " const int lane = tid_ & 31, warp = tid_ >> 5;\n";
-    } else {
-        s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-        s << " { const unsigned long long inst = blockIdx.x;\n";
-    }
+    s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    s << " { const unsigned long long inst = blockIdx.x;\n";
     s << " const unsigned long long base = qdep(inst, P.ts);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
@@ -124,12 +114,6 @@ JitPass jit_generate(const Step &st)
              "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
           << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
           << " = make_double2(x2, x3); }\n";
-    if (pf && loop) {
-        s << "  if ((lane & 3) == 0 && inst + gridDim.x < P.n_inst) {\n";
-        s << "   const double2 *q = P.st + qdep(inst + gridDim.x, P.ts) + (" << gaddr(cur) << ");\n";
-        for (int j = 0; j < 8; j++) s << "   asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(q + (" << roff(cur, j) << ")));\n";
-        s << "  }\n";
-    }
     s << " }\n";
     auto smem_z = [&](uint64_t c, const char *tag) {
         s << "  const int zt" << tag << " = ";
@@ -262,7 +246,6 @@ JitPass jit_generate(const Step &st)
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
     s << " }\n";
-    if (loop) s << " __syncthreads();\n";
     s << " }\n}\n";
     JitPass jp;
     jp.src = s.str();
@@ -410,8 +393,7 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2) | ((uint64_t)env_int("QSIM_JIT_PREFETCH", 0) << 8) |
-        ((uint64_t)(env_int("QSIM_JIT_PERSIST", 0) > 0) << 16));
+    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));

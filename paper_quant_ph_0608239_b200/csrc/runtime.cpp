@@ -633,9 +633,7 @@ static qsim_status flush(qsim_ctx c)
                     void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                                      CU_LAUNCH_PARAM_END};
                     const unsigned smem = s.pass.use_smem ? kTileAmps * 16 : 0;
-                    static const int persist = getenv("QSIM_JIT_PERSIST") ? atoi(getenv("QSIM_JIT_PERSIST")) : 0;
-                    uint64_t grid = s.pass.n_inst;
-                    if (persist > 0 && grid > (uint64_t)persist * 148) grid = (uint64_t)persist * 148;
+                    const uint64_t grid = s.pass.n_inst;
                     CUresult cr = drv().launchKernel(fn, (unsigned)grid, 1, 1, kPassThreads, 1, 1, smem,
                                                  (CUstream)c->stream, nullptr, extra);
                     if (cr != CUDA_SUCCESS) {
