@@ -129,7 +129,8 @@ JitPass jit_generate(const Step &st)
             if ((i >> b) & 1) z ^= swz_host(1 << nib(c, b));
         return z;
     };
-    bool acc_used[16] = {false}, in_run = false;
+    bool in_run = false;
+    size_t run_begin = 0;
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
@@ -144,19 +145,51 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         if (op.code == OPC_PHASE_FLUSH) {
-            for (int v = 0; v < 16; v++)
-                if (acc_used[v])
-                    s << "  { const double2 e = qexp(th" << v << ", P.ptab); const double p1 = -e.y * a" << v
-                      << ".y, p2 = e.y * a" << v << ".x; a" << v << ".x = fma(e.x, a" << v << ".x, p1); a" << v
-                      << ".y = fma(e.x, a" << v << ".y, p2); }\n";
+            const PhaseRunPlan pr = plan_phase_run(st.ops.data() + run_begin, o - run_begin);
+            auto sum_below = [&](uint32_t i) {  // theta_i = sum of acc[S], S subset of i
+                std::string e;
+                for (uint32_t S = 0; S < 16; S++)
+                    if (((pr.used >> S) & 1) && (S & i) == S) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
+                return e;
+            };
+            auto mul = [&](const std::string &e, const std::string &v) {
+                s << "  { const double p1 = -" << e << ".y * " << v << ".y, p2 = " << e << ".y * " << v << ".x; " << v
+                  << ".x = fma(" << e << ".x, " << v << ".x, p1); " << v << ".y = fma(" << e << ".x, " << v
+                  << ".y, p2); }\n";
+            };
+            if (pr.mode == 0) {
+                std::vector<std::string> sums;
+                for (int i = 0; i < 16; i++) {
+                    const std::string e = sum_below((uint32_t)i);
+                    if (e.empty()) continue;
+                    size_t k = std::find(sums.begin(), sums.end(), e) - sums.begin();
+                    if (k == sums.size()) {
+                        sums.push_back(e);
+                        s << "  const double2 ex" << k << " = qexp(" << e << ", P.ptab);\n";
+                    }
+                    mul("ex" + std::to_string(k), A(i));
+                }
+            } else {
+                for (uint32_t S = 0; S < 16; S++)
+                    if ((pr.used >> S) & 1) s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n";
+                for (int i = 0; i < 16; i++)
+                    for (uint32_t S = 0; S < 16; S++)
+                        if (((pr.used >> S) & 1) && (S & (uint32_t)i) == S) mul("em" + std::to_string(S), A(i));
+            }
             s << " }\n";
             in_run = false;
             continue;
         }
         if (op.code == OPC_PHASE_ACC && !in_run) {
-            s << " { unsigned long long th0 = 0, th1 = 0, th2 = 0, th3 = 0, th4 = 0, th5 = 0, th6 = 0, th7 = 0, th8 = 0, "
-                 "th9 = 0, th10 = 0, th11 = 0, th12 = 0, th13 = 0, th14 = 0, th15 = 0;\n";
-            for (int v = 0; v < 16; v++) acc_used[v] = false;
+            // open the run scope and declare the monomial accumulators it uses
+            size_t e = o;
+            while (e < st.ops.size() && st.ops[e].code == OPC_PHASE_ACC) e++;
+            const PhaseRunPlan pr = plan_phase_run(st.ops.data() + o, e - o);
+            s << " {";
+            for (uint32_t S = 0; S < 16; S++)
+                if ((pr.used >> S) & 1) s << " unsigned long long mo" << S << " = 0;";
+            s << "\n";
+            run_begin = o;
             in_run = true;
         }
         const bool plw = op.mlane || op.mwarp;  // thread-dependent predicate
@@ -174,10 +207,10 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_PHASE_ACC) {
             s << "  const unsigned long long K = " << (sel ? "tp ? " : "") << "(unsigned long long)__double_as_longlong("
               << M << "[2])" << (sel ? " : 0ULL" : "") << ";\n";
-            for (int i = 0; i < 16; i++) {
-                if ((i & op.mreg) != op.vreg) continue;
-                s << "  th" << reg[i] << " += K;\n";
-                acc_used[reg[i]] = true;
+            const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
+            for (uint32_t T = Z;; T = (T - 1) & Z) {
+                s << "  mo" << (O | T) << (__builtin_popcount(T) & 1 ? " -= K;\n" : " += K;\n");
+                if (!T) break;
             }
         } else if (op.code == OPC_PHASE) {
             for (int i = 0; i < 16; i++) {

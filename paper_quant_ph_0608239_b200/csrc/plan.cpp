@@ -100,6 +100,42 @@ void Planner::choose_initial_layout(const std::vector<GateRec> &gates)
     for (int p = 0; p < n; p++) { qubit_at[p] = order[p]; phys_of[order[p]] = p; }
 }
 
+PhaseRunPlan plan_phase_run(const KOp *ops, size_t n)
+{
+    PhaseRunPlan r;
+    for (size_t o = 0; o < n; o++) {
+        const uint32_t m = ops[o].mreg, v = ops[o].vreg, O = m & v, Z = m & ~v;
+        for (uint32_t i = 0; i < 16; i++)
+            if ((i & m) == v) r.direct += 4;
+        for (uint32_t T = Z;; T = (T - 1) & Z) {  // subsets of Z
+            r.used |= 1u << (O | T);
+            r.acc += 2;  // one 64-bit add
+            if (!T) break;
+        }
+    }
+    const double kExp = 20, kMul = 4;  // e^{i theta} (table x Taylor) and complex multiply
+    // mode A: distinct (set of monomials below register i) -> one exp each
+    uint32_t keys[16];
+    int nkeys = 0, nregs = 0;
+    for (uint32_t i = 0; i < 16; i++) {
+        uint32_t key = 0;
+        for (uint32_t S = 0; S < 16; S++)
+            if (((r.used >> S) & 1) && (S & i) == S) key |= 1u << S;
+        if (!key) continue;
+        nregs++;
+        bool seen = false;
+        for (int k = 0; k < nkeys; k++) seen |= keys[k] == key;
+        if (!seen) keys[nkeys++] = key;
+    }
+    const double costA = nkeys * kExp + nregs * kMul;
+    double costB = 0;
+    for (uint32_t S = 0; S < 16; S++)
+        if ((r.used >> S) & 1) costB += kExp + kMul * (double)(16 >> __builtin_popcount(S));
+    r.mode = costB < costA ? 1 : 0;
+    r.acc += std::min(costA, costB);
+    return r;
+}
+
 // ------------------------------------------------------------------ passes
 namespace {
 struct POp {
@@ -273,16 +309,8 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
     for (size_t a = 0; a < st.ops.size();) {
         size_t b = a;
         while (b < st.ops.size() && st.ops[b].code == OPC_PHASE) b++;
-        // cost model (FP64-pipe ops per thread): direct = 4 per touched register per
-        // op; accumulated = integer adds + one e^{i theta} (~20) + cmul per touched register
-        double direct = 0;
-        uint32_t touched = 0;
-        for (size_t o = a; o < b; o++) {
-            const KOp &op = st.ops[o];
-            for (uint32_t i = 0; i < 16; i++)
-                if ((i & op.mreg) == op.vreg) { direct += 4; touched |= 1u << i; }
-        }
-        const double acc = 24.0 * __builtin_popcount(touched);  // table x Taylor flush (jit.cpp qexp)
+        const PhaseRunPlan pr = plan_phase_run(st.ops.data() + a, b - a);
+        const double direct = pr.direct, acc = pr.acc;
         if (b - a >= (size_t)kPhaseRunMin && acc < 0.8 * direct) {
             for (size_t o = a; o < b; o++) {
                 KOp &op = st.ops[o];

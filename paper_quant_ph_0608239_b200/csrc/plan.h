@@ -28,6 +28,19 @@ struct GateRec {
 
 void classify(GateRec &g);  // sets cls, qN, qD
 
+// Phase runs (engine.h OPC_PHASE_ACC): register predicate (i & m) == v expands
+// into monomials x^S = prod_{b in S} i_b over the 4 register bits; an op adds
+// its angle to acc[S] (sign (-1)^|T|, S = O | T, T subset of the zero bits).
+// The flush applies e^{i theta_i}, theta_i = sum_{S subset of i} acc[S], either
+// per distinct register angle (mode A) or per monomial (mode B).
+struct PhaseRunPlan {
+    uint32_t used = 0;      // monomials S (bit S of the 16-bit set) with an accumulator
+    double direct = 0;      // FP64-pipe ops per thread applying the run op by op
+    double acc = 0;         // integer adds + flush (cheaper mode)
+    int mode = 0;           // 0: per register angle, 1: per monomial
+};
+PhaseRunPlan plan_phase_run(const KOp *ops, size_t n);
+
 enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5, ST_PAIRWISE = 6 };
 
 // global-target policy: remap (K-pair interchange),
