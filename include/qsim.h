@@ -186,8 +186,11 @@ qsim_status qsim_sync(qsim_ctx ctx);
 qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
 
 /* Options (integers): "fusion" (1 = fused tile passes [default], 0 = one
- * generic kernel per gate), "timing" (1 = CUDA-event time every launch),
- * "max_scan" (planner look-ahead window), "exchange_chunk_mb". */
+ * generic kernel per gate), "block_fusion" (1 = inside a pass, gate clusters
+ * on two tile qubits become one 4x4 unitary and one-qubit runs one 2x2
+ * [default]; 0 = every gate applied as given), "timing" (1 = CUDA-event time
+ * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb",
+ * "jit", "plan_cache", "pass_variant", "global_policy". */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {
@@ -225,7 +228,7 @@ const char *qsim_last_error(qsim_ctx ctx);
  * description of the steps (passes, perms, exchanges, pairwise combines,
  * relabels) into buf.  flags: bits 0-1 = fusion (0 off, 1 on, 2 on + NVRTC-
  * compile the pass kernels as a host-only check); bits 4-5 = global policy
- * + 1 (0 = default auto).  Returns QSIM_ERR_ARG if buf is too small. */
+ * + 1 (0 = default auto); bit 8 = no block fusion.  Returns QSIM_ERR_ARG if buf is too small. */
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
                            int flags, char *buf, size_t buf_bytes);
 

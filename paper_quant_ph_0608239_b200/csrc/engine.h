@@ -48,7 +48,14 @@ enum OpCode : int32_t {
     // e^{i theta} (JIT tier).  The interpreter applies OPC_PHASE_ACC like
     // OPC_PHASE (same m[0], m[1]) and ignores OPC_PHASE_FLUSH.
     OPC_PHASE_ACC = 5,
-    OPC_PHASE_FLUSH = 6
+    OPC_PHASE_FLUSH = 6,
+    // Fused two-qubit block (plan.cpp fuse_blocks): a general complex 4x4 on
+    // register bits k < k2 (k2 in `cfg`), 4x4 index j = bit_k + 2 bit_k2.
+    // m[] holds row 0; the next three ops (OPC_DATA) hold rows 1..3.  Never
+    // predicated.  16 FMA-pipe ops per amplitude, replacing >= 3 gates that
+    // would cost more (a brickwork U2 (x) U2, CNOT, U2 (x) U2 block: 32).
+    OPC_U4 = 7,
+    OPC_DATA = 8
 };
 
 enum Role : int32_t { ROLE_REG = 0, ROLE_LANE = 1, ROLE_WARP = 2, ROLE_OUT = 3 };
@@ -63,7 +70,7 @@ struct alignas(16) KOp {
     uint32_t mlane, vlane;
     uint32_t mwarp, vwarp;
     uint64_t mout, vout;
-    uint64_t cfg;  // OPC_TRANS: the new config
+    uint64_t cfg;  // OPC_TRANS: the new config; OPC_PHASE_ACC: angle; OPC_U4: k2
     uint64_t pad;
     double m[8];  // u00r u00i u01r u01i u10r u10i u11r u11i ; PHASE: f = (m[0], m[1])
 };

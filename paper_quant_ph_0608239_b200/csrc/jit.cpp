@@ -180,6 +180,32 @@ JitPass jit_generate(const Step &st)
             in_run = false;
             continue;
         }
+        if (op.code == OPC_DATA) continue;  // rows 1..3 of the preceding OPC_U4
+        if (op.code == OPC_U4) {
+            // same FMA chains, in the same order, as kernels.cu u4_apply
+            const int k = op.k, k2 = (int)op.cfg;
+            s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
+            for (int p = 0; p < 4; p++) {
+                int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
+                i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
+                const int idx[4] = {i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)};
+                s << "  { const double2 x0 = " << A(idx[0]) << ", x1 = " << A(idx[1]) << ", x2 = " << A(idx[2])
+                  << ", x3 = " << A(idx[3]) << ";\n";
+                for (int r = 0; r < 4; r++) {
+                    const std::string R = "P.m[" + std::to_string(m_idx[o] + r) + "]";
+                    s << "   { double re = " << R << "[0] * x0.x, im = " << R << "[0] * x0.y; re = fma(-" << R
+                      << "[1], x0.y, re); im = fma(" << R << "[1], x0.x, im);";
+                    for (int c = 1; c < 4; c++)
+                        s << " re = fma(" << R << "[" << 2 * c << "], x" << c << ".x, re); re = fma(-" << R << "["
+                          << 2 * c + 1 << "], x" << c << ".y, re); im = fma(" << R << "[" << 2 * c << "], x" << c
+                          << ".y, im); im = fma(" << R << "[" << 2 * c + 1 << "], x" << c << ".x, im);";
+                    s << " " << A(idx[r]) << " = make_double2(re, im); }\n";
+                }
+                s << "  }\n";
+            }
+            s << " }\n";
+            continue;
+        }
         if (op.code == OPC_PHASE_ACC && !in_run) {
             // open the run scope and declare the monomial accumulators it uses
             size_t e = o;
@@ -432,7 +458,7 @@ std::string jit_key(const Step &st)
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
         put((uint64_t)op.mreg | ((uint64_t)op.vreg << 8) | ((uint64_t)op.mlane << 16) | ((uint64_t)op.vlane << 24) |
             ((uint64_t)op.mwarp << 32) | ((uint64_t)op.vwarp << 40));
-        if (op.code == OPC_TRANS) put(op.cfg);
+        if (op.code == OPC_TRANS || op.code == OPC_U4) put(op.cfg);
     }
     return k;
 }

@@ -127,6 +127,48 @@ __device__ __forceinline__ void reg_op(double2 (&a)[16], const KOp &op, int code
     else reg_dispatch<OPC_U2, PRED>(a, op, k, mreg, vreg);
 }
 
+// Fused 4x4 block (OPC_U4) on register bits K < K2; rows[r].m = row r of the
+// complex matrix, 4x4 index j = bit_K + 2 bit_K2.  Each output is one
+// 8-long FMA chain for re and one for im, in the fixed column order the JIT
+// tier generates too (bitwise-identical tiers).
+template <int K, int K2>
+__device__ __forceinline__ void u4_apply(double2 (&a)[16], const KOp *rows)
+{
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+        const int i0 = (int)insert_zero(insert_zero((uint64_t)p, K), K2);
+        const int idx[4] = {i0, i0 | (1 << K), i0 | (1 << K2), i0 | (1 << K) | (1 << K2)};
+        const double2 x[4] = {a[idx[0]], a[idx[1]], a[idx[2]], a[idx[3]]};
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const double *m = rows[r].m;
+            double re = m[0] * x[0].x, im = m[0] * x[0].y;
+            re = fma(-m[1], x[0].y, re);
+            im = fma(m[1], x[0].x, im);
+#pragma unroll
+            for (int c = 1; c < 4; c++) {
+                re = fma(m[2 * c], x[c].x, re);
+                re = fma(-m[2 * c + 1], x[c].y, re);
+                im = fma(m[2 * c], x[c].y, im);
+                im = fma(m[2 * c + 1], x[c].x, im);
+            }
+            a[idx[r]] = make_double2(re, im);
+        }
+    }
+}
+
+__device__ __forceinline__ void u4_op(double2 (&a)[16], const KOp *rows)
+{
+    switch (rows[0].k * 4 + (int)rows[0].cfg) {
+    case 1: u4_apply<0, 1>(a, rows); break;
+    case 2: u4_apply<0, 2>(a, rows); break;
+    case 3: u4_apply<0, 3>(a, rows); break;
+    case 6: u4_apply<1, 2>(a, rows); break;
+    case 7: u4_apply<1, 3>(a, rows); break;
+    default: u4_apply<2, 3>(a, rows); break;
+    }
+}
+
 // Shared-memory layout of a tile: 16-B unit of tile-local index s sits at
 // swz(s) = s ^ fold3(s >> 3).  Tile-local bit t lands in 16-B bank group
 // residue t mod 3, so a warp access whose 5 lane bits cover all three
@@ -226,7 +268,12 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
             __syncthreads();
             continue;
         }
-        if (code == OPC_PHASE_FLUSH) continue;
+        if (code == OPC_PHASE_FLUSH || code == OPC_DATA) continue;
+        if (code == OPC_U4) {
+            u4_op(a, &P.ops[o]);
+            o += 3;
+            continue;
+        }
         const bool tp = ((lane & op.mlane) == op.vlane) && ((warp & op.mwarp) == op.vwarp) &&
                         ((gcta & op.mout) == op.vout);
         if (!tp) continue;

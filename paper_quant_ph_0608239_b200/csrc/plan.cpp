@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <limits>
 #include <sstream>
@@ -41,7 +42,7 @@ void classify(GateRec &g)
     } else if (g.kind == GK_PERM) {
         for (int c : g.controls) g.qD |= bit(c);
         for (int t : g.targets) g.qN |= bit(t);
-    } else {
+    } else {  // SWAP, U4
         for (int t : g.targets) g.qN |= bit(t);
     }
 }
@@ -138,12 +139,17 @@ PhaseRunPlan plan_phase_run(const KOp *ops, size_t n)
 
 // ------------------------------------------------------------------ passes
 namespace {
+constexpr int OP_BARRIER = -1;  // fusion only: an unfusable gate on the qubits in cm
+
 struct POp {
-    int code;      // OPC_U2 / OPC_U2R / OPC_XS / OPC_PHASE
-    int t;         // physical target (U2-type)
+    int code;      // OPC_U2 / OPC_U2R / OPC_XS / OPC_PHASE / OPC_U4 / OP_BARRIER
+    int t;         // physical target (U2-type); U4: physical bit of 4x4 index bit 0
     uint64_t cm, cv;
     double m[8];
     int gid;
+    int t2 = -1;   // U4: physical bit of 4x4 index bit 1
+    double m4[32]; // U4: row-major complex 4x4 (re, im)
+    bool fused = false;  // made by fuse_ops
 };
 
 }  // namespace
@@ -211,10 +217,260 @@ Cfg make_cfg(const std::vector<int> &reg_in, bool store)
     return c;
 }
 
+// physical bits an op acts on non-diagonally (a barrier op: none)
+uint64_t nondiag(const POp &p)
+{
+    if (p.code == OPC_PHASE || p.code == OP_BARRIER) return 0;
+    return bit(p.t) | (p.t2 >= 0 ? bit(p.t2) : 0);
+}
+
 bool conflict(const POp &a, const POp &b)
 {
-    const uint64_t Na = a.code == OPC_PHASE ? 0 : bit(a.t), Nb = b.code == OPC_PHASE ? 0 : bit(b.t);
+    const uint64_t Na = nondiag(a), Nb = nondiag(b);
     return (Na & (Nb | b.cm)) || (a.cm & Nb);
+}
+
+// ------------------------------------------------- two-qubit block fusion
+// On a fused random layer the pass is bound by the FP64 pipe (DESIGN.md
+// §5.2), not by HBM.  A cluster of gates acting only on two qubits {a, b} --
+// e.g. the brickwork's U2 (x) U2, CNOT, U2 (x) U2 -- equals one 4x4 unitary
+// (the product of the gates' embeddings, Eqs. NUM2-NUM8 written on the 4-dim
+// subspace), which costs 16 FMA-pipe ops per amplitude instead of 8 per
+// general U2.  Greedy, in sequence order: every two-qubit gate seeds a block
+// that absorbs the neighbouring gates on {a, b} that can move next to it (no
+// unabsorbed gate on a shared qubit in between); the block is kept only if it
+// is cheaper than its gates.  Runs of one-qubit gates on one qubit merge into
+// one U2 the same way.  Used on the logical gate list before passes are
+// formed (Planner::plan, so blocks are never cut by a pass boundary) and on
+// each pass's op list (for what the first round left).
+uint64_t qset(const POp &p) { return nondiag(p) | p.cm; }
+
+// FMA-pipe ops per amplitude of the shard (touched fraction included)
+double op_cost(const POp &p)
+{
+    const double touched = std::ldexp(1.0, -__builtin_popcountll(p.cm));
+    switch (p.code) {
+    case OPC_U2: return 8 * touched;
+    case OPC_U2R: return 4 * touched;
+    case OPC_XS: return 0;
+    case OPC_PHASE: return 4 * touched;
+    case OPC_U4: return 16;
+    }
+    return 0;
+}
+
+typedef std::complex<double> cd;
+
+// 4x4 embedding of op p on the subspace index j = bit(pa) + 2 bit(pb)
+void embed4(const POp &p, int pa, int pb, cd E[4][4])
+{
+    for (int r = 0; r < 4; r++)
+        for (int c = 0; c < 4; c++) E[r][c] = 0;
+    if (p.code == OPC_U4) {
+        const bool flip = p.t != pa;  // p's index bit 0 is pb
+        auto pm = [&](int x) { return flip ? ((x & 1) << 1) | (x >> 1) : x; };
+        for (int r = 0; r < 4; r++)
+            for (int c = 0; c < 4; c++)
+                E[r][c] = cd(p.m4[8 * pm(r) + 2 * pm(c)], p.m4[8 * pm(r) + 2 * pm(c) + 1]);
+        return;
+    }
+    auto pred = [&](int j) {
+        for (int s = 0; s < 2; s++) {
+            const int pos = s ? pb : pa;
+            if (((p.cm >> pos) & 1) && (int)((p.cv >> pos) & 1) != ((j >> s) & 1)) return false;
+        }
+        return true;
+    };
+    for (int j = 0; j < 4; j++) {
+        if (!pred(j)) { E[j][j] = 1; continue; }
+        if (p.code == OPC_PHASE) { E[j][j] = cd(p.m[0], p.m[1]); continue; }
+        const int s = p.t == pa ? 0 : 1;
+        const int bj = (j >> s) & 1, j0 = j & ~(1 << s), j1 = j0 | (1 << s);
+        E[j0][j] = cd(p.m[bj ? 2 : 0], p.m[bj ? 3 : 1]);  // U[0][bj]
+        E[j1][j] = cd(p.m[bj ? 6 : 4], p.m[bj ? 7 : 5]);  // U[1][bj]
+    }
+}
+
+// absorb into the cluster seeded at g the ops on `mask` that can move next to it
+std::vector<size_t> cluster(const std::vector<POp> &ops, const std::vector<char> &used, size_t g, uint64_t mask,
+                            bool allow_pairs)
+{
+    std::vector<size_t> got{g};
+    auto ok = [&](size_t h, uint64_t stopped) {
+        const POp &p = ops[h];
+        const uint64_t S = qset(p);
+        if (used[h] || p.code == OP_BARRIER || (S & ~mask) || (S & stopped)) return false;
+        if (!allow_pairs) return p.code != OPC_PHASE && p.code != OPC_U4 && !p.cm;
+        return true;
+    };
+    uint64_t stopped = 0;
+    for (size_t h = g; h-- > 0 && stopped != mask;) {
+        const uint64_t S = qset(ops[h]);
+        if (!(S & mask)) continue;
+        if (ok(h, stopped)) got.push_back(h);
+        else stopped |= S & mask;
+    }
+    stopped = 0;
+    for (size_t h = g + 1; h < ops.size() && stopped != mask; h++) {
+        const uint64_t S = qset(ops[h]);
+        if (!(S & mask)) continue;
+        if (ok(h, stopped)) got.push_back(h);
+        else stopped |= S & mask;
+    }
+    std::sort(got.begin(), got.end());
+    return got;
+}
+
+// Fuse `ops` in place.  cost[i] = FMA-pipe ops per amplitude of ops[i];
+// pair_ok(c) says whether bit c may be one of a block's two qubits.
+template <class PairOk>
+void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pair_ok)
+{
+    const size_t n = ops.size();
+    std::vector<char> used(n, 0), has_repl(n, 0);
+    std::vector<POp> repl(n);
+    // two-qubit blocks
+    for (size_t g = 0; g < n; g++) {
+        const POp &s = ops[g];
+        if (used[g] || s.code == OPC_PHASE || s.code == OP_BARRIER) continue;
+        int pa, pb;
+        if (s.code == OPC_U4) {
+            pa = std::min(s.t, s.t2);
+            pb = std::max(s.t, s.t2);
+        } else {
+            if (__builtin_popcountll(s.cm) != 1) continue;
+            const int c = __builtin_ctzll(s.cm);
+            pa = std::min(c, s.t);
+            pb = std::max(c, s.t);
+        }
+        if (!pair_ok(pa) || !pair_ok(pb)) continue;
+        const uint64_t mask = bit(pa) | bit(pb);
+        std::vector<size_t> got = cluster(ops, used, g, mask, true);
+        double before = 0;
+        for (size_t h : got) before += cost[h];
+        if (got.size() < 2 || before <= 16 + 2) continue;  // a 4x4 costs 16 + register copies
+        cd B[4][4], E[4][4], T[4][4];
+        for (int r = 0; r < 4; r++)
+            for (int q = 0; q < 4; q++) B[r][q] = r == q ? 1 : 0;
+        for (size_t h : got) {  // B <- E_h B, in sequence order
+            embed4(ops[h], pa, pb, E);
+            for (int r = 0; r < 4; r++)
+                for (int q = 0; q < 4; q++) {
+                    cd acc = 0;
+                    for (int k = 0; k < 4; k++) acc += E[r][k] * B[k][q];
+                    T[r][q] = acc;
+                }
+            for (int r = 0; r < 4; r++)
+                for (int q = 0; q < 4; q++) B[r][q] = T[r][q];
+        }
+        POp u{};
+        u.code = OPC_U4;
+        u.fused = true;
+        u.t = pa;
+        u.t2 = pb;
+        u.gid = s.gid;
+        for (int r = 0; r < 4; r++)
+            for (int q = 0; q < 4; q++) {
+                u.m4[8 * r + 2 * q] = B[r][q].real();
+                u.m4[8 * r + 2 * q + 1] = B[r][q].imag();
+            }
+        for (size_t h : got) used[h] = 1;
+        repl[g] = u;
+        has_repl[g] = 1;
+    }
+    // runs of one-qubit gates on one qubit
+    for (size_t g = 0; g < n; g++) {
+        const POp &s = ops[g];
+        if (used[g] || s.code == OPC_PHASE || s.code == OPC_U4 || s.code == OP_BARRIER || s.cm) continue;
+        std::vector<size_t> got = cluster(ops, used, g, bit(s.t), false);
+        if (got.size() < 2) continue;
+        cd U[2][2] = {{1, 0}, {0, 1}};
+        double before = 0;
+        for (size_t h : got) {
+            const POp &p = ops[h];
+            before += cost[h];
+            const cd V[2][2] = {{cd(p.m[0], p.m[1]), cd(p.m[2], p.m[3])}, {cd(p.m[4], p.m[5]), cd(p.m[6], p.m[7])}};
+            cd W[2][2];
+            for (int r = 0; r < 2; r++)
+                for (int q = 0; q < 2; q++) W[r][q] = V[r][0] * U[0][q] + V[r][1] * U[1][q];
+            for (int r = 0; r < 2; r++)
+                for (int q = 0; q < 2; q++) U[r][q] = W[r][q];
+        }
+        POp u{};
+        u.fused = true;
+        u.t = s.t;
+        u.gid = s.gid;
+        const double m[8] = {U[0][0].real(), U[0][0].imag(), U[0][1].real(), U[0][1].imag(),
+                             U[1][0].real(), U[1][0].imag(), U[1][1].real(), U[1][1].imag()};
+        for (int k = 0; k < 8; k++) u.m[k] = m[k];
+        const bool xs = m[0] == 0 && m[1] == 0 && m[6] == 0 && m[7] == 0 && m[2] == 1 && m[3] == 0 && m[4] == 1 &&
+                        m[5] == 0;
+        const bool real = m[1] == 0 && m[3] == 0 && m[5] == 0 && m[7] == 0;
+        u.code = xs ? OPC_XS : real ? OPC_U2R : OPC_U2;
+        if (op_cost(u) >= before) continue;
+        for (size_t h : got) used[h] = 1;
+        repl[g] = u;
+        has_repl[g] = 1;
+    }
+    std::vector<POp> out;
+    for (size_t g = 0; g < n; g++) {
+        if (has_repl[g]) out.push_back(repl[g]);
+        else if (!used[g]) out.push_back(ops[g]);
+    }
+    ops.swap(out);
+}
+
+void fuse_blocks(std::vector<POp> &ops, const int tl_of[64])
+{
+    std::vector<double> cost;
+    for (const POp &p : ops) cost.push_back(op_cost(p));
+    fuse_ops(ops, cost, [&](int c) { return c < 64 && tl_of[c] >= 0; });
+}
+
+// the same fusion on the LOGICAL gate list (qubit numbers as bits)
+std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_blocks_on)
+{
+    std::vector<POp> ops(gates.size());
+    std::vector<double> cost(gates.size());
+    for (size_t i = 0; i < gates.size(); i++) {
+        const GateRec &g = gates[i];
+        POp &p = ops[i];
+        p = POp{};
+        p.gid = (int)i;
+        if (g.kind != GK_U2) {
+            p.code = OP_BARRIER;
+            p.t = -1;
+            p.cm = g.qN | g.qD;
+            continue;
+        }
+        p.t = g.target;
+        for (int c : g.controls) p.cm |= bit(c);
+        p.cv = p.cm;
+        for (int k = 0; k < 8; k++) p.m[k] = g.u[k];
+        p.code = g.cls == CLS_XS ? OPC_XS : g.cls == CLS_REAL ? OPC_U2R : OPC_U2;
+        const double touched = std::ldexp(1.0, -(int)g.controls.size());
+        cost[i] = (g.cls == CLS_GENERAL ? 8 : g.cls == CLS_XS ? 0 : 4) * touched;
+    }
+    fuse_ops(ops, cost, [&](int q) { return !((no_blocks_on >> q) & 1); });
+    std::vector<GateRec> out;
+    out.reserve(ops.size());
+    for (const POp &p : ops) {
+        if (!p.fused) { out.push_back(gates[p.gid]); continue; }
+        GateRec r;
+        r.id = gates[p.gid].id;
+        if (p.code == OPC_U4) {
+            r.kind = GK_U4;
+            r.targets = {p.t, p.t2};
+            for (int k = 0; k < 32; k++) r.u4[k] = p.m4[k];
+        } else {
+            r.kind = GK_U2;
+            r.target = p.t;
+            for (int k = 0; k < 8; k++) r.u[k] = p.m[k];
+        }
+        classify(r);
+        out.push_back(std::move(r));
+    }
+    return out;
 }
 }  // namespace
 
@@ -235,6 +491,11 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         return true;
     };
     auto tl = [&](const POp &p) { return tl_of[p.t]; };
+    auto in_regs = [&](const Cfg &c, const POp &p) {
+        int j;
+        if (c.role_of(tl_of[p.t], j) != ROLE_REG) return false;
+        return p.t2 < 0 || c.role_of(tl_of[p.t2], j) == ROLE_REG;
+    };
     // upcoming register bits: targets of ready ops first, then of the rest, in order
     auto upcoming = [&](bool store, std::vector<int> &reg) {
         reg.clear();
@@ -243,9 +504,17 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             for (size_t b = 0; b < n && reg.size() < 4; b++) {
                 if (done[b] || pops[b].code == OPC_PHASE) continue;
                 if ((pass == 0) != ready(b)) continue;
-                int t = tl(pops[b]);
-                if (store && (t == 1 || t == 2)) continue;
-                if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
+                std::vector<int> need;
+                need.push_back(tl(pops[b]));
+                if (pops[b].t2 >= 0) need.push_back(tl_of[pops[b].t2]);
+                bool skip = false;
+                for (int t : need) skip |= store && (t == 1 || t == 2);
+                if (skip) continue;
+                std::vector<int> add;
+                for (int t : need)
+                    if (std::find(reg.begin(), reg.end(), t) == reg.end()) add.push_back(t);
+                if (reg.size() + add.size() > 4) continue;  // a block needs both of its bits at once
+                for (int t : add) reg.push_back(t);
             }
         for (int t = 3; reg.size() < 4 && t < kTileBits; t++)
             if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
@@ -261,6 +530,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         st.ops.push_back(tr);
         st.op_gate.push_back(-1);
         st.op_t.push_back(-1);
+        st.op_t2.push_back(-1);
         st.op_cm.push_back(0);
         st.op_cv.push_back(0);
     };
@@ -269,8 +539,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         size_t pick = n;
         for (size_t b = 0; b < n; b++) {
             if (done[b] || !ready(b)) continue;
-            int j;
-            if (pops[b].code == OPC_PHASE || cfg.role_of(tl(pops[b]), j) == ROLE_REG) { pick = b; break; }
+            if (pops[b].code == OPC_PHASE || in_regs(cfg, pops[b])) { pick = b; break; }
         }
         if (pick == n) {
             upcoming(false, reg);
@@ -287,6 +556,37 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             op.k = j;
         }
         for (int k = 0; k < 8; k++) op.m[k] = p.m[k];
+        if (p.code == OPC_U4) {
+            // register bits k < k2; 4x4 index bit 0 <-> register bit k
+            int j2 = 0;
+            cfg.role_of(tl_of[p.t2], j2);
+            const bool flip = j > j2;
+            int pt = p.t, pt2 = p.t2;
+            if (flip) { std::swap(j, j2); std::swap(pt, pt2); }
+            auto perm = [&](int x) { return flip ? ((x & 1) << 1) | (x >> 1) : x; };
+            KOp rows[4];
+            for (int r = 0; r < 4; r++) {
+                rows[r] = KOp{};
+                rows[r].code = r ? OPC_DATA : OPC_U4;
+                for (int q = 0; q < 4; q++) {
+                    rows[r].m[2 * q] = p.m4[8 * perm(r) + 2 * perm(q)];
+                    rows[r].m[2 * q + 1] = p.m4[8 * perm(r) + 2 * perm(q) + 1];
+                }
+            }
+            rows[0].k = j;
+            rows[0].cfg = (uint64_t)j2;
+            for (int r = 0; r < 4; r++) {
+                st.ops.push_back(rows[r]);
+                st.op_gate.push_back(r ? -1 : p.gid);
+                st.op_t.push_back(r ? -1 : pt);
+                st.op_t2.push_back(r ? -1 : pt2);
+                st.op_cm.push_back(0);
+                st.op_cv.push_back(0);
+            }
+            done[pick] = 1;
+            left--;
+            continue;
+        }
         for (int b = 0; b < 64; b++) {
             if (!((p.cm >> b) & 1)) continue;
             const uint32_t v = (uint32_t)((p.cv >> b) & 1);
@@ -300,6 +600,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         st.ops.push_back(op);
         st.op_gate.push_back(p.gid);
         st.op_t.push_back(p.code == OPC_PHASE ? -1 : p.t);
+        st.op_t2.push_back(-1);
         st.op_cm.push_back(p.cm);
         st.op_cv.push_back(p.cv);
         done[pick] = 1;
@@ -325,6 +626,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             st.ops.insert(st.ops.begin() + b, fl);
             st.op_gate.insert(st.op_gate.begin() + b, -1);
             st.op_t.insert(st.op_t.begin() + b, -1);
+            st.op_t2.insert(st.op_t2.begin() + b, -1);
             st.op_cm.insert(st.op_cm.begin() + b, 0);
             st.op_cv.insert(st.op_cv.begin() + b, 0);
             b++;
@@ -372,6 +674,23 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
             continue;
         }
         if (g.kind == GK_PERM) { block(); continue; }
+        if (g.kind == GK_U4) {
+            const int t0 = phys_of[g.targets[0]], t1 = phys_of[g.targets[1]];
+            if (t0 >= M || t1 >= M) { block(); continue; }
+            const int extra = (!in_tile[t0]) + (!in_tile[t1]);
+            if ((int)freeb.size() + extra > kTileBits - 3) { block(); continue; }
+            for (int t : {t0, t1})
+                if (!in_tile[t]) { in_tile[t] = true; freeb.push_back(t); }
+            POp p{};
+            p.code = OPC_U4;
+            p.t = t0;
+            p.t2 = t1;
+            for (int k = 0; k < 32; k++) p.m4[k] = g.u4[k];
+            p.gid = g.id;
+            pops.push_back(p);
+            done[i] = 1;
+            continue;
+        }
         uint64_t cm = 0;
         for (int c : g.controls) cm |= bit(phys_of[c]);
         if (g.cls == CLS_DIAG) {
@@ -409,8 +728,8 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     // tile: physical bits 0,1,2 + the free bits (first-use order), filled up to 12
     std::vector<int> order;
     for (const POp &p : pops)
-        if (p.code != OPC_PHASE && p.t >= 3 && std::find(order.begin(), order.end(), p.t) == order.end())
-            order.push_back(p.t);
+        for (int t : {p.code == OPC_PHASE ? -1 : p.t, p.t2})
+            if (t >= 3 && std::find(order.begin(), order.end(), t) == order.end()) order.push_back(t);
     for (int b : freeb)
         if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
     for (int p = 3; (int)order.size() < kTileBits - 3 && p < M; p++)
@@ -423,6 +742,7 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     for (int b = 0; b < 64; b++) tl_of[b] = -1;
     for (int t = 0; t < 3; t++) { d.tp[t] = t; tl_of[t] = t; }
     for (int j = 0; j < kTileBits - 3; j++) { d.tp[3 + j] = order[j]; tl_of[order[j]] = 3 + j; }
+    if (opt.block_fusion) fuse_blocks(pops, tl_of);
     uint64_t cfg0 = 0;
     lower_pass(pops, tl_of, st, cfg0);
     d.cfg0 = cfg0;
@@ -567,11 +887,20 @@ void Planner::remap(const std::vector<int> &local_q, const std::vector<int> &glo
     out.push_back(std::move(s));
 }
 
-void Planner::plan(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out)
+void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &opt, std::vector<Step> &out)
 {
+    const bool fused = opt.fusion && M >= kTileBits;
+    // two-qubit blocks on the whole gate list first (never cut by a pass)
+    std::vector<GateRec> blocked;
+    // No blocks on the initially global qubits: a control or a diagonal gate
+    // there is free (no exchange), and an isolated gate there may go pairwise;
+    // inside a 4x4 block it would be a non-diagonal target.
+    uint64_t no_blocks_on = 0;
+    for (int p = M; p < n; p++) no_blocks_on |= bit(qubit_at[p]);
+    if (fused && opt.block_fusion) blocked = fuse_gates(user_gates, no_blocks_on);
+    const std::vector<GateRec> &gates = fused && opt.block_fusion ? blocked : user_gates;
     std::vector<char> done(gates.size(), 0);
     size_t first = 0;
-    const bool fused = opt.fusion && M >= kTileBits;
     while (true) {
         while (first < gates.size() && done[first]) first++;
         if (first >= gates.size()) break;
@@ -643,12 +972,15 @@ std::string plan_to_json(const Planner &P, const std::vector<Step> &steps)
             for (size_t k = 0; k < st.ops.size(); k++) {
                 const KOp &op = st.ops[k];
                 o << (k ? "," : "") << "{\"gate\":" << st.op_gate[k] << ",\"t\":" << st.op_t[k]
+                  << ",\"t2\":" << (k < st.op_t2.size() ? st.op_t2[k] : -1)
                   << ",\"cm\":" << st.op_cm[k] << ",\"cv\":" << st.op_cv[k] << ",\"code\":" << op.code
                   << ",\"k\":" << op.k << ",\"cfg\":" << op.cfg
                   << ",\"mreg\":" << op.mreg << ",\"vreg\":" << op.vreg << ",\"mlane\":" << op.mlane
                   << ",\"vlane\":" << op.vlane << ",\"mwarp\":" << op.mwarp << ",\"vwarp\":" << op.vwarp
                   << ",\"mout\":" << op.mout << ",\"vout\":" << op.vout << ",\"m\":[";
-                for (int j = 0; j < 8; j++) o << (j ? "," : "") << op.m[j];
+                const int rows = op.code == OPC_U4 ? 4 : 1;  // U4: rows 1..3 in the next ops
+                for (int r = 0; r < rows; r++)
+                    for (int j = 0; j < 8; j++) o << (r || j ? "," : "") << st.ops[k + r].m[j];
                 o << "]}";
             }
             o << "]}";

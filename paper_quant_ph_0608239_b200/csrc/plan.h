@@ -9,7 +9,7 @@
 
 namespace qsb {
 
-enum GateKind { GK_U2 = 0, GK_PERM = 2, GK_SWAP = 3 };
+enum GateKind { GK_U2 = 0, GK_PERM = 2, GK_SWAP = 3, GK_U4 = 4 /* planner-made fused block */ };
 enum GateClass { CLS_GENERAL = 0, CLS_REAL = 1, CLS_DIAG = 2, CLS_XS = 3 };
 
 // A validated gate in LOGICAL qubits.
@@ -17,8 +17,9 @@ struct GateRec {
     int kind = GK_U2;
     int target = -1;                  // U2
     std::vector<int> controls;
-    std::vector<int> targets;         // PERM (register order) / SWAP (2)
+    std::vector<int> targets;         // PERM (register order) / SWAP (2) / U4 (index bits 0, 1)
     double u[8] = {1, 0, 0, 0, 0, 0, 1, 0};
+    double u4[32] = {0};              // U4: row-major complex 4x4
     int cls = CLS_GENERAL;
     std::vector<uint32_t> perm;
     uint64_t qN = 0;  // logical qubits acted on non-diagonally
@@ -54,6 +55,7 @@ struct Step {
     std::vector<KOp> ops;
     std::vector<int> op_gate;     // gate id behind each op (-1 for TRANS)
     std::vector<int> op_t;        // physical target of each op (-1: PHASE/TRANS)
+    std::vector<int> op_t2;       // OPC_U4: physical bit of 4x4 index bit 1 (else -1)
     std::vector<uint64_t> op_cm, op_cv;  // full-index predicate of each op (for introspection)
     // ST_GENERIC: one U2 on physical target t, controls (full-index mask/val)
     // ST_PAIRWISE: one U2 on GLOBAL physical target t (partner shards combine)
@@ -74,6 +76,7 @@ struct Step {
 
 struct PlanOptions {
     bool fusion = true;
+    bool block_fusion = true;  // fuse gate clusters on two tile qubits into 4x4 blocks (OPC_U4)
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
 };

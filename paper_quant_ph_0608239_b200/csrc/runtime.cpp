@@ -78,7 +78,7 @@ struct qsim_ctx_s {
     double *d_red = nullptr;
     size_t d_red_cap = 0;
     // options
-    bool fusion = true, timing = false;
+    bool fusion = true, timing = false, block_fusion = true;
     int max_scan = 1 << 30;
     int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
     int global_policy = GP_AUTO;
@@ -131,12 +131,14 @@ struct qsim_ctx_s {
 
 // algorithmic FP64 FMA-pipe instructions of one pass over a 2^M shard: per
 // touched amplitude 8 for a complex 2x2, 4 for a real 2x2, 4 for a phase,
-// 0 for an exact swap; the predicate bits (controls) halve the touched set
+// 0 for an exact swap, 16 for a fused 4x4 block; the predicate bits (controls)
+// halve the touched set
 static double pass_fp64_slots(const Step &s, int M)
 {
     double tot = 0;
     for (const KOp &op : s.ops) {
-        if (op.code == OPC_TRANS || op.code == OPC_XS || op.code == OPC_PHASE_FLUSH) continue;
+        if (op.code == OPC_TRANS || op.code == OPC_XS || op.code == OPC_PHASE_FLUSH || op.code == OPC_DATA) continue;
+        if (op.code == OPC_U4) { tot += 16 * std::ldexp(1.0, M); continue; }
         const int pb = __builtin_popcount(op.mreg) + __builtin_popcount(op.mlane) + __builtin_popcount(op.mwarp) +
                        __builtin_popcountll(op.mout);
         const double per = op.code == OPC_U2 ? 8.0 : 4.0;
@@ -584,6 +586,7 @@ static qsim_status flush(qsim_ctx c)
         std::vector<Step> steps;
         PlanOptions opt;
         opt.fusion = c->fusion;
+        opt.block_fusion = c->block_fusion;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
         c->planner->plan(c->queue, opt, steps);
@@ -1134,6 +1137,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     if (!key) return QSIM_ERR_ARG;
     std::string k(key);
     if (k == "fusion") { c->fusion = value != 0; c->pc.valid = false; }
+    else if (k == "block_fusion") { c->block_fusion = value != 0; c->pc.valid = false; }
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
@@ -1204,6 +1208,7 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     std::vector<Step> steps;
     PlanOptions opt;
     opt.fusion = (fusion & 3) != 0;
+    opt.block_fusion = !(fusion & 0x100);
     opt.global_policy = (fusion >> 4) & 3 ? ((fusion >> 4) & 3) - 1 : GP_AUTO;
     P.plan(recs, opt, steps);
     std::string jit_info;

@@ -9,8 +9,20 @@ import json
 import numpy as np
 
 
+def _apply_u4(psi, idx, t, t2, m):
+    """Fused 4x4 block: index j = bit_t + 2 bit_t2, m = 4 rows of 4 complex."""
+    U = np.asarray(m, dtype=np.float64).reshape(4, 4, 2)
+    U = U[..., 0] + 1j * U[..., 1]
+    b0 = idx[(idx & ((1 << t) | (1 << t2))) == 0]
+    ii = [b0, b0 | (1 << t), b0 | (1 << t2), b0 | (1 << t) | (1 << t2)]
+    x = np.stack([psi[i] for i in ii])
+    y = U @ x
+    for r in range(4):
+        psi[ii[r]] = y[r]
+
+
 def _apply(psi, idx, code, t, cm, cv, m):
-    if code == 6:  # phase-run flush marker
+    if code in (6, 8):  # phase-run flush marker / U4 data rows
         return
     sel = (idx & cm) == cv
     if code in (3, 5):  # PHASE / PHASE_ACC
@@ -46,7 +58,10 @@ def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
         ty = st["type"]
         if ty == "pass":
             for op in st["ops"]:
-                if op["code"] in (4, 6):
+                if op["code"] in (4, 6, 8):
+                    continue
+                if op["code"] == 7:
+                    _apply_u4(psi, idx, op["t"], op["t2"], op["m"])
                     continue
                 _apply(psi, idx, op["code"], op["t"], op["cm"], op["cv"], op["m"])
         elif ty == "generic":

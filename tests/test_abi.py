@@ -67,8 +67,8 @@ def test_validation_codes(pkg):
         assert e.value.status == code
 
 
-def _check_plan(pkg, oracle_mod, n, P, init, gates, fusion=True, policy=None):
-    js = _plan(pkg, n, P, gates, fusion, policy)
+def _check_plan(pkg, oracle_mod, n, P, init, gates, fusion=True, policy=None, block_fusion=True):
+    js = pkg.plan_json(n, P, gates, fusion, policy, block_fusion)
     got = run_plan(js, n, init, gates)
     o = oracle_mod.Oracle(n)
     o.init_basis(init)
@@ -88,6 +88,55 @@ def test_plan_random_brickwork(pkg, oracle_mod, P):
     assert npass < len(gates) / 4  # fusion actually fuses
     if P > 1:
         assert any(s["type"] == "exchange" for s in steps)
+
+
+def _pass_ops(d):
+    return [op for s in d["plan"]["steps"] if s["type"] == "pass" for op in s["ops"]]
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_block_fusion_brickwork(pkg, oracle_mod, P):
+    """Two-qubit block fusion (plan.cpp fuse_blocks): the brickwork's
+    U2 (x) U2, CNOT, U2 (x) U2 clusters become 4x4 unitaries; executing the
+    fused plan gives the oracle's state, and the fused pass program costs
+    about half the FP64 work of the unfused one."""
+    n = 14
+    gates = C.random_brickwork(n, 8, seed=13)
+    d = _check_plan(pkg, oracle_mod, n, P, 5, gates)
+    d0 = _check_plan(pkg, oracle_mod, n, P, 5, gates, block_fusion=False)
+    ops, ops0 = _pass_ops(d), _pass_ops(d0)
+    assert not any(op["code"] == 7 for op in ops0)
+    n_u4 = sum(op["code"] == 7 for op in ops)
+    assert n_u4 >= len(gates) // 8
+
+    def cost(ops):
+        c = 0.0
+        for op in ops:
+            k = op["code"]
+            bits = bin(op["cm"]).count("1")
+            c += {0: 8.0, 1: 4.0, 3: 4.0, 7: 16.0 * 2 ** bits}.get(k, 0.0) / 2 ** bits
+        return c
+    assert cost(ops) < 0.6 * cost(ops0)
+
+
+def test_block_fusion_mixed_predicates(pkg, oracle_mod):
+    """Blocks next to controlled gates with out-of-cluster controls, phases on
+    the pair, one-qubit runs, Toffolis and relabels: still the oracle's state."""
+    n = 13
+    rng = G.SplitMix64(77)
+    gates = []
+    for layer in range(4):
+        for q in range(n):
+            gates.append(G.one_q(q, G.haar_u2(rng)))
+        for q in range(layer % 2, n - 1, 2):
+            gates.append(G.cnot(q, q + 1))
+        gates += [G.cphase(1, 2, 0.3 + layer), G.ctrl([5], 3, G.haar_u2(rng)), G.one_q(4, G.H),
+                  G.one_q(4, G.haar_u2(rng)), G.toffoli(0, 6, 7), G.ctrl([8], 9, G.haar_u2(rng)),
+                  G.one_q(8, G.haar_u2(rng)), G.one_q(9, G.haar_u2(rng)), G.swap(10, 11),
+                  G.ctrl([2], 1, G.PAULI_X), G.one_q(2, G.R(0.7))]
+    for P in (1, 2):
+        d = _check_plan(pkg, oracle_mod, n, P, 11, gates)
+        assert any(op["code"] == 7 for op in _pass_ops(d))
 
 
 def test_plan_qft_sharded(pkg, oracle_mod):

@@ -63,7 +63,7 @@ def _worker(rank, world, port, case, out_q, policy=None):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_quant_ph_0608239_b200 as P
-        from workloads import circuits as C
+        from tests.plan_exec import _apply_u4
         n, init, gates, qs = case()
         plan = json.loads(P.plan_json(n, world, gates, policy=policy))
         G = (world - 1).bit_length()
@@ -79,7 +79,9 @@ def _worker(rank, world, port, case, out_q, policy=None):
             ty = st["type"]
             if ty == "pass":
                 for op in st["ops"]:
-                    if op["code"] not in (4, 6):
+                    if op["code"] == 7:  # fused 4x4 block on two local bits
+                        _apply_u4(shard, np.arange(1 << M, dtype=np.int64), op["t"], op["t2"], op["m"])
+                    elif op["code"] not in (4, 6, 8):
                         _apply(shard, full, op["code"], op["t"], op["cm"], op["cv"], op["m"])
             elif ty == "generic":
                 _apply(shard, full, st["code"], st["t"], st["cm"], st["cv"], st["m"])
@@ -195,7 +197,12 @@ def test_sharded_path_gloo(oracle_mod, world, case, policy):
     procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, policy)) for r in range(world)]
     for p in procs:
         p.start()
-    logical, prob, n_ex = q.get(timeout=300)
+    try:
+        logical, prob, n_ex = q.get(timeout=120)
+    except Exception:
+        for p in procs:
+            p.kill()
+        raise
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

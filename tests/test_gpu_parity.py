@@ -114,6 +114,37 @@ def test_jit_tier_matches_interpreter(P, oracle_mod, n, ranks):
     assert_parity(s_int, o, n)
 
 
+def mixed_blocks(n, seed):
+    """Brickwork layers interleaved with gates that touch a block's pair from
+    outside (controls, phases, Toffolis, swaps, one-qubit runs)."""
+    rng = G.SplitMix64(seed)
+    gates = []
+    for layer in range(5):
+        gates += [G.one_q(q, G.haar_u2(rng)) for q in range(n)]
+        gates += [G.cnot(q, q + 1) for q in range(layer % 2, n - 1, 2)]
+        gates += [G.cphase(1, 2, 0.3 + layer), G.ctrl([5], 3, G.haar_u2(rng)), G.one_q(4, G.H),
+                  G.one_q(4, G.haar_u2(rng)), G.toffoli(0, 6, 7), G.ctrl([8], 9, G.haar_u2(rng)),
+                  G.one_q(8, G.haar_u2(rng)), G.one_q(9, G.haar_u2(rng)), G.swap(10, n - 1),
+                  G.ctrl([2], 1, G.PAULI_X), G.one_q(2, G.R(0.7)), G.ctrl([n - 1], 0, G.haar_u2(rng))]
+    return gates
+
+
+@pytest.mark.parametrize("n,ranks", [(13, 1), (16, 1), (16, 4)])
+@pytest.mark.parametrize("jit", [0, 1])
+def test_block_fusion_parity(P, oracle_mod, n, ranks, jit):
+    """Fused two-qubit blocks (OPC_U4, plan.cpp fuse_ops) vs the oracle, with
+    block fusion on and off, on both pass tiers."""
+    gates = C.random_brickwork(n, 6, seed=n) + mixed_blocks(n, seed=n)
+    o = oracle_run(oracle_mod, n, 9, gates)
+    for bf in (1, 0):
+        sim = P.QSim(n, n_ranks=ranks, transport="local" if ranks == 1 else "virtual")
+        sim.set_option("jit", jit)
+        sim.set_option("block_fusion", bf)
+        sim.init_basis(9)
+        sim.run_circuit(gates)
+        assert_parity(sim, o, n)
+
+
 @pytest.mark.parametrize("ranks,n", [(2, 14), (4, 15), (8, 16), (8, 12), (4, 9)])
 def test_every_gate_sharded_virtual(P, oracle_mod, ranks, n):
     gates = kitchen_sink(n, seed=100 + n)
