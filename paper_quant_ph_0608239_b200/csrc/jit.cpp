@@ -58,13 +58,38 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
 
 }  // namespace
 
+// pipelined CTAs per SM: 3 staged tiles of 64 KB (12-bit tiles) fit once,
+// of 32 KB (11-bit tiles) twice, in the 227 KB of shared memory
+constexpr int kPipeCtasPerSm = kTileBits >= 12 ? 1 : 2;
+
+bool jit_pipelined()
+{
+    static const bool p = env_int("QSIM_JIT_PIPE", 0) != 0;
+    return p;
+}
+
+void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, unsigned &smem)
+{
+    if (jit_pipelined()) {
+        static const int cap = env_int("QSIM_PASS_GRID", 0);  // testing: fewer CTAs, more tiles each
+        grid = (unsigned)std::min<uint64_t>(st.pass.n_inst, (uint64_t)std::max(1, cap > 0 ? cap : kPipeCtasPerSm * n_sm));
+        block = 2 * kPassThreads;
+        smem = 3 * kTileAmps * 16;
+    } else {
+        grid = (unsigned)st.pass.n_inst;
+        block = kPassThreads;
+        smem = st.pass.use_smem ? kTileAmps * 16 : 0;
+    }
+}
+
 JitPass jit_generate(const Step &st)
 {
     std::vector<int> out_idx, m_idx;
     Layout L = layout_of(st, out_idx, m_idx);
     std::ostringstream s;
     const int minb = env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2);  // CTAs per SM (register cap)
-    s << "// minb=" << minb << "\n";
+    const bool pipe = jit_pipelined();
+    s << "// minb=" << minb << " pipe=" << pipe << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
          "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long out["
@@ -82,12 +107,84 @@ JitPass jit_generate(const Step &st)
          " const double s = x * fma(x2, fma(x2, fma(x2, fma(x2, 2.7557319223985893e-06, -1.9841269841269841e-04), "
          "8.3333333333333332e-03), -1.6666666666666666e-01), 1.0);\n"
          " return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));\n}\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads << ", " << minb
-      << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
-    s << " extern __shared__ double2 sm[];\n";
-    s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    s << " { const unsigned long long inst = blockIdx.x;\n";
-    s << " const unsigned long long base = qdep(inst, P.ts);\n";
+    const int NT = kPassThreads, ROWS = kTileAmps / 8;
+    std::string BAR = "__syncthreads();";
+    if (!pipe) {
+        s << "#define TPM P.tpm\n#define TSP P.ts\n";
+        s << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb
+          << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
+        s << " extern __shared__ double2 sm[];\n";
+        s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+        s << " { const unsigned long long inst = blockIdx.x;\n";
+    } else {
+        // Persistent, one CTA per SM, two thread groups of NT threads working on
+        // alternate tiles of this CTA (k = g, g+2, ...).  Tiles are staged in a
+        // ring of 3 shared-memory buffers by cp.async (16 B per thread and
+        // instruction, coalesced 512-B warp requests, written straight into
+        // the swizzled layout), completion tracked by one mbarrier per buffer
+        // (every thread of the issuing group arrives when its copies land).
+        // The group starting tile k issues tile k+1's copies, into the buffer
+        // its own tile k-2 used; the buffer of tile k then serves its
+        // re-layouts (named barrier per group).  So the HBM reads of one tile
+        // overlap the FP64 work and the stores of the others.
+        BAR = "asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + g), \"r\"(" + std::to_string(NT) + ") : \"memory\");";
+        const int JB = kTileBits - 4;  // tile bits of the copy index j (thread covers bits 0..JB-1)
+        s << "__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }\n";
+        s << "__device__ __forceinline__ void issue_tile(const JP &P, unsigned long long inst, unsigned sbuf, unsigned mb, "
+             "int tidv, const volatile unsigned long long *tpmv, const int *tsv)\n{\n"
+             " int tid; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(tid) : \"r\"(tidv));\n"
+             " unsigned long long toff = (unsigned long long)(tid & 7);\n"
+             "#pragma unroll\n for (int b = 3; b < " << JB << "; b++) if ((tid >> b) & 1) toff |= tpmv[b];\n"
+             " const unsigned tsw = (unsigned)(tid ^ (((tid >> 3) ^ (tid >> 6) ^ (tid >> 9)) & 7));\n"
+             " const double2 *src = P.st + (qdep(inst, tsv) | toff);\n"
+             " const unsigned long long h0 = tpmv[" << JB << "], h1 = tpmv[" << JB + 1 << "], h2 = tpmv[" << JB + 2
+          << "], h3 = tpmv[" << JB + 3 << "];\n"
+             "#pragma unroll\n for (int j = 0; j < 16; j++) {\n"
+             "  unsigned long long o = 0;\n"
+             "  if (j & 1) o |= h0;\n  if (j & 2) o |= h1;\n  if (j & 4) o |= h2;\n  if (j & 8) o |= h3;\n"
+             "  const int sj = j << " << JB << ";\n"
+             "  const unsigned zj = (unsigned)(sj ^ (((sj >> 3) ^ (sj >> 6) ^ (sj >> 9)) & 7));\n"
+             "  asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sbuf + ((zj ^ tsw) << 4)), "
+             "\"l\"(src + o) : \"memory\");\n"
+             " }\n"
+             " asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(mb) : \"memory\");\n}\n";
+        s << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", " << kPipeCtasPerSm
+          << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
+        s << " extern __shared__ __align__(128) double2 smraw[];\n";
+        // mbarrier of tile k: k % 6 (not k % 3): a group can run one tile ahead
+        // of the other and wait for tile k+1 before it is issued; with 6
+        // barriers that barrier's previous phase (tile k-5) is known complete,
+        // so its parity cannot alias.
+        s << " __shared__ __align__(8) unsigned long long mbar[6];\n";
+        // tile bit positions in shared memory: the loop re-reads them after each
+        // barrier instead of holding (and spilling) copies in registers
+        s << " __shared__ volatile unsigned long long TPM[" << kTileBits << "];\n __shared__ int TSP[" << kTileBits << "];\n";
+        s << " if (threadIdx.x < " << kTileBits << ") { TPM[threadIdx.x] = P.tpm[threadIdx.x]; TSP[threadIdx.x] = P.ts[threadIdx.x]; }\n";
+        s << " const int g = threadIdx.x / " << NT << ", tid = threadIdx.x % " << NT << ";\n";
+        s << " if (threadIdx.x == 0) {\n"
+             "  for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
+          << ";\" :: \"r\"(su32(&mbar[i])) : \"memory\");\n"
+             "  asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n }\n";
+        s << " __syncthreads();\n";
+        s << " const unsigned long long G = gridDim.x;\n";
+        s << " const unsigned long long ntile = P.n_inst > blockIdx.x ? (P.n_inst - blockIdx.x + G - 1) / G : 0;\n";
+        s << " if (g == 0 && ntile > 0) issue_tile(P, blockIdx.x, su32(smraw), su32(&mbar[0]), tid, TPM, TSP);\n";
+        s << " for (unsigned long long k = g; k < ntile; k += 2) {\n";
+        s << " const int bk = (int)(k % 3);\n";
+        s << " double2 *sm = smraw + bk * " << kTileAmps << ";\n";
+        s << " " << BAR << "\n";
+        s << " if (k + 1 < ntile) { const int bn = (int)((k + 1) % 3); issue_tile(P, blockIdx.x + (k + 1) * G, su32(smraw + bn * "
+          << kTileAmps << "), su32(&mbar[(k + 1) % 6]), tid, TPM, TSP); }\n";
+        s << " { const unsigned mb = su32(&mbar[k % 6]), par = (unsigned)((k / 6) & 1); unsigned done = 0;\n"
+             "   while (!done) asm volatile(\"{\\n .reg .pred p;\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\\n selp.u32 %0, 1, 0, p;\\n}\" "
+             ": \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
+        s << " const unsigned long long inst = blockIdx.x + k * G;\n";
+        // re-derive the thread coordinates every tile (opaque to the compiler):
+        // hoisting the per-config address terms out of the loop spills them
+        s << " int tidk; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(tidk) : \"r\"(tid));\n";
+        s << " const int lane = tidk & 31, warp = tidk >> 5;\n";
+    }
+    s << " const unsigned long long base = qdep(inst, TSP);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
     int reg[16];
@@ -96,25 +193,17 @@ JitPass jit_generate(const Step &st)
     auto gaddr = [&](uint64_t c) {
         std::ostringstream g;
         g << "(unsigned long long)((lane & 3) << 1)";
-        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? P.tpm[" << nib(c, 4 + j) << "] : 0ULL)";
-        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? P.tpm[" << nib(c, 9 + j) << "] : 0ULL)";
+        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? TPM[" << nib(c, 4 + j) << "] : 0ULL)";
+        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? TPM[" << nib(c, 9 + j) << "] : 0ULL)";
         return g.str();
     };
     auto roff = [&](uint64_t c, int j) {
         std::ostringstream g;
         g << "0ULL";
         for (int b = 0; b < 3; b++)
-            if ((j >> b) & 1) g << " | P.tpm[" << nib(c, 1 + b) << "]";
+            if ((j >> b) & 1) g << " | TPM[" << nib(c, 1 + b) << "]";
         return g.str();
     };
-    uint64_t cur = st.pass.cfg0;
-    s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
-    for (int j = 0; j < 8; j++)
-        s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
-             "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
-          << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
-          << " = make_double2(x2, x3); }\n";
-    s << " }\n";
     auto smem_z = [&](uint64_t c, const char *tag) {
         s << "  const int zt" << tag << " = ";
         for (int j = 0; j < 5; j++) s << "(((lane >> " << j << ") & 1) << " << nib(c, 4 + j) << ") | ";
@@ -129,19 +218,38 @@ JitPass jit_generate(const Step &st)
             if ((i >> b) & 1) z ^= swz_host(1 << nib(c, b));
         return z;
     };
+    uint64_t cur = st.pass.cfg0;
+    if (!pipe) {
+        s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
+        for (int j = 0; j < 8; j++)
+            s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
+                 "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
+              << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
+              << " = make_double2(x2, x3); }\n";
+        s << " }\n";
+    } else {
+        // the staged tile is in the swizzled layout: read it straight into the
+        // config of the first op (a leading re-layout is folded into the read)
+        if (!st.ops.empty() && st.ops[0].code == OPC_TRANS) cur = st.ops[0].cfg;
+        s << " {\n";
+        smem_z(cur, "s");
+        for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzs ^ " << zreg(cur, i) << "];\n";
+        s << "  " << BAR << "\n }\n";
+    }
     bool in_run = false;
     size_t run_begin = 0;
-    for (size_t o = 0; o < st.ops.size(); o++) {
+    const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
+    for (size_t o = o_first; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
             s << " {\n";
             smem_z(cur, "a");
             for (int i = 0; i < 16; i++) s << "  sm[zza ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
-            s << "  __syncthreads();\n";
+            s << "  " << BAR << "\n";
             cur = op.cfg;
             smem_z(cur, "b");
             for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzb ^ " << zreg(cur, i) << "];\n";
-            s << "  __syncthreads();\n }\n";
+            s << "  " << BAR << "\n }\n";
             continue;
         }
         if (op.code == OPC_PHASE_FLUSH) {
@@ -305,7 +413,10 @@ JitPass jit_generate(const Step &st)
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
     s << " }\n";
-    s << " }\n}\n";
+    s << " }\n";
+    // a thread must not exit with its copies (for the other group's tile) in flight
+    if (pipe) s << " asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
+    s << "}\n";
     JitPass jp;
     jp.src = s.str();
     jp.param_bytes = L.bytes;
@@ -452,7 +563,7 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2));
+    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2) | ((uint64_t)jit_pipelined() << 16));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
@@ -510,7 +621,7 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
             err = "cuModuleLoadData/cuModuleGetFunction failed";
             return false;
         }
-        D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, kTileAmps * 16);
+        D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, jit_pipelined() ? 3 * kTileAmps * 16 : kTileAmps * 16);
         std::lock_guard<std::mutex> g(mu_);
         mods_.push_back(mod);
         fns_[keys[i]] = fn;

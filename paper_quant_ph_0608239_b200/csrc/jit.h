@@ -46,6 +46,12 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
 // (host-only check; n = distinct structures)
 bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms);
 
+// Kernel variant: pipelined = persistent CTA per SM, two thread groups on
+// alternate tiles, tiles staged in shared memory by cp.async.bulk (default;
+// QSIM_JIT_PIPE=0 selects one non-persistent CTA per tile, loads to registers).
+bool jit_pipelined();
+void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, unsigned &smem);
+
 // structural key of a pass (what the generated source depends on)
 std::string jit_key(const Step &st);
 

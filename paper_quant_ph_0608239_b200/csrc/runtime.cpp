@@ -57,6 +57,7 @@ struct qsim_ctx_s {
     bool own_scratch = false;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    int n_sm = 148;  // SMs of the current device (persistent pass grid)
     ncclComm_t comm = nullptr;
     Planner *planner = nullptr;
     bool initialized = false, init_pending = false;
@@ -635,10 +636,10 @@ static qsim_status flush(qsim_ctx c)
                     size_t sz = pp[i].size();
                     void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                                      CU_LAUNCH_PARAM_END};
-                    const unsigned smem = s.pass.use_smem ? kTileAmps * 16 : 0;
-                    const uint64_t grid = s.pass.n_inst;
-                    CUresult cr = drv().launchKernel(fn, (unsigned)grid, 1, 1, kPassThreads, 1, 1, smem,
-                                                 (CUstream)c->stream, nullptr, extra);
+                    unsigned grid, block, smem;
+                    jit_launch_dims(s, c->n_sm, grid, block, smem);
+                    CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)c->stream, nullptr,
+                                                     extra);
                     if (cr != CUDA_SUCCESS) {
                         c->poisoned = true;
                         FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
@@ -789,6 +790,12 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof(id));
         if (ncclCommInitRank(&c->comm, P, id, cfg->rank) != ncclSuccess) return bail(QSIM_ERR_COMM);
+    }
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaGetLastError();
     }
     if (cudaMalloc((void **)&c->d_shard_ptrs, sizeof(double2 *) * nsh) != cudaSuccess) return bail(QSIM_ERR_OOM);
     if (cudaMemcpy(c->d_shard_ptrs, c->shards.data(), sizeof(double2 *) * nsh, cudaMemcpyHostToDevice) != cudaSuccess)

@@ -28,7 +28,7 @@ hh = rows[1]
 iS, iE, iSrc = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Instructions Executed"), hh.index("Source")
 samp, ex = collections.Counter(), collections.Counter()
 for row in rows[2:]:
-    if len(row) <= iE:
+    if len(row) <= iE or row[0] in ("Kernel Name", "Address"):
         continue
     t = row[iSrc].strip().split()
     if not t:
