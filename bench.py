@@ -90,6 +90,28 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def pass_roofline(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float):
+    """Per-launch roofline of the planned passes (host planner, same plan as
+    the engine): each pass needs max(FP64 FMA-slot work / FP64 peak, 32 B/amp /
+    HBM peak).  Returns (sum over passes of that bound in ms, FMA-slots per amp)."""
+    from paper_quant_ph_0608239_b200 import plan_json
+    G = (world - 1).bit_length()
+    amps = float(1 << (n - G))
+    d = json.loads(plan_json(n, world, gates))
+    cost = {0: 8.0, 1: 4.0, 3: 4.0, 5: 4.0, 7: 16.0}
+    t = slots = 0.0
+    for st in d["plan"]["steps"]:
+        if st["type"] != "pass":
+            continue
+        f = 0.0
+        for op in st["ops"]:
+            bits = sum(bin(op[k]).count("1") for k in ("mreg", "mlane", "mwarp", "mout"))
+            f += cost.get(op["code"], 0.0) / (1 << bits)
+        slots += f
+        t += max(2.0 * f * amps / (fp64_tflops * 1e12), 32.0 * amps / (hbm_gbs * 1e9))
+    return 1e3 * t, slots
+
+
 def cpu_sample(layers: int):
     """The oracle on the first `layers` layers of the same 24-qubit circuit."""
     import oracle
@@ -216,6 +238,7 @@ def run_ours(args):
     fp64_peak = 2.0 * FP64_FMA_PER_CLK_PER_SM * N_SM * sm_max * 1e6 / 1e12  # TFLOP/s
     fp64_ach = (2.0 * st["pass_fp64_slots"] / (pass_ms / 1e3) / 1e12) if pass_ms > 0 else None
     hbm_ach = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
+    t_min_ms, _ = pass_roofline(n, world, gates, fp64_peak, hbm_peak)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tp):
@@ -237,6 +260,9 @@ def run_ours(args):
                          "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x %.0f MHz" % sm_max,
                          "launches": int(st["passes"]), "kernel_ms": pass_ms,
                          "kernel_share_of_step": pass_ms / ms if ms > 0 else None,
+                         # per-launch bound max(FP64, HBM) summed over the passes of a step
+                         "per_pass_bound": {"t_min_ms_per_step": t_min_ms,
+                                            "frac": (t_min_ms * args.steps / pass_ms) if pass_ms > 0 else None},
                          "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": (hbm_ach / hbm_peak) if hbm_ach else None, "peak_source": peak_src,
                                  "bytes_per_launch": 32 << (n - G)}},

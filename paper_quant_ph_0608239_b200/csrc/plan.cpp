@@ -887,18 +887,78 @@ void Planner::remap(const std::vector<int> &local_q, const std::vector<int> &glo
     out.push_back(std::move(s));
 }
 
+// Modelled device time of a planned step list (seconds): a pass costs
+// max(FP64 FMA-slot work / FP64 peak, 32 B/amp / HBM peak), a K-pair exchange
+// its (2^K-1)/2^K shard share over NVLink plus the HBM pack/unpack, other
+// steps one HBM round trip.  Peaks: derived FP64, measured
+// HBM copy and NVLink peer-copy bandwidths (B200_PROFILING.md).
+double plan_cost(const std::vector<Step> &steps, int M)
+{
+    const double amps = std::ldexp(1.0, M), fp64 = 37.2e12, hbm = 6.5e12, nvl = 0.77e12;
+    double t = 0;
+    for (const Step &s : steps) {
+        switch (s.type) {
+        case ST_PASS: {
+            double f = 0;
+            for (const KOp &op : s.ops) {
+                const int pb = __builtin_popcount(op.mreg) + __builtin_popcount(op.mlane) +
+                               __builtin_popcount(op.mwarp) + __builtin_popcountll(op.mout);
+                const double c = op.code == OPC_U2 ? 8 : op.code == OPC_U4 ? 16
+                               : (op.code == OPC_U2R || op.code == OPC_PHASE || op.code == OPC_PHASE_ACC) ? 4 : 0;
+                f += c * std::ldexp(1.0, -pb);
+            }
+            t += std::max(2 * f * amps / fp64, 32 * amps / hbm);
+            break;
+        }
+        case ST_EXCHANGE: {
+            const double share = 1.0 - std::ldexp(1.0, -(int)s.lpos.size());
+            t += share * 16 * amps / nvl + 2 * share * 16 * amps / hbm;
+            break;
+        }
+        case ST_PAIRWISE: t += 16 * amps / nvl + 48 * amps / hbm; break;
+        case ST_RELABEL: break;
+        default: t += 32 * amps / hbm; break;
+        }
+    }
+    return t;
+}
+
 void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &opt, std::vector<Step> &out)
 {
     const bool fused = opt.fusion && M >= kTileBits;
-    // two-qubit blocks on the whole gate list first (never cut by a pass)
-    std::vector<GateRec> blocked;
+    if (!fused || !opt.block_fusion) {
+        plan_list(user_gates, opt, out);
+        return;
+    }
+    // two-qubit blocks on the whole gate list first (never cut by a pass).
     // No blocks on the initially global qubits: a control or a diagonal gate
     // there is free (no exchange), and an isolated gate there may go pairwise;
     // inside a 4x4 block it would be a non-diagonal target.
     uint64_t no_blocks_on = 0;
     for (int p = M; p < n; p++) no_blocks_on |= bit(qubit_at[p]);
-    if (fused && opt.block_fusion) blocked = fuse_gates(user_gates, no_blocks_on);
-    const std::vector<GateRec> &gates = fused && opt.block_fusion ? blocked : user_gates;
+    const std::vector<GateRec> blocked = fuse_gates(user_gates, no_blocks_on);
+    if (G == 0) {
+        plan_list(blocked, opt, out);
+        return;
+    }
+    // Sharded: tying gates into blocks can change which of them meet a
+    // nonlocal qubit (more exchanges); plan both ways (the second keeps the
+    // pass-local fusion of build_pass) and keep the cheaper by the cost model.
+    const Planner start = *this;
+    std::vector<Step> a, b;
+    plan_list(blocked, opt, a);
+    const Planner after_a = *this;
+    *this = start;
+    plan_list(user_gates, opt, b);
+    const bool take_a = plan_cost(a, M) <= plan_cost(b, M);
+    if (take_a) *this = after_a;
+    std::vector<Step> &pick = take_a ? a : b;
+    for (Step &s : pick) out.push_back(std::move(s));
+}
+
+void Planner::plan_list(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out)
+{
+    const bool fused = opt.fusion && M >= kTileBits;
     std::vector<char> done(gates.size(), 0);
     size_t first = 0;
     while (true) {

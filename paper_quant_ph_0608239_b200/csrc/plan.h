@@ -104,7 +104,11 @@ private:
     void emit_generic(const GateRec &g, std::vector<Step> &out);
     void emit_perm(const GateRec &g, std::vector<Step> &out);
     void swap_layout(int pa, int pb);
+    void plan_list(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out);
 };
+
+// modelled device seconds of a step list on 2^M-amplitude shards (planner choices)
+double plan_cost(const std::vector<Step> &steps, int M);
 
 std::string plan_to_json(const Planner &final_state, const std::vector<Step> &steps);
 
