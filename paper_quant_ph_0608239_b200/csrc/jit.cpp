@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <sstream>
 #include <thread>
 
@@ -236,6 +237,45 @@ JitPass jit_generate(const Step &st)
         for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzs ^ " << zreg(cur, i) << "];\n";
         s << "  " << BAR << "\n }\n";
     }
+    // Deferred predicated swaps.  An exact-X op whose predicate depends on the
+    // lane, warp or out-of-tile bits (a CNOT/Toffoli target in a register,
+    // control elsewhere) cannot be a register renaming.  Instead of 32 selects
+    // it is recorded as a pending "flip" of register bit k under a per-thread
+    // predicate; pending flips commute with each other and with every op that
+    // does not touch bit k, and the next data movement absorbs them: the
+    // shared-memory stores of a re-layout or the global stores of the pass
+    // write register i to the slot of i ^ (1 << k) (an address XOR).  An op on
+    // bit k first materialises the swap (selects).
+    struct Flip { int k; std::string pred; };
+    std::vector<Flip> flips;
+    auto emit_swap = [&](int k, const std::string &pred) {
+        s << " { const bool tp = " << pred << ";\n";
+        for (int p = 0; p < 8; p++) {
+            const int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1)), i1 = i0 | (1 << k);
+            const std::string x = A(i0), y = A(i1);
+            s << "  { const double2 t = " << x << "; " << x << ".x = tp ? " << y << ".x : " << x << ".x; " << x
+              << ".y = tp ? " << y << ".y : " << x << ".y; " << y << ".x = tp ? t.x : " << y << ".x; " << y
+              << ".y = tp ? t.y : " << y << ".y; }\n";
+        }
+        s << " }\n";
+    };
+    auto materialize = [&](uint32_t regbits) {
+        for (size_t f = 0; f < flips.size();) {
+            if ((regbits >> flips[f].k) & 1) {
+                emit_swap(flips[f].k, flips[f].pred);
+                flips.erase(flips.begin() + f);
+            } else {
+                f++;
+            }
+        }
+    };
+    // per-thread XOR of the slot index of every register under the pending flips
+    auto flip_mask = [&](const char *name, const char *type, std::function<std::string(int)> unit) {
+        s << "  const " << type << " " << name << " = 0";
+        for (const Flip &f : flips) s << " ^ ((" << f.pred << ") ? (" << type << ")(" << unit(f.k) << ") : (" << type << ")0)";
+        s << ";\n";
+        flips.clear();
+    };
     bool in_run = false;
     size_t run_begin = 0;
     const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
@@ -244,7 +284,9 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_TRANS) {
             s << " {\n";
             smem_z(cur, "a");
-            for (int i = 0; i < 16; i++) s << "  sm[zza ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
+            const uint64_t cfa = cur;
+            flip_mask("zfa", "int", [&](int k) { return std::to_string(swz_host(1 << nib(cfa, k))); });
+            for (int i = 0; i < 16; i++) s << "  sm[(zza ^ zfa) ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
             s << "  " << BAR << "\n";
             cur = op.cfg;
             smem_z(cur, "b");
@@ -253,6 +295,7 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         if (op.code == OPC_PHASE_FLUSH) {
+            materialize(15);
             const PhaseRunPlan pr = plan_phase_run(st.ops.data() + run_begin, o - run_begin);
             auto sum_below = [&](uint32_t i) {  // theta_i = sum of acc[S], S subset of i
                 std::string e;
@@ -292,6 +335,7 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_U4) {
             // same FMA chains, in the same order, as kernels.cu u4_apply
             const int k = op.k, k2 = (int)op.cfg;
+            materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
             for (int p = 0; p < 4; p++) {
                 int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
@@ -334,6 +378,11 @@ JitPass jit_generate(const Step &st)
         if (op.mwarp) pr << " && ((warp & " << op.mwarp << ") == " << op.vwarp << ")";
         if (pout) pr << " && ((gcta & P.out[" << out_idx[o] << "][0]) == P.out[" << out_idx[o] << "][1])";
         const bool sel = plw || (pout && op.code == OPC_XS);  // select-based (no branch)
+        if (op.code == OPC_XS && sel && op.mreg == 0) {  // defer (see Flip)
+            flips.push_back({op.k, pr.str()});
+            continue;
+        }
+        materialize(op.mreg | (op.code == OPC_PHASE || op.code == OPC_PHASE_ACC ? 0u : 1u << op.k));
         s << " { // op " << o << " code " << op.code << "\n";
         if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
         if (pout && !sel) s << "  if (tp) {\n";
@@ -407,9 +456,14 @@ JitPass jit_generate(const Step &st)
         if (pout && !sel) s << "  }\n";
         s << " }\n";
     }
+    materialize(1);  // register bit 0 lies inside one 256-bit store
     s << " {\n  double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
+    {
+        const uint64_t cfs = cur;
+        flip_mask("gf", "unsigned long long", [&](int k) { return "TPM[" + std::to_string(nib(cfs, k)) + "]"; });
+    }
     for (int j = 0; j < 8; j++)
-        s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + (" << roff(cur, j) << ")), \"d\"("
+        s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + ((" << roff(cur, j) << ") ^ gf)), \"d\"("
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
     s << " }\n";

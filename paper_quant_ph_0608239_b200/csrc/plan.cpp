@@ -542,8 +542,29 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             if (pops[b].code == OPC_PHASE || in_regs(cfg, pops[b])) { pick = b; break; }
         }
         if (pick == n) {
-            upcoming(false, reg);
-            cfg = make_cfg(reg, false);
+            // If one store-capable config (tile bit 0 in a register, bits 1, 2
+            // on lanes) can host every remaining op, use it: the pass then ends
+            // without the re-layout back to a store config.
+            std::vector<int> need;
+            bool store_fits = true;
+            for (size_t b = 0; b < n && store_fits; b++) {
+                if (done[b] || pops[b].code == OPC_PHASE) continue;
+                for (int t : {tl(pops[b]), pops[b].t2 >= 0 ? tl_of[pops[b].t2] : -1}) {
+                    if (t < 0) continue;
+                    if (t == 1 || t == 2) store_fits = false;
+                    if (t != 0 && std::find(need.begin(), need.end(), t) == need.end()) need.push_back(t);
+                }
+            }
+            if (store_fits && need.size() <= 3) {
+                std::vector<int> r{0};
+                for (int t : need) r.push_back(t);
+                for (int t = 3; r.size() < 4 && t < kTileBits; t++)
+                    if (std::find(r.begin(), r.end(), t) == r.end()) r.push_back(t);
+                cfg = make_cfg(r, true);
+            } else {
+                upcoming(false, reg);
+                cfg = make_cfg(reg, false);
+            }
             emit_trans(cfg);
             continue;
         }
