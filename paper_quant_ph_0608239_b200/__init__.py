@@ -8,3 +8,4 @@ from .qsim import (QSim, QsimError, exchange_peers, get_unique_id, pack_gates, p
                    G_1Q, G_CTRL, G_PERM, G_SWAP)
 from ._native import LIB_PATH, EXPORTS  # noqa: F401
 from .program import Program, ProgramError, parse_program, run_program, serialize_program  # noqa: F401
+from . import shor  # noqa: F401
