@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = nccl_dir()
     tile = os.environ.get("QSB_TILE_BITS")
-    defs = ["-DQSB_TILE_BITS=" + tile] if tile else []
+    regs = os.environ.get("QSB_REG_BITS")
+    defs = (["-DQSB_TILE_BITS=" + tile] if tile else []) + (["-DQSB_REG_BITS=" + regs] if regs else [])
     inc = [*defs, "-I", CSRC, "-I", INCLUDE, "-I", os.path.join(nccl, "include"), "-I", os.path.join(CUDA, "include")]
     objs = []
     cmds = []

@@ -9,14 +9,16 @@
 // one HBM read + write (32 B/amplitude) for many gates.
 //
 // A "config" assigns the 12 tile-local bits to thread coordinates:
-//   i    (4 bits, in-thread register index) <-> r[0..3]
-//   lane (5 bits)                           <-> l[0..4]
-//   warp (3 bits)                           <-> w[0..2]
+//   i    (kRegBits bits, in-thread register index) <-> r[0..kRegBits-1]
+//   lane (5 bits)                                  <-> l[0..4]
+//   warp (the rest)                                <-> w[0..kWarpBits-1]
+// (kRegBits = 4: 16 amplitudes per thread, 256 threads per 12-bit tile;
+//  kRegBits = 5: 32 amplitudes per thread, 128 threads.)
 // Gates are applied to register bits only (k = position in r); OPC_TRANS
 // moves the tile to another config through XOR-swizzled shared memory.
 // Load/store configs have r[0] = 0, l[0] = 1, l[1] = 2 (256-bit accesses of
 // amplitude pairs, whole 128-B lines per 4 lanes).
-// A config is packed in nibbles: r0 r1 r2 r3 l0 l1 l2 l3 l4 w0 .. w(kWarpBits-1).
+// A config is packed in nibbles: r0 .. r(kRegBits-1) l0 .. l4 w0 .. w(kWarpBits-1).
 #pragma once
 #include <cstdint>
 
@@ -25,14 +27,22 @@ namespace qsb {
 #ifndef QSB_TILE_BITS
 #define QSB_TILE_BITS 12
 #endif
-constexpr int kTileBits = QSB_TILE_BITS;      // tile = 3 fixed low bits + 9 free bits (+ warp bits)
+#ifndef QSB_REG_BITS
+#define QSB_REG_BITS 4
+#endif
+constexpr int kTileBits = QSB_TILE_BITS;      // tile = 3 fixed low bits + 9 free bits
 constexpr int kTileAmps = 1 << kTileBits;
-constexpr int kWarpBits = kTileBits - 9;      // 4 register bits + 5 lane bits + warp bits
+constexpr int kRegBits = QSB_REG_BITS;        // in-thread register bits
+constexpr int kAmpsPerThread = 1 << kRegBits;
+constexpr int kWarpBits = kTileBits - kRegBits - 5;  // register bits + 5 lane bits + warp bits
 constexpr int kPassThreads = 32 << kWarpBits;
+constexpr int kLaneNib = kRegBits, kWarpNib = kRegBits + 5;  // nibble offsets in a packed config
+// fused-pass CTAs per SM the register file holds (<= 128 registers per thread
+// for 16 amplitudes, <= 168 for 32)
+constexpr int kPassMinBlocks = kRegBits == 4 ? 8192 / kTileAmps : 3;
 constexpr int kPermTileBits = 12;
 constexpr int kPhaseRunMin = 4;             // k_perm tile (targets + low bits)
 constexpr int kPermTileAmps = 1 << kPermTileBits;
-constexpr int kAmpsPerThread = 16;
 // ops of one pass travel in the kernel parameter block (<= 32 KB on sm_100)
 constexpr int kMaxPassOps = 240;
 
@@ -65,7 +75,7 @@ enum Role : int32_t { ROLE_REG = 0, ROLE_LANE = 1, ROLE_WARP = 2, ROLE_OUT = 3 }
 // (rank << M) | local index, restricted to bits outside the tile.
 struct alignas(16) KOp {
     int32_t code;
-    int32_t k;  // register bit (0..3) of the target
+    int32_t k;  // register bit (0..kRegBits-1) of the target
     uint32_t mreg, vreg;
     uint32_t mlane, vlane;
     uint32_t mwarp, vwarp;

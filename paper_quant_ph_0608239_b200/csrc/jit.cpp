@@ -88,7 +88,7 @@ JitPass jit_generate(const Step &st)
     std::vector<int> out_idx, m_idx;
     Layout L = layout_of(st, out_idx, m_idx);
     std::ostringstream s;
-    const int minb = env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2);  // CTAs per SM (register cap)
+    const int minb = env_int("QSIM_JIT_MINB", kPassMinBlocks);  // CTAs per SM (register cap)
     const bool pipe = jit_pipelined();
     s << "// minb=" << minb << " pipe=" << pipe << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
@@ -129,7 +129,7 @@ JitPass jit_generate(const Step &st)
         // re-layouts (named barrier per group).  So the HBM reads of one tile
         // overlap the FP64 work and the stores of the others.
         BAR = "asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + g), \"r\"(" + std::to_string(NT) + ") : \"memory\");";
-        const int JB = kTileBits - 4;  // tile bits of the copy index j (thread covers bits 0..JB-1)
+        const int JB = kTileBits - kRegBits;  // tile bits of the copy index j (thread covers bits 0..JB-1)
         s << "__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }\n";
         s << "__device__ __forceinline__ void issue_tile(const JP &P, unsigned long long inst, unsigned sbuf, unsigned mb, "
              "int tidv, const volatile unsigned long long *tpmv, const int *tsv)\n{\n"
@@ -138,11 +138,11 @@ JitPass jit_generate(const Step &st)
              "#pragma unroll\n for (int b = 3; b < " << JB << "; b++) if ((tid >> b) & 1) toff |= tpmv[b];\n"
              " const unsigned tsw = (unsigned)(tid ^ (((tid >> 3) ^ (tid >> 6) ^ (tid >> 9)) & 7));\n"
              " const double2 *src = P.st + (qdep(inst, tsv) | toff);\n"
-             " const unsigned long long h0 = tpmv[" << JB << "], h1 = tpmv[" << JB + 1 << "], h2 = tpmv[" << JB + 2
-          << "], h3 = tpmv[" << JB + 3 << "];\n"
-             "#pragma unroll\n for (int j = 0; j < 16; j++) {\n"
+             " unsigned long long h[" << kRegBits << "];\n#pragma unroll\n for (int b = 0; b < " << kRegBits << "; b++) h[b] = tpmv[" << JB << " + b];\n"
+          
+             "#pragma unroll\n for (int j = 0; j < " << kAmpsPerThread << "; j++) {\n"
              "  unsigned long long o = 0;\n"
-             "  if (j & 1) o |= h0;\n  if (j & 2) o |= h1;\n  if (j & 4) o |= h2;\n  if (j & 8) o |= h3;\n"
+             "#pragma unroll\n  for (int b = 0; b < " << kRegBits << "; b++) if ((j >> b) & 1) o |= h[b];\n"
              "  const int sj = j << " << JB << ";\n"
              "  const unsigned zj = (unsigned)(sj ^ (((sj >> 3) ^ (sj >> 6) ^ (sj >> 9)) & 7));\n"
              "  asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sbuf + ((zj ^ tsw) << 4)), "
@@ -187,42 +187,44 @@ JitPass jit_generate(const Step &st)
     }
     s << " const unsigned long long base = qdep(inst, TSP);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
-    s << " double2 a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11, a12, a13, a14, a15;\n";
-    int reg[16];
-    for (int i = 0; i < 16; i++) reg[i] = i;
+    s << " double2 a0";
+    for (int i = 1; i < kAmpsPerThread; i++) s << ", a" << i;
+    s << ";\n";
+    int reg[kAmpsPerThread];
+    for (int i = 0; i < kAmpsPerThread; i++) reg[i] = i;
     auto A = [&](int i) { return "a" + std::to_string(reg[i]); };
     auto gaddr = [&](uint64_t c) {
         std::ostringstream g;
         g << "(unsigned long long)((lane & 3) << 1)";
-        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? TPM[" << nib(c, 4 + j) << "] : 0ULL)";
-        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? TPM[" << nib(c, 9 + j) << "] : 0ULL)";
+        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? TPM[" << nib(c, kLaneNib + j) << "] : 0ULL)";
+        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? TPM[" << nib(c, kWarpNib + j) << "] : 0ULL)";
         return g.str();
     };
     auto roff = [&](uint64_t c, int j) {
         std::ostringstream g;
         g << "0ULL";
-        for (int b = 0; b < 3; b++)
+        for (int b = 0; b < kRegBits - 1; b++)
             if ((j >> b) & 1) g << " | TPM[" << nib(c, 1 + b) << "]";
         return g.str();
     };
     auto smem_z = [&](uint64_t c, const char *tag) {
         s << "  const int zt" << tag << " = ";
-        for (int j = 0; j < 5; j++) s << "(((lane >> " << j << ") & 1) << " << nib(c, 4 + j) << ") | ";
-        for (int j = 0; j < kWarpBits; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, 9 + j) << ") | ";
+        for (int j = 0; j < 5; j++) s << "(((lane >> " << j << ") & 1) << " << nib(c, kLaneNib + j) << ") | ";
+        for (int j = 0; j < kWarpBits; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, kWarpNib + j) << ") | ";
         s << "0;\n";
         s << "  const int zz" << tag << " = zt" << tag << " ^ (((zt" << tag << " >> 3) ^ (zt" << tag << " >> 6) ^ (zt"
           << tag << " >> 9)) & 7);\n";
     };
     auto zreg = [&](uint64_t c, int i) {
         int z = 0;
-        for (int b = 0; b < 4; b++)
+        for (int b = 0; b < kRegBits; b++)
             if ((i >> b) & 1) z ^= swz_host(1 << nib(c, b));
         return z;
     };
     uint64_t cur = st.pass.cfg0;
     if (!pipe) {
         s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
-        for (int j = 0; j < 8; j++)
+        for (int j = 0; j < kAmpsPerThread / 2; j++)
             s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
                  "\"=d\"(x1), \"=d\"(x2), \"=d\"(x3) : \"l\"(p + ("
               << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
@@ -234,7 +236,7 @@ JitPass jit_generate(const Step &st)
         if (!st.ops.empty() && st.ops[0].code == OPC_TRANS) cur = st.ops[0].cfg;
         s << " {\n";
         smem_z(cur, "s");
-        for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzs ^ " << zreg(cur, i) << "];\n";
+        for (int i = 0; i < kAmpsPerThread; i++) s << "  " << A(i) << " = sm[zzs ^ " << zreg(cur, i) << "];\n";
         s << "  " << BAR << "\n }\n";
     }
     // Deferred predicated swaps.  An exact-X op whose predicate depends on the
@@ -250,7 +252,7 @@ JitPass jit_generate(const Step &st)
     std::vector<Flip> flips;
     auto emit_swap = [&](int k, const std::string &pred) {
         s << " { const bool tp = " << pred << ";\n";
-        for (int p = 0; p < 8; p++) {
+        for (int p = 0; p < kAmpsPerThread / 2; p++) {
             const int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1)), i1 = i0 | (1 << k);
             const std::string x = A(i0), y = A(i1);
             s << "  { const double2 t = " << x << "; " << x << ".x = tp ? " << y << ".x : " << x << ".x; " << x
@@ -286,20 +288,20 @@ JitPass jit_generate(const Step &st)
             smem_z(cur, "a");
             const uint64_t cfa = cur;
             flip_mask("zfa", "int", [&](int k) { return std::to_string(swz_host(1 << nib(cfa, k))); });
-            for (int i = 0; i < 16; i++) s << "  sm[(zza ^ zfa) ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
+            for (int i = 0; i < kAmpsPerThread; i++) s << "  sm[(zza ^ zfa) ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
             s << "  " << BAR << "\n";
             cur = op.cfg;
             smem_z(cur, "b");
-            for (int i = 0; i < 16; i++) s << "  " << A(i) << " = sm[zzb ^ " << zreg(cur, i) << "];\n";
+            for (int i = 0; i < kAmpsPerThread; i++) s << "  " << A(i) << " = sm[zzb ^ " << zreg(cur, i) << "];\n";
             s << "  " << BAR << "\n }\n";
             continue;
         }
         if (op.code == OPC_PHASE_FLUSH) {
-            materialize(15);
+            materialize((1u << kRegBits) - 1);
             const PhaseRunPlan pr = plan_phase_run(st.ops.data() + run_begin, o - run_begin);
             auto sum_below = [&](uint32_t i) {  // theta_i = sum of acc[S], S subset of i
                 std::string e;
-                for (uint32_t S = 0; S < 16; S++)
+                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
                     if (((pr.used >> S) & 1) && (S & i) == S) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
                 return e;
             };
@@ -310,7 +312,7 @@ JitPass jit_generate(const Step &st)
             };
             if (pr.mode == 0) {
                 std::vector<std::string> sums;
-                for (int i = 0; i < 16; i++) {
+                for (int i = 0; i < kAmpsPerThread; i++) {
                     const std::string e = sum_below((uint32_t)i);
                     if (e.empty()) continue;
                     size_t k = std::find(sums.begin(), sums.end(), e) - sums.begin();
@@ -321,10 +323,10 @@ JitPass jit_generate(const Step &st)
                     mul("ex" + std::to_string(k), A(i));
                 }
             } else {
-                for (uint32_t S = 0; S < 16; S++)
+                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
                     if ((pr.used >> S) & 1) s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n";
-                for (int i = 0; i < 16; i++)
-                    for (uint32_t S = 0; S < 16; S++)
+                for (int i = 0; i < kAmpsPerThread; i++)
+                    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
                         if (((pr.used >> S) & 1) && (S & (uint32_t)i) == S) mul("em" + std::to_string(S), A(i));
             }
             s << " }\n";
@@ -337,7 +339,7 @@ JitPass jit_generate(const Step &st)
             const int k = op.k, k2 = (int)op.cfg;
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
-            for (int p = 0; p < 4; p++) {
+            for (int p = 0; p < kAmpsPerThread / 4; p++) {
                 int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
                 i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
                 const int idx[4] = {i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)};
@@ -364,7 +366,7 @@ JitPass jit_generate(const Step &st)
             while (e < st.ops.size() && st.ops[e].code == OPC_PHASE_ACC) e++;
             const PhaseRunPlan pr = plan_phase_run(st.ops.data() + o, e - o);
             s << " {";
-            for (uint32_t S = 0; S < 16; S++)
+            for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
                 if ((pr.used >> S) & 1) s << " unsigned long long mo" << S << " = 0;";
             s << "\n";
             run_begin = o;
@@ -396,7 +398,7 @@ JitPass jit_generate(const Step &st)
                 if (!T) break;
             }
         } else if (op.code == OPC_PHASE) {
-            for (int i = 0; i < 16; i++) {
+            for (int i = 0; i < kAmpsPerThread; i++) {
                 if ((i & op.mreg) != op.vreg) continue;
                 const std::string v = A(i);
                 s << "  { const double p1 = -" << M << "[1] * " << v << ".y, p2 = " << M << "[1] * " << v << ".x; ";
@@ -409,7 +411,7 @@ JitPass jit_generate(const Step &st)
             }
         } else {
             const int k = op.k;
-            for (int p = 0; p < 8; p++) {
+            for (int p = 0; p < kAmpsPerThread / 2; p++) {
                 const int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1)), i1 = i0 | (1 << k);
                 if ((i0 & (int)op.mreg) != (int)op.vreg) continue;
                 const std::string x = A(i0), y = A(i1);
@@ -462,7 +464,7 @@ JitPass jit_generate(const Step &st)
         const uint64_t cfs = cur;
         flip_mask("gf", "unsigned long long", [&](int k) { return "TPM[" + std::to_string(nib(cfs, k)) + "]"; });
     }
-    for (int j = 0; j < 8; j++)
+    for (int j = 0; j < kAmpsPerThread / 2; j++)
         s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + ((" << roff(cur, j) << ") ^ gf)), \"d\"("
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
@@ -617,7 +619,7 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", 4096 / kTileAmps * 2) | ((uint64_t)jit_pipelined() << 16));
+    put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));

@@ -51,7 +51,7 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t v, int p)
 // ---------------------------------------------------------------- k_pass
 // In-place pair updates: every output is finished by one FMA that consumes
 // the old value held in the same register, after all partial sums that still
-// need the old values are formed.  This keeps the 16 amplitudes in fixed
+// need the old values are formed.  This keeps the amplitudes in fixed
 // registers across the op loop (no compiler copies).
 __device__ __forceinline__ void u2_inplace(double2 &x, double2 &y, const double2 u00, const double2 u01,
                                            const double2 u10, const double2 u11)
@@ -82,7 +82,7 @@ __device__ __forceinline__ void swap_inplace(double &x, double &y)
 }
 
 template <int K, int CODE, bool PRED>
-__device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint32_t mreg, uint32_t vreg)
+__device__ __forceinline__ void reg_apply(double2 (&a)[kAmpsPerThread], const KOp &op, uint32_t mreg, uint32_t vreg)
 {
     double2 u00, u01, u10, u11;
     if (CODE != OPC_XS) {
@@ -92,7 +92,7 @@ __device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint3
         u11 = make_double2(op.m[6], op.m[7]);
     }
 #pragma unroll
-    for (int p = 0; p < 8; p++) {
+    for (int p = 0; p < kAmpsPerThread / 2; p++) {
         const int i0 = ((p >> K) << (K + 1)) | (p & ((1 << K) - 1));
         const int i1 = i0 | (1 << K);
         if (PRED && (i0 & mreg) != vreg) continue;
@@ -108,18 +108,23 @@ __device__ __forceinline__ void reg_apply(double2 (&a)[16], const KOp &op, uint3
 }
 
 template <int CODE, bool PRED>
-__device__ __forceinline__ void reg_dispatch(double2 (&a)[16], const KOp &op, int k, uint32_t mreg, uint32_t vreg)
+__device__ __forceinline__ void reg_dispatch(double2 (&a)[kAmpsPerThread], const KOp &op, int k, uint32_t mreg,
+                                             uint32_t vreg)
 {
     switch (k) {
     case 0: reg_apply<0, CODE, PRED>(a, op, mreg, vreg); break;
     case 1: reg_apply<1, CODE, PRED>(a, op, mreg, vreg); break;
     case 2: reg_apply<2, CODE, PRED>(a, op, mreg, vreg); break;
-    default: reg_apply<3, CODE, PRED>(a, op, mreg, vreg); break;
+    case 3: reg_apply<3, CODE, PRED>(a, op, mreg, vreg); break;
+    default:
+        if constexpr (kRegBits > 4) reg_apply<kRegBits - 1, CODE, PRED>(a, op, mreg, vreg);
+        break;
     }
 }
 
 template <bool PRED>
-__device__ __forceinline__ void reg_op(double2 (&a)[16], const KOp &op, int code, uint32_t mreg, uint32_t vreg)
+__device__ __forceinline__ void reg_op(double2 (&a)[kAmpsPerThread], const KOp &op, int code, uint32_t mreg,
+                                       uint32_t vreg)
 {
     const int k = op.k;
     if (code == OPC_XS) reg_dispatch<OPC_XS, PRED>(a, op, k, mreg, vreg);
@@ -132,10 +137,10 @@ __device__ __forceinline__ void reg_op(double2 (&a)[16], const KOp &op, int code
 // 8-long FMA chain for re and one for im, in the fixed column order the JIT
 // tier generates too (bitwise-identical tiers).
 template <int K, int K2>
-__device__ __forceinline__ void u4_apply(double2 (&a)[16], const KOp *rows)
+__device__ __forceinline__ void u4_apply(double2 (&a)[kAmpsPerThread], const KOp *rows)
 {
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
+    for (int p = 0; p < kAmpsPerThread / 4; p++) {
         const int i0 = (int)insert_zero(insert_zero((uint64_t)p, K), K2);
         const int idx[4] = {i0, i0 | (1 << K), i0 | (1 << K2), i0 | (1 << K) | (1 << K2)};
         const double2 x[4] = {a[idx[0]], a[idx[1]], a[idx[2]], a[idx[3]]};
@@ -157,15 +162,25 @@ __device__ __forceinline__ void u4_apply(double2 (&a)[16], const KOp *rows)
     }
 }
 
-__device__ __forceinline__ void u4_op(double2 (&a)[16], const KOp *rows)
+__device__ __forceinline__ void u4_op(double2 (&a)[kAmpsPerThread], const KOp *rows)
 {
-    switch (rows[0].k * 4 + (int)rows[0].cfg) {
+    switch (rows[0].k * 8 + (int)rows[0].cfg) {
     case 1: u4_apply<0, 1>(a, rows); break;
     case 2: u4_apply<0, 2>(a, rows); break;
     case 3: u4_apply<0, 3>(a, rows); break;
-    case 6: u4_apply<1, 2>(a, rows); break;
-    case 7: u4_apply<1, 3>(a, rows); break;
-    default: u4_apply<2, 3>(a, rows); break;
+    case 10: u4_apply<1, 2>(a, rows); break;
+    case 11: u4_apply<1, 3>(a, rows); break;
+    case 19: u4_apply<2, 3>(a, rows); break;
+    default:
+        if constexpr (kRegBits > 4) {
+            switch (rows[0].k * 8 + (int)rows[0].cfg) {
+            case 4: u4_apply<0, 4>(a, rows); break;
+            case 12: u4_apply<1, 4>(a, rows); break;
+            case 20: u4_apply<2, 4>(a, rows); break;
+            default: u4_apply<3, 4>(a, rows); break;
+            }
+        }
+        break;
     }
 }
 
@@ -177,49 +192,64 @@ __device__ __forceinline__ void u4_op(double2 (&a)[16], const KOp *rows)
 __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
 // thread's lane/warp part of the smem index and the 4 register-bit parts
-__device__ __forceinline__ void smem_coords(uint64_t c, int lane, int warp, int &zt, int (&zr)[4])
+__device__ __forceinline__ void smem_coords(uint64_t c, int lane, int warp, int &zt, int (&zr)[kRegBits])
 {
     int st = 0;
 #pragma unroll
-    for (int j = 0; j < 5; j++) st |= ((lane >> j) & 1) << cfg_nib(c, 4 + j);
+    for (int j = 0; j < 5; j++) st |= ((lane >> j) & 1) << cfg_nib(c, kLaneNib + j);
 #pragma unroll
-    for (int j = 0; j < kWarpBits; j++) st |= ((warp >> j) & 1) << cfg_nib(c, 9 + j);
+    for (int j = 0; j < kWarpBits; j++) st |= ((warp >> j) & 1) << cfg_nib(c, kWarpNib + j);
     zt = swz(st);
 #pragma unroll
-    for (int j = 0; j < 4; j++) zr[j] = swz(1 << cfg_nib(c, j));
+    for (int j = 0; j < kRegBits; j++) zr[j] = swz(1 << cfg_nib(c, j));
 }
 
 template <int I>
-__device__ __forceinline__ int zsel(int zt, const int (&zr)[4])
+__device__ __forceinline__ int zsel(int zt, const int (&zr)[kRegBits])
 {
-    return zt ^ ((I & 1) ? zr[0] : 0) ^ ((I & 2) ? zr[1] : 0) ^ ((I & 4) ? zr[2] : 0) ^ ((I & 8) ? zr[3] : 0);
+    int z = zt;
+#pragma unroll
+    for (int b = 0; b < kRegBits; b++)
+        if ((I >> b) & 1) z ^= zr[b];
+    return z;
 }
 
 template <int I>
-__device__ __forceinline__ void sts_all(double2 *sm, const double2 (&a)[16], int zt, const int (&zr)[4])
+__device__ __forceinline__ void sts_all(double2 *sm, const double2 (&a)[kAmpsPerThread], int zt,
+                                        const int (&zr)[kRegBits])
 {
     sm[zsel<I>(zt, zr)] = a[I];
-    if constexpr (I + 1 < 16) sts_all<I + 1>(sm, a, zt, zr);
+    if constexpr (I + 1 < kAmpsPerThread) sts_all<I + 1>(sm, a, zt, zr);
 }
 template <int I>
-__device__ __forceinline__ void lds_all(const double2 *sm, double2 (&a)[16], int zt, const int (&zr)[4])
+__device__ __forceinline__ void lds_all(const double2 *sm, double2 (&a)[kAmpsPerThread], int zt,
+                                        const int (&zr)[kRegBits])
 {
     a[I] = sm[zsel<I>(zt, zr)];
-    if constexpr (I + 1 < 16) lds_all<I + 1>(sm, a, zt, zr);
+    if constexpr (I + 1 < kAmpsPerThread) lds_all<I + 1>(sm, a, zt, zr);
 }
 
 // global offset of the thread's lane/warp part and register-bit parts (load/store configs)
 __device__ __forceinline__ void global_coords(const PassDesc &d, uint64_t c, int lane, int warp, uint64_t &gt,
-                                              uint64_t &g1, uint64_t &g2, uint64_t &g3)
+                                              uint64_t (&g)[kRegBits])
 {
     gt = (uint64_t)((lane & 3) << 1);  // l0 = tile bit 1 = phys 1, l1 = tile bit 2 = phys 2
 #pragma unroll
-    for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << d.tp[cfg_nib(c, 4 + j)];
+    for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << d.tp[cfg_nib(c, kLaneNib + j)];
 #pragma unroll
-    for (int j = 0; j < kWarpBits; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, 9 + j)];
-    g1 = 1ULL << d.tp[cfg_nib(c, 1)];
-    g2 = 1ULL << d.tp[cfg_nib(c, 2)];
-    g3 = 1ULL << d.tp[cfg_nib(c, 3)];
+    for (int j = 0; j < kWarpBits; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, kWarpNib + j)];
+#pragma unroll
+    for (int b = 1; b < kRegBits; b++) g[b] = 1ULL << d.tp[cfg_nib(c, b)];  // register bit 0: within a 256-bit access
+}
+
+// global offset of register pair j (register bits 1.. of the pair index)
+__device__ __forceinline__ uint64_t pair_off(int j, const uint64_t (&g)[kRegBits])
+{
+    uint64_t ro = 0;
+#pragma unroll
+    for (int b = 1; b < kRegBits; b++)
+        if ((j >> (b - 1)) & 1) ro |= g[b];
+    return ro;
 }
 
 template <int CAP>
@@ -242,23 +272,20 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     const uint64_t gcta = d.rank_bits | base;
 
     uint64_t cfg = d.cfg0;
-    double2 a[16];
+    double2 a[kAmpsPerThread];
     {
-        uint64_t gt, g1, g2, g3;
-        global_coords(d, cfg, lane, warp, gt, g1, g2, g3);
+        uint64_t gt, g[kRegBits];
+        global_coords(d, cfg, lane, warp, gt, g);
         const double2 *p = st + base + gt;
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            const uint64_t ro = ((j & 1) ? g1 : 0) | ((j & 2) ? g2 : 0) | ((j & 4) ? g3 : 0);
-            ld256(p + ro, a[2 * j], a[2 * j + 1]);
-        }
+        for (int j = 0; j < kAmpsPerThread / 2; j++) ld256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);
     }
 
     for (int o = 0; o < d.n_ops; o++) {
         const KOp &op = P.ops[o];
         const int code = op.code;
         if (code == OPC_TRANS) {
-            int zt, zr[4];
+            int zt, zr[kRegBits];
             smem_coords(cfg, lane, warp, zt, zr);
             sts_all<0>(sm, a, zt, zr);
             __syncthreads();
@@ -281,7 +308,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
         if (code == OPC_PHASE || code == OPC_PHASE_ACC) {
             const double fr = op.m[0], fi = op.m[1];
 #pragma unroll
-            for (int i = 0; i < 16; i++) {
+            for (int i = 0; i < kAmpsPerThread; i++) {
                 if ((i & mreg) != vreg) continue;
                 const double p1 = -fi * a[i].y, p2 = fi * a[i].x;
                 a[i].x = fma(fr, a[i].x, p1);
@@ -294,14 +321,11 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     }
 
     {
-        uint64_t gt, g1, g2, g3;
-        global_coords(d, cfg, lane, warp, gt, g1, g2, g3);
+        uint64_t gt, g[kRegBits];
+        global_coords(d, cfg, lane, warp, gt, g);
         double2 *p = st + base + gt;
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            const uint64_t ro = ((j & 1) ? g1 : 0) | ((j & 2) ? g2 : 0) | ((j & 4) ? g3 : 0);
-            st256(p + ro, a[2 * j], a[2 * j + 1]);
-        }
+        for (int j = 0; j < kAmpsPerThread / 2; j++) st256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);
     }
 }
 
@@ -331,7 +355,7 @@ static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cud
 
 void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s)
 {
-    constexpr int kMinB = 8192 / kTileAmps;  // 2 CTAs of 256 threads, or 4 of 128 (<= 128 registers)
+    constexpr int kMinB = kPassMinBlocks;
     if (variant == 1) launch_pass_minb<kMinB / 2>(d, ops, st, s);
     else launch_pass_minb<kMinB>(d, ops, st, s);
 }
@@ -339,7 +363,7 @@ void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cu
 int pass_regs_per_thread()
 {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, (k_pass<kMaxPassOps, 8192 / kTileAmps>)) != cudaSuccess) return -1;
+    if (cudaFuncGetAttributes(&fa, (k_pass<kMaxPassOps, kPassMinBlocks>)) != cudaSuccess) return -1;
     return fa.numRegs;
 }
 

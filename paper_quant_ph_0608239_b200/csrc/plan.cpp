@@ -106,7 +106,7 @@ PhaseRunPlan plan_phase_run(const KOp *ops, size_t n)
     PhaseRunPlan r;
     for (size_t o = 0; o < n; o++) {
         const uint32_t m = ops[o].mreg, v = ops[o].vreg, O = m & v, Z = m & ~v;
-        for (uint32_t i = 0; i < 16; i++)
+        for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++)
             if ((i & m) == v) r.direct += 4;
         for (uint32_t T = Z;; T = (T - 1) & Z) {  // subsets of Z
             r.used |= 1u << (O | T);
@@ -116,11 +116,11 @@ PhaseRunPlan plan_phase_run(const KOp *ops, size_t n)
     }
     const double kExp = 20, kMul = 4;  // e^{i theta} (table x Taylor) and complex multiply
     // mode A: distinct (set of monomials below register i) -> one exp each
-    uint32_t keys[16];
+    uint32_t keys[kAmpsPerThread];
     int nkeys = 0, nregs = 0;
-    for (uint32_t i = 0; i < 16; i++) {
+    for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++) {
         uint32_t key = 0;
-        for (uint32_t S = 0; S < 16; S++)
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
             if (((r.used >> S) & 1) && (S & i) == S) key |= 1u << S;
         if (!key) continue;
         nregs++;
@@ -130,8 +130,8 @@ PhaseRunPlan plan_phase_run(const KOp *ops, size_t n)
     }
     const double costA = nkeys * kExp + nregs * kMul;
     double costB = 0;
-    for (uint32_t S = 0; S < 16; S++)
-        if ((r.used >> S) & 1) costB += kExp + kMul * (double)(16 >> __builtin_popcount(S));
+    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+        if ((r.used >> S) & 1) costB += kExp + kMul * (double)(kAmpsPerThread >> __builtin_popcount(S));
     r.mode = costB < costA ? 1 : 0;
     r.acc += std::min(costA, costB);
     return r;
@@ -163,19 +163,19 @@ static void set_u2_code(const GateRec &g, POp &p)
 namespace {
 // thread-coordinate assignment of the 12 tile-local bits (see engine.h)
 struct Cfg {
-    int r[4], l[5], w[kWarpBits];
+    int r[kRegBits], l[5], w[kWarpBits];
     uint64_t pack() const
     {
         uint64_t c = 0;
-        for (int j = 0; j < 4; j++) c |= (uint64_t)r[j] << (4 * j);
-        for (int j = 0; j < 5; j++) c |= (uint64_t)l[j] << (4 * (4 + j));
-        for (int j = 0; j < kWarpBits; j++) c |= (uint64_t)w[j] << (4 * (9 + j));
+        for (int j = 0; j < kRegBits; j++) c |= (uint64_t)r[j] << (4 * j);
+        for (int j = 0; j < 5; j++) c |= (uint64_t)l[j] << (4 * (kLaneNib + j));
+        for (int j = 0; j < kWarpBits; j++) c |= (uint64_t)w[j] << (4 * (kWarpNib + j));
         return c;
     }
     bool store_ok() const { return r[0] == 0 && l[0] == 1 && l[1] == 2; }
     int role_of(int t, int &j) const
     {
-        for (j = 0; j < 4; j++)
+        for (j = 0; j < kRegBits; j++)
             if (r[j] == t) return ROLE_REG;
         for (j = 0; j < 5; j++)
             if (l[j] == t) return ROLE_LANE;
@@ -197,7 +197,7 @@ Cfg make_cfg(const std::vector<int> &reg_in, bool store)
         reg.insert(reg.begin(), 0);
     }
     bool used[kTileBits] = {false};
-    for (int j = 0; j < 4; j++) { c.r[j] = reg[j]; used[reg[j]] = true; }
+    for (int j = 0; j < kRegBits; j++) { c.r[j] = reg[j]; used[reg[j]] = true; }
     std::vector<int> lanes;
     if (store) { lanes = {1, 2}; used[1] = used[2] = true; }
     // one lane bit of every missing residue first
@@ -500,8 +500,8 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
     auto upcoming = [&](bool store, std::vector<int> &reg) {
         reg.clear();
         if (store) reg.push_back(0);
-        for (int pass = 0; pass < 2 && reg.size() < 4; pass++)
-            for (size_t b = 0; b < n && reg.size() < 4; b++) {
+        for (int pass = 0; pass < 2 && reg.size() < (size_t)kRegBits; pass++)
+            for (size_t b = 0; b < n && reg.size() < (size_t)kRegBits; b++) {
                 if (done[b] || pops[b].code == OPC_PHASE) continue;
                 if ((pass == 0) != ready(b)) continue;
                 std::vector<int> need;
@@ -513,10 +513,10 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
                 std::vector<int> add;
                 for (int t : need)
                     if (std::find(reg.begin(), reg.end(), t) == reg.end()) add.push_back(t);
-                if (reg.size() + add.size() > 4) continue;  // a block needs both of its bits at once
+                if (reg.size() + add.size() > (size_t)kRegBits) continue;  // a block needs both of its bits at once
                 for (int t : add) reg.push_back(t);
             }
-        for (int t = 3; reg.size() < 4 && t < kTileBits; t++)
+        for (int t = 3; reg.size() < (size_t)kRegBits && t < kTileBits; t++)
             if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
     };
     std::vector<int> reg;
@@ -555,10 +555,10 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
                     if (t != 0 && std::find(need.begin(), need.end(), t) == need.end()) need.push_back(t);
                 }
             }
-            if (store_fits && need.size() <= 3) {
+            if (store_fits && need.size() <= (size_t)kRegBits - 1) {
                 std::vector<int> r{0};
                 for (int t : need) r.push_back(t);
-                for (int t = 3; r.size() < 4 && t < kTileBits; t++)
+                for (int t = 3; r.size() < (size_t)kRegBits && t < kTileBits; t++)
                     if (std::find(r.begin(), r.end(), t) == r.end()) r.push_back(t);
                 cfg = make_cfg(r, true);
             } else {
@@ -656,9 +656,9 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
     }
     if (!cfg.store_ok()) {
         std::vector<int> r2;
-        for (int k = 0; k < 4; k++)
+        for (int k = 0; k < kRegBits; k++)
             if (cfg.r[k] != 1 && cfg.r[k] != 2) r2.push_back(cfg.r[k]);
-        for (int t = 3; r2.size() < 4 && t < kTileBits; t++)
+        for (int t = 3; r2.size() < (size_t)kRegBits && t < kTileBits; t++)
             if (std::find(r2.begin(), r2.end(), t) == r2.end()) r2.push_back(t);
         if (std::find(r2.begin(), r2.end(), 0) == r2.end()) { r2.insert(r2.begin(), 0); r2.pop_back(); }
         emit_trans(make_cfg(r2, true));
