@@ -120,4 +120,24 @@ struct PermDesc {
     int32_t tile_sorted[kPermTileBits]; // same positions sorted ascending
 };
 
+// A run of controlled permutations of ONE target register (consecutive perm
+// gates with identical targets, e.g. Shor's modular multiplications by
+// y^(2^j) mod G) applied in one pass (k_perm_run): each element
+// gathers through the inverse tables of the perms whose controls it satisfies.
+constexpr int kMaxPermRun = 32;
+struct PermRunDesc {
+    uint64_t rank_bits;
+    uint64_t n_inst;
+    int32_t M;
+    int32_t t;           // target bits = tile-local bits 0..t-1 (register order)
+    int32_t tile_bits;
+    int32_t R;           // perms in the run (<= kMaxPermRun)
+    int32_t contiguous;
+    int32_t tab_offset;  // first inverse table (R tables of 2^t uint32) in the perm-table array
+    int32_t tile_pos[kPermTileBits];
+    int32_t tile_sorted[kPermTileBits];
+    uint32_t m_tile[kMaxPermRun], v_tile[kMaxPermRun];  // controls on tile-local bits
+    uint64_t m_out[kMaxPermRun], v_out[kMaxPermRun];    // controls outside the tile (incl. rank bits)
+};
+
 }  // namespace qsb

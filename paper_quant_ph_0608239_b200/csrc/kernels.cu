@@ -9,6 +9,7 @@
 // sm_100a) move two amplitudes per instruction.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "engine.h"
@@ -470,6 +471,121 @@ __global__ void __launch_bounds__(256) k_perm(const __grid_constant__ PermDesc d
         if ((e & d.m_ctrl_tile) != d.v_ctrl_tile) continue;
         st[base + dep_tile(e, d.tile_pos, d.tile_bits)] = sm[(e & ~T) | perm[e & T]];
     }
+}
+
+// Run of permutations of one register (PermRunDesc).  Persistent CTAs: the
+// R inverse tables (as uint16) are staged in shared memory once, then each tile
+// (targets + extra bits, as in k_perm) is staged and every element gathers
+// through the tables of the perms whose controls it satisfies, latest first:
+// out[x, w] = in[x, P_j1^-1(... P_jk^-1(w))].  Controls are never targets, so
+// the active set depends only on the non-target bits, shared by an element
+// and its source.  Elements no perm touches are neither read nor written.
+__global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRunDesc d, double2 *__restrict__ st,
+                                                  const uint32_t *__restrict__ tabs)
+{
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const uint32_t E = 1u << d.tile_bits, TT = 1u << d.t, T = TT - 1, NX = E >> d.t;
+    double2 *sm = reinterpret_cast<double2 *>(smraw);
+    uint32_t *xmask = reinterpret_cast<uint32_t *>(smraw + (size_t)E * sizeof(double2));  // NX entries
+    uint16_t *tab = reinterpret_cast<uint16_t *>(xmask + NX);                            // R * TT entries
+    for (uint32_t i = threadIdx.x; i < (uint32_t)d.R * TT; i += blockDim.x) tab[i] = (uint16_t)__ldg(tabs + d.tab_offset + i);
+    // in-tile control predicates of every extra-bit pattern x (tile-local e = x << t | w)
+    for (uint32_t x = threadIdx.x; x < NX; x += blockDim.x) {
+        uint32_t m = 0;
+        for (int j = 0; j < d.R; j++)
+            if (((x << d.t) & d.m_tile[j]) == d.v_tile[j]) m |= 1u << j;
+        xmask[x] = m;
+    }
+    __syncthreads();
+    for (uint64_t inst = blockIdx.x; inst < d.n_inst; inst += gridDim.x) {
+        uint64_t base = inst;
+        for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
+        uint32_t A = 0;  // perms whose out-of-tile controls this tile satisfies
+        for (int j = 0; j < d.R; j++)
+            if (((d.rank_bits | base) & d.m_out[j]) == d.v_out[j]) A |= 1u << j;
+        if (!A) continue;  // uniform: no barrier skipped by part of the CTA
+        if (d.contiguous) {
+            const double2 *src = st + base;
+            for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
+                if (!(A & xmask[e >> d.t])) continue;
+                double2 x0, x1;
+                ld256(src + e, x0, x1);
+                sm[e] = x0;
+                sm[e + 1] = x1;
+            }
+        } else {
+            for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
+                if (A & xmask[e >> d.t]) sm[e] = st[base + dep_tile(e, d.tile_pos, d.tile_bits)];
+        }
+        __syncthreads();
+        if (d.contiguous && d.t >= 3) {
+            // 8 consecutive elements share the non-target bits: 8 independent
+            // lookup chains per step hide the shared-memory latency
+            double2 *dst = st + base;
+            for (uint32_t e = 8 * threadIdx.x; e < E; e += 8 * blockDim.x) {
+                uint32_t act = A & xmask[e >> d.t];
+                if (!act) continue;
+                uint32_t w[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) w[i] = (e + i) & T;
+                while (act) {
+                    const int j = 31 - __clz(act);  // latest active perm first (inverse order)
+                    const uint16_t *tj = tab + j * TT;
+#pragma unroll
+                    for (int i = 0; i < 8; i++) w[i] = tj[w[i]];
+                    act &= ~(1u << j);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i += 2) st256(dst + e + i, sm[(e & ~T) | w[i]], sm[(e & ~T) | w[i + 1]]);
+            }
+        } else if (d.contiguous) {
+            double2 *dst = st + base;
+            for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
+                const uint32_t act0 = A & xmask[e >> d.t];  // e, e+1 differ in target bit 0 only
+                if (!act0) continue;
+                uint32_t w0 = e & T, w1 = (e + 1) & T, act = act0;
+                while (act) {
+                    const int j = 31 - __clz(act);
+                    w0 = tab[j * TT + w0];
+                    w1 = tab[j * TT + w1];
+                    act &= ~(1u << j);
+                }
+                st256(dst + e, sm[(e & ~T) | w0], sm[((e + 1) & ~T) | w1]);
+            }
+        } else {
+            for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+                uint32_t act = A & xmask[e >> d.t];
+                if (!act) continue;
+                uint32_t w = e & T;
+                while (act) {
+                    const int j = 31 - __clz(act);
+                    w = tab[j * TT + w];
+                    act &= ~(1u << j);
+                }
+                st[base + dep_tile(e, d.tile_pos, d.tile_bits)] = sm[(e & ~T) | w];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t perm_run_smem(const PermRunDesc &d)
+{
+    const size_t E = (size_t)1 << d.tile_bits;
+    return E * sizeof(double2) + (E >> d.t) * sizeof(uint32_t) + (size_t)d.R * ((size_t)1 << d.t) * sizeof(uint16_t);
+}
+
+void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab, int n_sm, cudaStream_t s)
+{
+    const size_t smem = perm_run_smem(d);
+    cudaFuncSetAttribute(k_perm_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_perm_run, 256, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    const uint64_t grid = std::min<uint64_t>(d.n_inst, (uint64_t)per_sm * (uint64_t)n_sm);
+    k_perm_run<<<(unsigned)grid, 256, smem, s>>>(d, st, perm_tab);
 }
 
 void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaStream_t s)

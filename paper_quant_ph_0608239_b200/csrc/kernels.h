@@ -28,6 +28,8 @@ void launch_gate_generic(double2 *st, int M, uint64_t rank_bits, int t, uint64_t
 void launch_phase_generic(double2 *st, int M, uint64_t rank_bits, uint64_t cm, uint64_t cv, double fr, double fi,
                           cudaStream_t s);
 void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaStream_t s);
+size_t perm_run_smem(const PermRunDesc &d);
+void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab, int n_sm, cudaStream_t s);
 void launch_init(double2 *st, uint64_t n_amps, int64_t one_at, cudaStream_t s);
 void launch_probs(const double2 *st, const ProbsDesc &d, double *partial, double *out, cudaStream_t s);
 void launch_expect(const double2 *st, int M, double *partial, double *out /* M+1 */, cudaStream_t s);

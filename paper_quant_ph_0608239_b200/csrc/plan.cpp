@@ -5,6 +5,7 @@
 //   * ST_PASS      one fused tile pass (kernels.cu k_pass) applying many gates
 //   * ST_GENERIC / ST_PHASE   one gate per launch (small shards, fusion off)
 //   * ST_PERM      one controlled register permutation (k_perm)
+//   * ST_PERMRUN   a run of permutations of one register in one pass (k_perm_run)
 //   * ST_EXCHANGE  the paper's K-pair local<->nonlocal qubit interchange
 //                  (Eqs. onequbitchange / twoqubitchange0-5)
 // It keeps sigma (qubit <-> physical bit).  SWAP gates are
@@ -829,6 +830,41 @@ void Planner::emit_perm(const GateRec &g, std::vector<Step> &out)
     out.push_back(std::move(s));
 }
 
+// Consecutive permutations of the same register (Shor's modular
+// multiplications) become one step: one HBM pass instead of one per gate.
+size_t Planner::emit_perm_run(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
+                              std::vector<Step> &out)
+{
+    const GateRec &g = gates[first];
+    std::vector<size_t> run{first};
+    for (size_t i = first + 1; i < gates.size() && run.size() < (size_t)kMaxPermRun; i++) {
+        if (done[i]) continue;
+        const GateRec &h = gates[i];
+        if (h.kind != GK_PERM || h.targets != g.targets) break;
+        run.push_back(i);
+    }
+    if (run.size() < 2 || g.targets.size() > 16) {
+        emit_perm(g, out);
+        done[first] = 1;
+        return 1;
+    }
+    Step s;
+    s.type = ST_PERMRUN;
+    for (int t : g.targets) s.ptargets.push_back(phys_of[t]);
+    for (size_t i : run) {
+        const GateRec &h = gates[i];
+        uint64_t cm = 0;
+        for (int c : h.controls) cm |= bit(phys_of[c]);
+        s.run_cm.push_back(cm);
+        s.run_gate.push_back(h.id);
+        s.perm.insert(s.perm.end(), h.perm.begin(), h.perm.end());
+        done[i] = 1;
+    }
+    s.gate_id = g.id;
+    out.push_back(std::move(s));
+    return run.size();
+}
+
 void Planner::emit_exchange(const std::vector<GateRec> &gates, const std::vector<char> &done, size_t first,
                             std::vector<Step> &out)
 {
@@ -1019,8 +1055,7 @@ void Planner::plan_list(const std::vector<GateRec> &gates, const PlanOptions &op
             continue;
         }
         if (g.kind == GK_PERM) {
-            emit_perm(g, out);
-            done[first] = 1;
+            emit_perm_run(gates, done, first, out);
             continue;
         }
         if (fused) {
@@ -1077,6 +1112,15 @@ std::string plan_to_json(const Planner &P, const std::vector<Step> &steps)
             break;
         case ST_PERM:
             o << "{\"type\":\"perm\",\"gate\":" << st.gate_id << ",\"cm\":" << st.cm << ",\"targets\":[";
+            for (size_t j = 0; j < st.ptargets.size(); j++) o << (j ? "," : "") << st.ptargets[j];
+            o << "]}";
+            break;
+        case ST_PERMRUN:
+            o << "{\"type\":\"permrun\",\"gates\":[";
+            for (size_t j = 0; j < st.run_gate.size(); j++) o << (j ? "," : "") << st.run_gate[j];
+            o << "],\"cms\":[";
+            for (size_t j = 0; j < st.run_cm.size(); j++) o << (j ? "," : "") << st.run_cm[j];
+            o << "],\"targets\":[";
             for (size_t j = 0; j < st.ptargets.size(); j++) o << (j ? "," : "") << st.ptargets[j];
             o << "]}";
             break;

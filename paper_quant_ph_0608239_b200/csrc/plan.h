@@ -42,7 +42,8 @@ struct PhaseRunPlan {
 };
 PhaseRunPlan plan_phase_run(const KOp *ops, size_t n);
 
-enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5, ST_PAIRWISE = 6 };
+enum StepType { ST_PASS = 0, ST_GENERIC = 1, ST_PHASE = 2, ST_PERM = 3, ST_EXCHANGE = 4, ST_RELABEL = 5, ST_PAIRWISE = 6,
+                ST_PERMRUN = 7 };
 
 // global-target policy: remap (K-pair interchange),
 // pairwise (partner shards combine, sigma unchanged), or auto
@@ -65,9 +66,11 @@ struct Step {
     uint64_t cm = 0, cv = 0;
     double m[8] = {0};
     int gate_id = -1;
-    // ST_PERM
+    // ST_PERM / ST_PERMRUN
     std::vector<int> ptargets;    // physical positions, register order
-    std::vector<uint32_t> perm;
+    std::vector<uint32_t> perm;   // PERMRUN: the R tables back to back
+    std::vector<uint64_t> run_cm; // PERMRUN: full-index control mask of each perm (fires on all ones)
+    std::vector<int> run_gate;    // PERMRUN: gate id of each perm
     // ST_EXCHANGE: swap local bits lpos[i] with global bits gpos[i]
     std::vector<int> lpos, gpos;
     // ST_RELABEL: swap physical roles of logical qubits a,b (no data)
@@ -103,6 +106,8 @@ private:
                     const PlanOptions &opt, std::vector<Step> &out);
     void emit_generic(const GateRec &g, std::vector<Step> &out);
     void emit_perm(const GateRec &g, std::vector<Step> &out);
+    size_t emit_perm_run(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
+                         std::vector<Step> &out);
     void swap_layout(int pa, int pb);
     void plan_list(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out);
 };

@@ -479,7 +479,7 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 {
     size_t nops = 0, nperm = 0;  // pass ops travel in the kernel parameter block
     for (Step &s : steps)
-        if (s.type == ST_PERM) nperm += s.perm.size();
+        if (s.type == ST_PERM || s.type == ST_PERMRUN) nperm += s.perm.size();
     (void)nops;
     if (nperm == 0) return QSIM_OK;
     qsim_status st;
@@ -488,9 +488,10 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
     if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));  // staging reuse
     size_t p = 0;
     for (Step &s : steps) {
-        if (s.type == ST_PERM) {
-            // k_perm gathers: out[w] = in[perm^-1(w)]
-            for (size_t w = 0; w < s.perm.size(); w++) c->h_perm[p + s.perm[w]] = (uint32_t)w;
+        if (s.type == ST_PERM || s.type == ST_PERMRUN) {
+            // k_perm / k_perm_run gather: out[w] = in[perm^-1(w)]; a run's tables back to back
+            const size_t TT = (size_t)1 << s.ptargets.size();
+            for (size_t w = 0; w < s.perm.size(); w++) c->h_perm[p + (w / TT) * TT + s.perm[w]] = (uint32_t)(w % TT);
             s.t = (int)p;  // perm offset
             p += s.perm.size();
         }
@@ -503,6 +504,52 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 
 static int local_ranks(qsim_ctx c, int i) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? i : c->rank; }
 static int n_local(qsim_ctx c) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? c->P : 1; }
+
+static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
+{
+    PermRunDesc d{};
+    const int M = c->M, t = (int)s.ptargets.size();
+    // smaller tiles than k_perm's: the run's tables share the shared memory,
+    // and more resident CTAs hide the load latency of the gather
+    static const int run_tb = [] { const char *e = getenv("QSIM_PERMRUN_TILE"); return e ? atoi(e) : 10; }();
+    int tb = std::max(std::min(run_tb, M), t);
+    d.M = M;
+    d.t = t;
+    d.tile_bits = tb;
+    d.R = (int)s.run_cm.size();
+    d.tab_offset = s.t;
+    bool used[64] = {false};
+    for (int i = 0; i < t; i++) { d.tile_pos[i] = s.ptargets[i]; used[s.ptargets[i]] = true; }
+    int nb = t;
+    for (int p = 0; p < M && nb < tb; p++)
+        if (!used[p]) { d.tile_pos[nb++] = p; used[p] = true; }
+    int srt[kPermTileBits];
+    for (int i = 0; i < tb; i++) srt[i] = d.tile_pos[i];
+    std::sort(srt, srt + tb);
+    for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
+    d.n_inst = 1ULL << (M - tb);
+    d.contiguous = 1;
+    for (int i = 0; i < tb; i++)
+        if (d.tile_pos[i] != i) d.contiguous = 0;
+    for (int j = 0; j < d.R; j++)
+        for (int b = 0; b < 64; b++) {
+            if (!((s.run_cm[j] >> b) & 1)) continue;
+            int tl = -1;
+            for (int i = 0; i < tb; i++)
+                if (d.tile_pos[i] == b) tl = i;
+            if (tl >= 0) { d.m_tile[j] |= 1u << tl; d.v_tile[j] |= 1u << tl; }
+            else { d.m_out[j] |= 1ULL << b; d.v_out[j] |= 1ULL << b; }
+        }
+    if (perm_run_smem(d) > 200 * 1024) FAIL(c, QSIM_ERR_ARG, "permutation run too large for shared memory");
+    RangeGuard rg(c, 2, 0);
+    for (int i = 0; i < n_local(c); i++) {
+        d.rank_bits = (uint64_t)local_ranks(c, i) << M;
+        launch_perm_run(d, c->shards[i], c->d_perm, c->n_sm, c->stream);
+        LAUNCHED(c);
+        c->stats.perm_launches++;
+    }
+    return QSIM_OK;
+}
 
 static qsim_status exec_perm(qsim_ctx c, const Step &s)
 {
@@ -672,6 +719,9 @@ static qsim_status flush(qsim_ctx c)
         }
         case ST_PERM:
             if ((st = exec_perm(c, s)) != QSIM_OK) return st;
+            break;
+        case ST_PERMRUN:
+            if ((st = exec_perm_run(c, s)) != QSIM_OK) return st;
             break;
         case ST_EXCHANGE:
             if ((st = exec_exchange(c, s)) != QSIM_OK) return st;

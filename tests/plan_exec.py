@@ -41,6 +41,20 @@ def _apply(psi, idx, code, t, cm, cv, m):
     psi[i1] = u10 * x + u11 * y
 
 
+def _apply_perm(psi, idx, perm, T, cm):
+    w = np.zeros_like(idx)
+    for b, p in enumerate(T):
+        w |= ((idx >> p) & 1) << b
+    pw = np.asarray(perm, dtype=np.int64)[w]
+    dest = idx.copy()
+    for b, p in enumerate(T):
+        dest = (dest & ~(1 << p)) | (((pw >> b) & 1) << p)
+    sel = (idx & cm) == cm
+    new = psi.copy()
+    new[dest[sel]] = psi[idx[sel]]
+    return new
+
+
 def _swap_bits(idx, a, b):
     ba, bb = (idx >> a) & 1, (idx >> b) & 1
     return idx ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
@@ -68,6 +82,9 @@ def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
             _apply(psi, idx, st["code"], st["t"], st["cm"], st["cv"], st["m"])
         elif ty == "phase":
             _apply(psi, idx, 3, -1, st["cm"], st["cv"], st["m"])
+        elif ty == "permrun":  # the run's perms in order, each with its own controls
+            for gid, cm in zip(st["gates"], st["cms"]):
+                psi = _apply_perm(psi, idx, gates[gid].perm, st["targets"], cm)
         elif ty == "perm":
             g = gates[st["gate"]]
             T = st["targets"]

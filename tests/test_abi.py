@@ -139,6 +139,25 @@ def test_block_fusion_mixed_predicates(pkg, oracle_mod):
         assert any(op["code"] == 7 for op in _pass_ops(d))
 
 
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_plan_perm_run(pkg, oracle_mod, P):
+    """Consecutive permutations of one register (Shor's modular
+    multiplications, and a mix of 0/1/2 controls) become one permrun step."""
+    w = C.shor_order_finding(35, 3, 8, 6)
+    d = _check_plan(pkg, oracle_mod, w.n, P, w.init, w.gates)
+    runs = [s for s in d["plan"]["steps"] if s["type"] == "permrun"]
+    assert len(runs) == 1 and len(runs[0]["gates"]) == 8
+    assert not any(s["type"] == "perm" for s in d["plan"]["steps"])
+    r = np.random.default_rng(5)
+    tg = (2, 7, 4)
+    gates = [G.one_q(q, G.H) for q in range(13)]
+    for ctl in [(), (0,), (9, 12), (1,), (12,), (3, 5), ()]:
+        gates.append(G.perm_gate(ctl, tg, r.permutation(8).astype(np.uint32)))
+    gates.append(G.one_q(4, G.H))
+    d = _check_plan(pkg, oracle_mod, 13, P, 0, gates)
+    assert [len(s["gates"]) for s in d["plan"]["steps"] if s["type"] == "permrun"] == [7]
+
+
 def test_plan_qft_sharded(pkg, oracle_mod):
     w = C.qft_basis(14, 12345)
     d = _check_plan(pkg, oracle_mod, 14, 4, w.init, w.gates)

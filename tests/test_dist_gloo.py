@@ -87,6 +87,20 @@ def _worker(rank, world, port, case, out_q, policy=None):
                 _apply(shard, full, st["code"], st["t"], st["cm"], st["cv"], st["m"])
             elif ty == "phase":
                 _apply(shard, full, 3, -1, st["cm"], st["cv"], st["m"])
+            elif ty == "permrun":
+                loc = np.arange(1 << M, dtype=np.int64)
+                for gid, cm in zip(st["gates"], st["cms"]):
+                    w = np.zeros(1 << M, dtype=np.int64)
+                    for b, p in enumerate(st["targets"]):
+                        w |= ((loc >> p) & 1) << b
+                    pw = np.asarray(gates[gid].perm, dtype=np.int64)[w]
+                    dest = loc.copy()
+                    for b, p in enumerate(st["targets"]):
+                        dest = (dest & ~(1 << p)) | (((pw >> b) & 1) << p)
+                    sel = (full & cm) == cm
+                    new = shard.copy()
+                    new[dest[sel]] = shard[sel]
+                    shard = new
             elif ty == "perm":
                 g = gates[st["gate"]]
                 T, cm = st["targets"], st["cm"]

@@ -145,6 +145,22 @@ def test_block_fusion_parity(P, oracle_mod, n, ranks, jit):
         assert_parity(sim, o, n)
 
 
+@pytest.mark.parametrize("n,ranks", [(13, 1), (16, 1), (16, 4), (14, 2)])
+def test_perm_run_parity(P, oracle_mod, n, ranks):
+    """A run of permutations of one register with 0/1/2 controls in and out of
+    the tile, on contiguous (low) and scattered targets (k_perm_run)."""
+    r = np.random.default_rng(n + ranks)
+    gates = [G.one_q(q, G.haar_u2(G.SplitMix64(q + 1))) for q in range(n)]
+    for tg in [(0, 1, 2), (5, 1, n - 3, 8)]:
+        for ctl in [(), (4,), (n - 1, 3), (n - 2,), (6,), (3, n - 1), ()]:
+            if set(ctl) & set(tg):
+                continue
+            gates.append(G.perm_gate(ctl, tg, r.permutation(1 << len(tg)).astype(np.uint32)))
+        gates.append(G.cnot(tg[0], n - 1))
+    sim = gpu_run(P, n, 3, gates, ranks=ranks)
+    assert_parity(sim, oracle_run(oracle_mod, n, 3, gates), n)
+
+
 @pytest.mark.parametrize("ranks,n", [(2, 14), (4, 15), (8, 16), (8, 12), (4, 9)])
 def test_every_gate_sharded_virtual(P, oracle_mod, ranks, n):
     gates = kitchen_sink(n, seed=100 + n)
