@@ -10,6 +10,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <atomic>
 #include <chrono>
@@ -339,6 +340,43 @@ JitPass jit_generate(const Step &st)
             const int k = op.k, k2 = (int)op.cfg;
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
+            const int il = env_int("QSIM_JIT_U4IL", 2);  // groups whose chains are emitted interleaved (measured: 2)
+            if (il > 1) {
+                for (int p0 = 0; p0 < kAmpsPerThread / 4; p0 += il) {
+                    s << "  {\n";
+                    std::vector<std::array<int, 4>> gi;
+                    for (int p = p0; p < p0 + il && p < kAmpsPerThread / 4; p++) {
+                        int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
+                        i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
+                        gi.push_back({i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)});
+                    }
+                    for (size_t g = 0; g < gi.size(); g++)
+                        for (int c = 0; c < 4; c++) s << "   const double2 x" << g << "_" << c << " = " << A(gi[g][c]) << ";\n";
+                    for (int c = 0; c < 4; c++)
+                        for (size_t g = 0; g < gi.size(); g++)
+                            for (int r = 0; r < 4; r++) {
+                                const std::string R = "P.m[" + std::to_string(m_idx[o] + r) + "]";
+                                const std::string re = "re" + std::to_string(g) + "_" + std::to_string(r),
+                                                  im = "im" + std::to_string(g) + "_" + std::to_string(r),
+                                                  x = "x" + std::to_string(g) + "_" + std::to_string(c);
+                                if (c == 0)
+                                    s << "   double " << re << " = " << R << "[0] * " << x << ".x, " << im << " = " << R
+                                      << "[0] * " << x << ".y; " << re << " = fma(-" << R << "[1], " << x << ".y, " << re
+                                      << "); " << im << " = fma(" << R << "[1], " << x << ".x, " << im << ");\n";
+                                else
+                                    s << "   " << re << " = fma(" << R << "[" << 2 * c << "], " << x << ".x, " << re << "); "
+                                      << re << " = fma(-" << R << "[" << 2 * c + 1 << "], " << x << ".y, " << re << "); "
+                                      << im << " = fma(" << R << "[" << 2 * c << "], " << x << ".y, " << im << "); " << im
+                                      << " = fma(" << R << "[" << 2 * c + 1 << "], " << x << ".x, " << im << ");\n";
+                            }
+                    for (size_t g = 0; g < gi.size(); g++)
+                        for (int r = 0; r < 4; r++)
+                            s << "   " << A(gi[g][r]) << " = make_double2(re" << g << "_" << r << ", im" << g << "_" << r << ");\n";
+                    s << "  }\n";
+                }
+                s << " }\n";
+                continue;
+            }
             for (int p = 0; p < kAmpsPerThread / 4; p++) {
                 int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
                 i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
@@ -619,7 +657,8 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16));
+    put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16) |
+        ((uint64_t)env_int("QSIM_JIT_U4IL", 2) << 20));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
