@@ -279,6 +279,16 @@ JitPass jit_generate(const Step &st)
         s << ";\n";
         flips.clear();
     };
+    bool u4_heavy = false;
+    {
+        double w4 = 0, w2 = 0;
+        for (const KOp &op : st.ops) {
+            if (op.code == OPC_U4) w4 += 16;
+            else if (op.code == OPC_U2) w2 += 8;
+            else if (op.code == OPC_U2R) w2 += 4;
+        }
+        u4_heavy = w4 >= 2 * w2;
+    }
     bool in_run = false;
     size_t run_begin = 0;
     const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
@@ -340,7 +350,10 @@ JitPass jit_generate(const Step &st)
             const int k = op.k, k2 = (int)op.cfg;
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
-            const int il = env_int("QSIM_JIT_U4IL", 2);  // groups whose chains are emitted interleaved (measured: 2)
+            // groups whose chains are emitted interleaved: 2 on passes dominated by
+            // blocks (config 2: -3%), 1 otherwise (register pressure: the chain
+            // circuit's U2-heavy passes ran 6% slower with 2)
+            const int il = env_int("QSIM_JIT_U4IL", u4_heavy ? 2 : 1);
             if (il > 1) {
                 for (int p0 = 0; p0 < kAmpsPerThread / 4; p0 += il) {
                     s << "  {\n";
@@ -658,7 +671,7 @@ std::string jit_key(const Step &st)
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
     put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16) |
-        ((uint64_t)env_int("QSIM_JIT_U4IL", 2) << 20));
+        ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));

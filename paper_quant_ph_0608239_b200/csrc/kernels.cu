@@ -934,23 +934,29 @@ static LPos make_lpos(int K, const int *lpos, uint64_t c, uint64_t *off)
     return L;
 }
 
-// 4 consecutive amplitudes per thread (two 256-bit accesses per side) when
-// the exchanged bits are >= 2: the paired runs are contiguous in both shards
-__global__ void __launch_bounds__(256) k_swap_blocks4(double2 *__restrict__ A, double2 *__restrict__ B,
-                                                      uint64_t n_quads, int K, LPos L, uint64_t offA, uint64_t offB)
+// 2 consecutive amplitudes per thread (one 256-bit access per side; a warp
+// covers 1 KB contiguous) when the exchanged bits are >= 1, two pairs in
+// flight per thread
+__global__ void __launch_bounds__(256) k_swap_blocks2(double2 *__restrict__ A, double2 *__restrict__ B,
+                                                      uint64_t n_pairs, int K, LPos L, uint64_t offA, uint64_t offB)
 {
-    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n_quads;
-         q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t idx = other_index(q << 2, L, K);
-        double2 a0, a1, a2, a3, b0, b1, b2, b3;
-        ld256(A + (idx | offA), a0, a1);
-        ld256(A + (idx | offA) + 2, a2, a3);
-        ld256(B + (idx | offB), b0, b1);
-        ld256(B + (idx | offB) + 2, b2, b3);
-        st256(A + (idx | offA), b0, b1);
-        st256(A + (idx | offA) + 2, b2, b3);
-        st256(B + (idx | offB), a0, a1);
-        st256(B + (idx | offB) + 2, a2, a3);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n_pairs; q += 2 * stride) {
+        const bool two = q + stride < n_pairs;
+        const uint64_t i0 = other_index(q << 1, L, K), i1 = two ? other_index((q + stride) << 1, L, K) : i0;
+        double2 a0, a1, b0, b1, c0, c1, d0, d1;
+        ld256(A + (i0 | offA), a0, a1);
+        ld256(B + (i0 | offB), b0, b1);
+        if (two) {
+            ld256(A + (i1 | offA), c0, c1);
+            ld256(B + (i1 | offB), d0, d1);
+        }
+        st256(A + (i0 | offA), b0, b1);
+        st256(B + (i0 | offB), a0, a1);
+        if (two) {
+            st256(A + (i1 | offA), d0, d1);
+            st256(B + (i1 | offB), c0, c1);
+        }
     }
 }
 
@@ -960,8 +966,8 @@ void launch_swap_blocks(double2 *A, double2 *B, int M, int K, const int *lpos, u
     LPos L = make_lpos(K, lpos, cA, &offA);
     make_lpos(K, lpos, cB, &offB);
     const uint64_t n_other = 1ULL << (M - K);
-    if (K > 0 && L.sorted[0] >= 2 && n_other >= 4) {
-        k_swap_blocks4<<<grid_for(n_other / 4, 256), 256, 0, s>>>(A, B, n_other / 4, K, L, offA, offB);
+    if (K > 0 && L.sorted[0] >= 1 && n_other >= 2) {
+        k_swap_blocks2<<<grid_for(n_other / 2, 256), 256, 0, s>>>(A, B, n_other / 2, K, L, offA, offB);
         return;
     }
     k_swap_blocks<<<grid_for(n_other, 256), 256, 0, s>>>(A, B, n_other, K, L, offA, offB);

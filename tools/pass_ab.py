@@ -11,7 +11,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_quant_ph_0608239_b200 import QSim, pack_gates  # noqa: E402
 from workloads import circuits as C  # noqa: E402
 
-w = C.config2_random()
+wl = os.environ.get("PASS_AB_WORKLOAD", "config2")
+if wl == "config2":
+    w = C.config2_random()
+elif wl.startswith("chain"):  # config-5 family at n qubits, e.g. chain28
+    n = int(wl[5:])
+    w = C.Workload("chain", n, 0, C.random_chain(n, 10, seed=5, sweep=True), {})
+elif wl.startswith("qft"):
+    w = C.qft_basis(int(wl[3:]), 12345)
+else:
+    raise SystemExit("unknown PASS_AB_WORKLOAD " + wl)
 packed = pack_gates(w.gates)
 opts = {}
 for a in sys.argv[1:]:
