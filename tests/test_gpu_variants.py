@@ -1,0 +1,72 @@
+"""GPU checks that need their own process (-m gpu): kernel variants selected
+by environment at library load, and the opt-in paper-scale parity run."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+_RUN = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+from paper_quant_ph_0608239_b200 import QSim
+from workloads import circuits as C
+n, shards, kind = {n}, {shards}, {kind!r}
+gates = C.random_brickwork(n, 40, seed=3) if kind == "brick" else C.random_chain(n, 10, seed=5, sweep=True)
+sim = QSim(n, n_ranks=shards, transport="virtual" if shards > 1 else "local")
+sim.init_basis(0)
+sim.run_circuit(gates)
+nrm = sim.norm()
+o = oracle.Oracle(n)
+o.init_basis(0)
+o.run(gates)
+view = o.psi.view(np.complex128)
+err, chunk = 0.0, 1 << 26
+for first in range(0, 1 << n, chunk):
+    g = sim.get_amplitudes(first, min(chunk, (1 << n) - first))
+    err = max(err, float(np.max(np.abs(g - view[first:first + g.size]))))
+st = sim.stats()
+print(json.dumps({{"n": n, "shards": shards, "gates": len(gates), "max_abs_diff": err, "norm_dev": abs(1 - nrm),
+                  "exchanges": st["exchanges"], "passes": st["passes"]}}))
+'''
+
+
+def _run(n, shards, kind, env=None, timeout=600):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    code = _RUN.format(root=ROOT, n=n, shards=shards, kind=kind)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout,
+                       env={**os.environ, **(env or {})})
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("grid", ["3", ""])
+def test_pipelined_pass_variant(grid):
+    """QSIM_JIT_PIPE=1 (persistent, cp.async-staged, 6-barrier ring; off by
+    default) at 22 qubits with many tiles per CTA (grid capped) and with the
+    full grid (the phase-aliasing race it once had showed up only there)."""
+    env = {"QSIM_JIT_PIPE": "1"}
+    if grid:
+        env["QSIM_PASS_GRID"] = grid
+    d = _run(22, 1, "brick", env)
+    assert d["max_abs_diff"] <= 1e-11 and d["norm_dev"] <= 1e-12
+
+
+@pytest.mark.skipif(not os.environ.get("QSIM_LARGE_PARITY"), reason="opt-in: set QSIM_LARGE_PARITY=<n> (33 takes ~25 min)")
+def test_large_full_state_parity():
+    """SURVEY §8(c)'s proxy for the 36-qubit row: the config-5 family at n
+    qubits on 8 virtual shards vs the oracle at n, amplitude by amplitude
+    (n = 33: 128 GiB on the GPU and in host RAM).  Result recorded in
+    profiles/r1_parity_33q_8shards.json."""
+    n = int(os.environ["QSIM_LARGE_PARITY"])
+    d = _run(n, 8, "chain", timeout=3600)
+    print(json.dumps(d))
+    assert d["max_abs_diff"] <= 1e-11 and d["norm_dev"] <= 1e-12 and d["exchanges"] >= 1
