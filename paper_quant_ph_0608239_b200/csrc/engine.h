@@ -94,8 +94,10 @@ struct PassDesc {
     int32_t n_ops;
     int32_t use_smem;
     int32_t pad;
-    int32_t tp[kTileBits];           // physical position of tile-local bit t
+    int32_t tp[kTileBits];           // physical position of tile-local bit t (load)
     int32_t tile_sorted[kTileBits];  // tp sorted ascending (instance deposit)
+    int32_t tp_out[kTileBits];       // physical position tile-local bit t is stored at (a
+                                     // permutation of tp: the next pass's low qubits)
 };
 
 #ifdef __CUDACC__

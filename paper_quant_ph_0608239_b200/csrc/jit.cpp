@@ -27,10 +27,11 @@ int nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
 int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
 constexpr size_t kOffTpm = 32, kOffTs = kOffTpm + 8 * kTileBits;
+constexpr size_t kOffTpo = (kOffTs + 4 * kTileBits + 7) / 8 * 8;  // natural u64 alignment
 
 struct Layout {
     int n_out = 0, n_m = 0;
-    size_t off_out = (kOffTs + 4 * kTileBits + 7) / 8 * 8, off_m = 0, bytes = 0;  // natural u64 alignment
+    size_t off_out = kOffTpo + 8 * kTileBits, off_m = 0, bytes = 0;
 };
 
 // generator variant (env, for A/B experiments): minimum CTAs per SM.  A
@@ -94,7 +95,7 @@ JitPass jit_generate(const Step &st)
     s << "// minb=" << minb << " pipe=" << pipe << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
          "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
-      << "]; unsigned long long out["
+      << "]; unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
          "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
@@ -112,7 +113,7 @@ JitPass jit_generate(const Step &st)
     const int NT = kPassThreads, ROWS = kTileAmps / 8;
     std::string BAR = "__syncthreads();";
     if (!pipe) {
-        s << "#define TPM P.tpm\n#define TSP P.ts\n";
+        s << "#define TPM P.tpm\n#define TSP P.ts\n#define TPO P.tpo\n";
         s << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb
           << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
         s << " extern __shared__ double2 sm[];\n";
@@ -160,8 +161,10 @@ JitPass jit_generate(const Step &st)
         s << " __shared__ __align__(8) unsigned long long mbar[6];\n";
         // tile bit positions in shared memory: the loop re-reads them after each
         // barrier instead of holding (and spilling) copies in registers
-        s << " __shared__ volatile unsigned long long TPM[" << kTileBits << "];\n __shared__ int TSP[" << kTileBits << "];\n";
-        s << " if (threadIdx.x < " << kTileBits << ") { TPM[threadIdx.x] = P.tpm[threadIdx.x]; TSP[threadIdx.x] = P.ts[threadIdx.x]; }\n";
+        s << " __shared__ volatile unsigned long long TPM[" << kTileBits << "], TPO[" << kTileBits << "];\n __shared__ int TSP["
+          << kTileBits << "];\n";
+        s << " if (threadIdx.x < " << kTileBits << ") { TPM[threadIdx.x] = P.tpm[threadIdx.x]; TPO[threadIdx.x] = P.tpo[threadIdx.x]; "
+             "TSP[threadIdx.x] = P.ts[threadIdx.x]; }\n";
         s << " const int g = threadIdx.x / " << NT << ", tid = threadIdx.x % " << NT << ";\n";
         s << " if (threadIdx.x == 0) {\n"
              "  for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
@@ -194,18 +197,20 @@ JitPass jit_generate(const Step &st)
     int reg[kAmpsPerThread];
     for (int i = 0; i < kAmpsPerThread; i++) reg[i] = i;
     auto A = [&](int i) { return "a" + std::to_string(reg[i]); };
-    auto gaddr = [&](uint64_t c) {
+    // global offsets of a config's lane/warp part and register pair j; tab =
+    // TPM (load positions) or TPO (store positions, the next pass's layout)
+    auto gaddr = [&](uint64_t c, const char *tab = "TPM") {
         std::ostringstream g;
         g << "(unsigned long long)((lane & 3) << 1)";
-        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? TPM[" << nib(c, kLaneNib + j) << "] : 0ULL)";
-        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? TPM[" << nib(c, kWarpNib + j) << "] : 0ULL)";
+        for (int j = 2; j < 5; j++) g << " | (((lane >> " << j << ") & 1) ? " << tab << "[" << nib(c, kLaneNib + j) << "] : 0ULL)";
+        for (int j = 0; j < kWarpBits; j++) g << " | (((warp >> " << j << ") & 1) ? " << tab << "[" << nib(c, kWarpNib + j) << "] : 0ULL)";
         return g.str();
     };
-    auto roff = [&](uint64_t c, int j) {
+    auto roff = [&](uint64_t c, int j, const char *tab = "TPM") {
         std::ostringstream g;
         g << "0ULL";
         for (int b = 0; b < kRegBits - 1; b++)
-            if ((j >> b) & 1) g << " | TPM[" << nib(c, 1 + b) << "]";
+            if ((j >> b) & 1) g << " | " << tab << "[" << nib(c, 1 + b) << "]";
         return g.str();
     };
     auto smem_z = [&](uint64_t c, const char *tag) {
@@ -510,13 +515,13 @@ JitPass jit_generate(const Step &st)
         s << " }\n";
     }
     materialize(1);  // register bit 0 lies inside one 256-bit store
-    s << " {\n  double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
+    s << " {\n  double2 *p = P.st + base + (" << gaddr(cur, "TPO") << ");\n";
     {
         const uint64_t cfs = cur;
-        flip_mask("gf", "unsigned long long", [&](int k) { return "TPM[" + std::to_string(nib(cfs, k)) + "]"; });
+        flip_mask("gf", "unsigned long long", [&](int k) { return "TPO[" + std::to_string(nib(cfs, k)) + "]"; });
     }
     for (int j = 0; j < kAmpsPerThread / 2; j++)
-        s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + ((" << roff(cur, j) << ") ^ gf)), \"d\"("
+        s << "  asm volatile(\"st.global.v4.f64 [%0], {%1,%2,%3,%4};\" :: \"l\"(p + ((" << roff(cur, j, "TPO") << ") ^ gf)), \"d\"("
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
     s << " }\n";
@@ -545,6 +550,8 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
         const uint64_t m = 1ULL << st.pass.tp[t];
         std::memcpy(b + kOffTpm + 8 * t, &m, 8);
         std::memcpy(b + kOffTs + 4 * t, &st.pass.tile_sorted[t], 4);
+        const uint64_t mo = 1ULL << st.pass.tp_out[t];
+        std::memcpy(b + kOffTpo + 8 * t, &mo, 8);
     }
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];

@@ -231,16 +231,17 @@ __device__ __forceinline__ void lds_all(const double2 *sm, double2 (&a)[kAmpsPer
 }
 
 // global offset of the thread's lane/warp part and register-bit parts (load/store configs)
-__device__ __forceinline__ void global_coords(const PassDesc &d, uint64_t c, int lane, int warp, uint64_t &gt,
+// tp: physical position of each tile-local bit (d.tp to load, d.tp_out to store)
+__device__ __forceinline__ void global_coords(const int32_t *tp, uint64_t c, int lane, int warp, uint64_t &gt,
                                               uint64_t (&g)[kRegBits])
 {
-    gt = (uint64_t)((lane & 3) << 1);  // l0 = tile bit 1 = phys 1, l1 = tile bit 2 = phys 2
+    gt = (uint64_t)((lane & 3) << 1);  // lanes 0, 1 hold the tile bits at phys 1, 2
 #pragma unroll
-    for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << d.tp[cfg_nib(c, kLaneNib + j)];
+    for (int j = 2; j < 5; j++) gt |= (uint64_t)((lane >> j) & 1) << tp[cfg_nib(c, kLaneNib + j)];
 #pragma unroll
-    for (int j = 0; j < kWarpBits; j++) gt |= (uint64_t)((warp >> j) & 1) << d.tp[cfg_nib(c, kWarpNib + j)];
+    for (int j = 0; j < kWarpBits; j++) gt |= (uint64_t)((warp >> j) & 1) << tp[cfg_nib(c, kWarpNib + j)];
 #pragma unroll
-    for (int b = 1; b < kRegBits; b++) g[b] = 1ULL << d.tp[cfg_nib(c, b)];  // register bit 0: within a 256-bit access
+    for (int b = 1; b < kRegBits; b++) g[b] = 1ULL << tp[cfg_nib(c, b)];  // register bit 0: within a 256-bit access
 }
 
 // global offset of register pair j (register bits 1.. of the pair index)
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     double2 a[kAmpsPerThread];
     {
         uint64_t gt, g[kRegBits];
-        global_coords(d, cfg, lane, warp, gt, g);
+        global_coords(d.tp, cfg, lane, warp, gt, g);
         const double2 *p = st + base + gt;
 #pragma unroll
         for (int j = 0; j < kAmpsPerThread / 2; j++) ld256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
 
     {
         uint64_t gt, g[kRegBits];
-        global_coords(d, cfg, lane, warp, gt, g);
+        global_coords(d.tp_out, cfg, lane, warp, gt, g);
         double2 *p = st + base + gt;
 #pragma unroll
         for (int j = 0; j < kAmpsPerThread / 2; j++) st256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);

@@ -173,7 +173,9 @@ struct Cfg {
         for (int j = 0; j < kWarpBits; j++) c |= (uint64_t)w[j] << (4 * (kWarpNib + j));
         return c;
     }
-    bool store_ok() const { return r[0] == 0 && l[0] == 1 && l[1] == 2; }
+    // global load/store config: register bit 0 and lanes 0, 1 hold the tile
+    // bits that sit at physical bits 0, 1, 2 (sb) -- 256-bit accesses, whole lines
+    bool store_ok(const int *sb) const { return r[0] == sb[0] && l[0] == sb[1] && l[1] == sb[2]; }
     int role_of(int t, int &j) const
     {
         for (j = 0; j < kRegBits; j++)
@@ -189,18 +191,20 @@ struct Cfg {
 
 // Complete a register set into a config.  Lanes must cover tile-bit residues
 // {0,1,2} mod 3 for conflict-free transposes (kernels.cu swz).
-Cfg make_cfg(const std::vector<int> &reg_in, bool store)
+const int kLoadBits[3] = {0, 1, 2};
+
+Cfg make_cfg(const std::vector<int> &reg_in, bool store, const int *sb = kLoadBits)
 {
     Cfg c;
     std::vector<int> reg = reg_in;
     if (store) {
-        reg.erase(std::remove(reg.begin(), reg.end(), 0), reg.end());
-        reg.insert(reg.begin(), 0);
+        reg.erase(std::remove(reg.begin(), reg.end(), sb[0]), reg.end());
+        reg.insert(reg.begin(), sb[0]);
     }
     bool used[kTileBits] = {false};
     for (int j = 0; j < kRegBits; j++) { c.r[j] = reg[j]; used[reg[j]] = true; }
     std::vector<int> lanes;
-    if (store) { lanes = {1, 2}; used[1] = used[2] = true; }
+    if (store) { lanes = {sb[1], sb[2]}; used[sb[1]] = used[sb[2]] = true; }
     // one lane bit of every missing residue first
     for (int res = 0; res < 3; res++) {
         bool have = false;
@@ -478,7 +482,8 @@ std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_b
 // Schedule the pass ops (dependency-respecting list scheduling that prefers
 // ops whose target is already in registers), insert OPC_TRANS re-layouts,
 // split every predicate over the thread coordinates.
-static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &st, uint64_t &cfg0)
+// sb: tile bits stored at physical bits 0, 1, 2 (the next pass's low qubits)
+static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &st, uint64_t &cfg0, const int *sb)
 {
     const size_t n = pops.size();
     std::vector<std::vector<int>> preds(n);
@@ -498,9 +503,9 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         return p.t2 < 0 || c.role_of(tl_of[p.t2], j) == ROLE_REG;
     };
     // upcoming register bits: targets of ready ops first, then of the rest, in order
-    auto upcoming = [&](bool store, std::vector<int> &reg) {
+    auto upcoming = [&](bool store, std::vector<int> &reg, const int *lb = kLoadBits) {
         reg.clear();
-        if (store) reg.push_back(0);
+        if (store) reg.push_back(lb[0]);
         for (int pass = 0; pass < 2 && reg.size() < (size_t)kRegBits; pass++)
             for (size_t b = 0; b < n && reg.size() < (size_t)kRegBits; b++) {
                 if (done[b] || pops[b].code == OPC_PHASE) continue;
@@ -509,7 +514,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
                 need.push_back(tl(pops[b]));
                 if (pops[b].t2 >= 0) need.push_back(tl_of[pops[b].t2]);
                 bool skip = false;
-                for (int t : need) skip |= store && (t == 1 || t == 2);
+                for (int t : need) skip |= store && (t == lb[1] || t == lb[2]);
                 if (skip) continue;
                 std::vector<int> add;
                 for (int t : need)
@@ -552,16 +557,16 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
                 if (done[b] || pops[b].code == OPC_PHASE) continue;
                 for (int t : {tl(pops[b]), pops[b].t2 >= 0 ? tl_of[pops[b].t2] : -1}) {
                     if (t < 0) continue;
-                    if (t == 1 || t == 2) store_fits = false;
-                    if (t != 0 && std::find(need.begin(), need.end(), t) == need.end()) need.push_back(t);
+                    if (t == sb[1] || t == sb[2]) store_fits = false;
+                    if (t != sb[0] && std::find(need.begin(), need.end(), t) == need.end()) need.push_back(t);
                 }
             }
             if (store_fits && need.size() <= (size_t)kRegBits - 1) {
-                std::vector<int> r{0};
+                std::vector<int> r{sb[0]};
                 for (int t : need) r.push_back(t);
-                for (int t = 3; r.size() < (size_t)kRegBits && t < kTileBits; t++)
-                    if (std::find(r.begin(), r.end(), t) == r.end()) r.push_back(t);
-                cfg = make_cfg(r, true);
+                for (int t = 0; r.size() < (size_t)kRegBits && t < kTileBits; t++)
+                    if (t != sb[1] && t != sb[2] && std::find(r.begin(), r.end(), t) == r.end()) r.push_back(t);
+                cfg = make_cfg(r, true, sb);
             } else {
                 upcoming(false, reg);
                 cfg = make_cfg(reg, false);
@@ -655,14 +660,14 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         }
         a = b == a ? a + 1 : b;
     }
-    if (!cfg.store_ok()) {
+    if (!cfg.store_ok(sb)) {
         std::vector<int> r2;
         for (int k = 0; k < kRegBits; k++)
-            if (cfg.r[k] != 1 && cfg.r[k] != 2) r2.push_back(cfg.r[k]);
-        for (int t = 3; r2.size() < (size_t)kRegBits && t < kTileBits; t++)
-            if (std::find(r2.begin(), r2.end(), t) == r2.end()) r2.push_back(t);
-        if (std::find(r2.begin(), r2.end(), 0) == r2.end()) { r2.insert(r2.begin(), 0); r2.pop_back(); }
-        emit_trans(make_cfg(r2, true));
+            if (cfg.r[k] != sb[1] && cfg.r[k] != sb[2]) r2.push_back(cfg.r[k]);
+        for (int t = 0; r2.size() < (size_t)kRegBits && t < kTileBits; t++)
+            if (t != sb[1] && t != sb[2] && std::find(r2.begin(), r2.end(), t) == r2.end()) r2.push_back(t);
+        if (std::find(r2.begin(), r2.end(), sb[0]) == r2.end()) { r2.insert(r2.begin(), sb[0]); r2.pop_back(); }
+        emit_trans(make_cfg(r2, true, sb));
     }
 }
 
@@ -765,8 +770,43 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     for (int t = 0; t < 3; t++) { d.tp[t] = t; tl_of[t] = t; }
     for (int j = 0; j < kTileBits - 3; j++) { d.tp[3 + j] = order[j]; tl_of[order[j]] = 3 + j; }
     if (opt.block_fusion) fuse_blocks(pops, tl_of);
+    // The next pass's low qubits.  Every tile contains physical bits 0, 1, 2
+    // (whole 128-B lines per warp access), so whatever logical qubits sit
+    // there occupy three of each tile's twelve bits.  The pass stores the
+    // three tile qubits the remaining gates need first at physical bits
+    // 0, 1, 2 (a permutation of the tile's own bit positions, free at the
+    // store), and sigma follows.  Config 2: 34 -> 22 passes.
+    int sb[3] = {0, 1, 2};
+    for (int t = 0; t < kTileBits; t++) d.tp_out[t] = d.tp[t];
+    if (opt.low_remap) {
+        std::vector<int> want;  // logical qubits
+        for (size_t i = first; i < gates.size() && want.size() < 3; i++) {
+            if (done[i]) continue;
+            for (int q = 0; q < n && want.size() < 3; q++)
+                if (((gates[i].qN >> q) & 1) && phys_of[q] < M && tl_of[phys_of[q]] >= 0 &&
+                    std::find(want.begin(), want.end(), q) == want.end())
+                    want.push_back(q);
+        }
+        for (int t = 0; t < 3 && want.size() < 3; t++)
+            if (std::find(want.begin(), want.end(), qubit_at[t]) == want.end()) want.push_back(qubit_at[t]);
+        for (int k = 0; k < 3; k++) sb[k] = tl_of[phys_of[want[k]]];
+        int dest[kTileBits];
+        for (int t = 0; t < kTileBits; t++) dest[t] = d.tp[t];
+        for (int k = 0; k < 3; k++) {
+            int tk = 0;
+            while (dest[tk] != k) tk++;
+            std::swap(dest[sb[k]], dest[tk]);
+        }
+        std::vector<int> was(kTileBits);
+        for (int t = 0; t < kTileBits; t++) was[t] = qubit_at[d.tp[t]];
+        for (int t = 0; t < kTileBits; t++) {
+            d.tp_out[t] = dest[t];
+            qubit_at[dest[t]] = was[t];
+            phys_of[was[t]] = dest[t];
+        }
+    }
     uint64_t cfg0 = 0;
-    lower_pass(pops, tl_of, st, cfg0);
+    lower_pass(pops, tl_of, st, cfg0, sb);
     d.cfg0 = cfg0;
     d.M = M;
     d.n_inst = 1ULL << (M - kTileBits);
@@ -1084,6 +1124,8 @@ std::string plan_to_json(const Planner &P, const std::vector<Step> &steps)
             for (int j = 0; j < kTileBits; j++) o << (j ? "," : "") << st.pass.tile_sorted[j];
             o << "],\"tp\":[";
             for (int j = 0; j < kTileBits; j++) o << (j ? "," : "") << st.pass.tp[j];
+            o << "],\"tp_out\":[";
+            for (int j = 0; j < kTileBits; j++) o << (j ? "," : "") << st.pass.tp_out[j];
             o << "],\"cfg0\":" << st.pass.cfg0 << ",\"ops\":[";
             for (size_t k = 0; k < st.ops.size(); k++) {
                 const KOp &op = st.ops[k];

@@ -80,6 +80,7 @@ struct Step {
 struct PlanOptions {
     bool fusion = true;
     bool block_fusion = true;  // fuse gate clusters on two tile qubits into 4x4 blocks (OPC_U4)
+    bool low_remap = true;     // a pass stores the next pass's first-needed qubits at physical bits 0,1,2
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
 };

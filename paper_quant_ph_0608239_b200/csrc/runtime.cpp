@@ -79,7 +79,7 @@ struct qsim_ctx_s {
     double *d_red = nullptr;
     size_t d_red_cap = 0;
     // options
-    bool fusion = true, timing = false, block_fusion = true;
+    bool fusion = true, timing = false, block_fusion = true, low_remap = true;
     int max_scan = 1 << 30;
     int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
     int global_policy = GP_AUTO;
@@ -635,6 +635,7 @@ static qsim_status flush(qsim_ctx c)
         PlanOptions opt;
         opt.fusion = c->fusion;
         opt.block_fusion = c->block_fusion;
+        opt.low_remap = c->low_remap;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
         c->planner->plan(c->queue, opt, steps);
@@ -1195,6 +1196,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     std::string k(key);
     if (k == "fusion") { c->fusion = value != 0; c->pc.valid = false; }
     else if (k == "block_fusion") { c->block_fusion = value != 0; c->pc.valid = false; }
+    else if (k == "low_remap") { c->low_remap = value != 0; c->pc.valid = false; }
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
@@ -1266,6 +1268,7 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     PlanOptions opt;
     opt.fusion = (fusion & 3) != 0;
     opt.block_fusion = !(fusion & 0x100);
+    opt.low_remap = !(fusion & 0x200);
     opt.global_policy = (fusion >> 4) & 3 ? ((fusion >> 4) & 3) - 1 : GP_AUTO;
     P.plan(recs, opt, steps);
     std::string jit_info;

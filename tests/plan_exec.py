@@ -55,6 +55,21 @@ def _apply_perm(psi, idx, perm, T, cm):
     return new
 
 
+def _store_remap(psi, idx, tp, tp_out):
+    """A pass stores tile bit t at physical bit tp_out[t] (was tp[t]): the
+    amplitude at index i moves to the index with those bits permuted."""
+    if list(tp) == list(tp_out):
+        return psi
+    j = idx.copy()
+    for a, b in zip(tp, tp_out):
+        j &= ~(1 << b)
+    for a, b in zip(tp, tp_out):
+        j |= ((idx >> a) & 1) << b
+    new = np.empty_like(psi)
+    new[j] = psi
+    return new
+
+
 def _swap_bits(idx, a, b):
     ba, bb = (idx >> a) & 1, (idx >> b) & 1
     return idx ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
@@ -78,6 +93,7 @@ def run_plan(js: str, n: int, init_index: int, gates) -> np.ndarray:
                     _apply_u4(psi, idx, op["t"], op["t2"], op["m"])
                     continue
                 _apply(psi, idx, op["code"], op["t"], op["cm"], op["cv"], op["m"])
+            psi = _store_remap(psi, idx, st["tp"], st.get("tp_out", st["tp"]))
         elif ty == "generic":
             _apply(psi, idx, st["code"], st["t"], st["cm"], st["cv"], st["m"])
         elif ty == "phase":

@@ -63,7 +63,7 @@ def _worker(rank, world, port, case, out_q, policy=None):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_quant_ph_0608239_b200 as P
-        from tests.plan_exec import _apply_u4
+        from tests.plan_exec import _apply_u4, _store_remap
         n, init, gates, qs = case()
         plan = json.loads(P.plan_json(n, world, gates, policy=policy))
         G = (world - 1).bit_length()
@@ -83,6 +83,7 @@ def _worker(rank, world, port, case, out_q, policy=None):
                         _apply_u4(shard, np.arange(1 << M, dtype=np.int64), op["t"], op["t2"], op["m"])
                     elif op["code"] not in (4, 6, 8):
                         _apply(shard, full, op["code"], op["t"], op["cm"], op["cv"], op["m"])
+                shard = _store_remap(shard, np.arange(1 << M, dtype=np.int64), st["tp"], st["tp_out"])
             elif ty == "generic":
                 _apply(shard, full, st["code"], st["t"], st["cm"], st["cv"], st["m"])
             elif ty == "phase":
