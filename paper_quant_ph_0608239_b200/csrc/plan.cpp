@@ -671,20 +671,26 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
     }
 }
 
-void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
-                         const PlanOptions &opt, std::vector<Step> &out)
+// The gate-collection loop of a pass (mutates done[], sigma for absorbed SWAP
+// relabels, and fills pops/freeb/in_tile).  pops == nullptr: dry run for the
+// low-qubit look-ahead (counts only).  Returns the number of gates taken.
+static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
+                           const PlanOptions &opt, std::vector<POp> *pops, std::vector<int> &freeb, bool in_tile[64],
+                           std::vector<std::pair<int, int>> *relabels)
 {
-    std::vector<POp> pops;
-    std::vector<int> freeb;
-    bool in_tile[64] = {false};
-    in_tile[0] = in_tile[1] = in_tile[2] = true;
+    const int n = P.n, M = P.M;
+    std::vector<int> &phys_of = P.phys_of;
     const uint64_t all = n >= 64 ? ~0ULL : (bit(n) - 1);
     uint64_t bN = 0, bD = 0;
     int scanned = 0;
-    std::vector<std::pair<int, int>> relabels;
+    size_t taken = 0, npops = 0;
     // each op may need a transpose in front of it: keep the lowered pass within kMaxPassOps
     const size_t max_pops = kMaxPassOps / 2;
-    for (size_t i = first; i < gates.size() && scanned < opt.max_scan && pops.size() + 2 <= max_pops; i++) {
+    auto push = [&](const POp &p) {
+        npops++;
+        if (pops) pops->push_back(p);
+    };
+    for (size_t i = first; i < gates.size() && scanned < opt.max_scan && npops + 2 <= max_pops; i++) {
         if (done[i]) continue;
         scanned++;
         const GateRec &g = gates[i];
@@ -695,8 +701,8 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
             continue;
         }
         if (g.kind == GK_SWAP) {
-            swap_layout(phys_of[g.targets[0]], phys_of[g.targets[1]]);
-            relabels.push_back({g.targets[0], g.targets[1]});
+            P.swap_layout(phys_of[g.targets[0]], phys_of[g.targets[1]]);
+            if (relabels) relabels->push_back({g.targets[0], g.targets[1]});
             done[i] = 1;
             continue;
         }
@@ -712,10 +718,12 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
             p.code = OPC_U4;
             p.t = t0;
             p.t2 = t1;
-            for (int k = 0; k < 32; k++) p.m4[k] = g.u4[k];
+            if (pops)
+                for (int k = 0; k < 32; k++) p.m4[k] = g.u4[k];
             p.gid = g.id;
-            pops.push_back(p);
+            push(p);
             done[i] = 1;
+            taken++;
             continue;
         }
         uint64_t cm = 0;
@@ -728,13 +736,14 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
             p.t = -1;
             if (!(g.u[0] == 1 && g.u[1] == 0)) {
                 p.cm = cm | tb; p.cv = cm; p.m[0] = g.u[0]; p.m[1] = g.u[1];
-                pops.push_back(p);
+                push(p);
             }
             if (!(g.u[6] == 1 && g.u[7] == 0)) {
                 p.cm = cm | tb; p.cv = cm | tb; p.m[0] = g.u[6]; p.m[1] = g.u[7];
-                pops.push_back(p);
+                push(p);
             }
             done[i] = 1;
+            taken++;
             continue;
         }
         int t = phys_of[g.target];
@@ -749,9 +758,22 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
         p.t = t;
         p.cm = p.cv = cm;
         p.gid = g.id;
-        pops.push_back(p);
+        push(p);
         done[i] = 1;
+        taken++;
     }
+    return taken;
+}
+
+void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
+                         const PlanOptions &opt, std::vector<Step> &out)
+{
+    std::vector<POp> pops;
+    std::vector<int> freeb;
+    bool in_tile[64] = {false};
+    in_tile[0] = in_tile[1] = in_tile[2] = true;
+    std::vector<std::pair<int, int>> relabels;
+    collect_pass(*this, gates, done, first, opt, &pops, freeb, in_tile, &relabels);
     // tile: physical bits 0,1,2 + the free bits (first-use order), filled up to 12
     std::vector<int> order;
     for (const POp &p : pops)
@@ -775,35 +797,72 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     // there occupy three of each tile's twelve bits.  The pass stores the
     // three tile qubits the remaining gates need first at physical bits
     // 0, 1, 2 (a permutation of the tile's own bit positions, free at the
-    // store), and sigma follows.  Config 2: 34 -> 22 passes.
+    // store), and sigma follows.  Which three: the triple whose
+    // next pass (a dry run of the collection) takes the most gates, among
+    // the first remap_lookahead tile qubits the remaining gates need.
     int sb[3] = {0, 1, 2};
     for (int t = 0; t < kTileBits; t++) d.tp_out[t] = d.tp[t];
-    if (opt.low_remap) {
-        std::vector<int> want;  // logical qubits
-        for (size_t i = first; i < gates.size() && want.size() < 3; i++) {
-            if (done[i]) continue;
-            for (int q = 0; q < n && want.size() < 3; q++)
-                if (((gates[i].qN >> q) & 1) && phys_of[q] < M && tl_of[phys_of[q]] >= 0 &&
-                    std::find(want.begin(), want.end(), q) == want.end())
-                    want.push_back(q);
-        }
-        for (int t = 0; t < 3 && want.size() < 3; t++)
-            if (std::find(want.begin(), want.end(), qubit_at[t]) == want.end()) want.push_back(qubit_at[t]);
-        for (int k = 0; k < 3; k++) sb[k] = tl_of[phys_of[want[k]]];
+    // store the tile so that logical qubits q3[k] land at physical bit k
+    auto remap_low = [&](Planner &Q, const int q3[3], int *tp_out, int *sbits) {
         int dest[kTileBits];
         for (int t = 0; t < kTileBits; t++) dest[t] = d.tp[t];
         for (int k = 0; k < 3; k++) {
+            sbits[k] = tl_of[Q.phys_of[q3[k]]];
             int tk = 0;
             while (dest[tk] != k) tk++;
-            std::swap(dest[sb[k]], dest[tk]);
+            std::swap(dest[sbits[k]], dest[tk]);
         }
-        std::vector<int> was(kTileBits);
-        for (int t = 0; t < kTileBits; t++) was[t] = qubit_at[d.tp[t]];
+        int was[kTileBits];
+        for (int t = 0; t < kTileBits; t++) was[t] = Q.qubit_at[d.tp[t]];
         for (int t = 0; t < kTileBits; t++) {
-            d.tp_out[t] = dest[t];
-            qubit_at[dest[t]] = was[t];
-            phys_of[was[t]] = dest[t];
+            if (tp_out) tp_out[t] = dest[t];
+            Q.qubit_at[dest[t]] = was[t];
+            Q.phys_of[was[t]] = dest[t];
         }
+    };
+    if (opt.low_remap) {
+        // candidates: tile qubits in the order the remaining gates need them
+        // (non-diagonally), then the current low qubits, then the rest
+        const size_t K = (size_t)std::max(3, opt.remap_lookahead);
+        std::vector<int> cand;
+        auto in_tile_q = [&](int q) { return phys_of[q] < M && tl_of[phys_of[q]] >= 0; };
+        auto add = [&](int q) {
+            if (cand.size() < K && in_tile_q(q) && std::find(cand.begin(), cand.end(), q) == cand.end()) cand.push_back(q);
+        };
+        for (size_t i = first; i < gates.size() && cand.size() < K; i++) {
+            if (done[i]) continue;
+            for (int q = 0; q < n; q++)
+                if ((gates[i].qN >> q) & 1) add(q);
+        }
+        for (int t = 0; t < 3; t++) add(qubit_at[t]);
+        for (int t = 0; t < kTileBits && cand.size() < 3; t++) add(qubit_at[d.tp[t]]);
+        int best[3] = {cand[0], cand[1], cand[2]};
+        size_t next_first = first;
+        while (next_first < gates.size() && done[next_first]) next_first++;
+        if (opt.remap_lookahead > 3 && next_first < gates.size()) {
+            // one-pass look-ahead: the triple whose next pass takes the most gates
+            size_t best_score = 0;
+            bool have = false;
+            for (size_t a = 0; a < cand.size(); a++)
+                for (size_t b = a + 1; b < cand.size(); b++)
+                    for (size_t c = b + 1; c < cand.size(); c++) {
+                        Planner Q = *this;
+                        const int q3[3] = {cand[a], cand[b], cand[c]};
+                        int sbq[3];
+                        remap_low(Q, q3, nullptr, sbq);
+                        std::vector<char> done2 = done;
+                        std::vector<int> fb;
+                        bool it[64] = {false};
+                        it[0] = it[1] = it[2] = true;
+                        const size_t score = collect_pass(Q, gates, done2, next_first, opt, nullptr, fb, it, nullptr);
+                        if (!have || score > best_score) {
+                            best_score = score;
+                            have = true;
+                            for (int k = 0; k < 3; k++) best[k] = q3[k];
+                        }
+                    }
+        }
+        remap_low(*this, best, d.tp_out, sb);
     }
     uint64_t cfg0 = 0;
     lower_pass(pops, tl_of, st, cfg0, sb);

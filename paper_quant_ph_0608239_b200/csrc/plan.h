@@ -81,6 +81,7 @@ struct PlanOptions {
     bool fusion = true;
     bool block_fusion = true;  // fuse gate clusters on two tile qubits into 4x4 blocks (OPC_U4)
     bool low_remap = true;     // a pass stores the next pass's first-needed qubits at physical bits 0,1,2
+    int remap_lookahead = 6;   // candidates searched for those three (<= 3: the first three needed)
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
 };
@@ -109,7 +110,11 @@ private:
     void emit_perm(const GateRec &g, std::vector<Step> &out);
     size_t emit_perm_run(const std::vector<GateRec> &gates, std::vector<char> &done, size_t first,
                          std::vector<Step> &out);
+
+public:
     void swap_layout(int pa, int pb);
+
+private:
     void plan_list(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out);
 };
 

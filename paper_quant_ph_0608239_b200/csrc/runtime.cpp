@@ -80,6 +80,7 @@ struct qsim_ctx_s {
     size_t d_red_cap = 0;
     // options
     bool fusion = true, timing = false, block_fusion = true, low_remap = true;
+    int remap_lookahead = PlanOptions().remap_lookahead;
     int max_scan = 1 << 30;
     int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
     int global_policy = GP_AUTO;
@@ -636,6 +637,7 @@ static qsim_status flush(qsim_ctx c)
         opt.fusion = c->fusion;
         opt.block_fusion = c->block_fusion;
         opt.low_remap = c->low_remap;
+        opt.remap_lookahead = c->remap_lookahead;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
         c->planner->plan(c->queue, opt, steps);
@@ -1197,6 +1199,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     if (k == "fusion") { c->fusion = value != 0; c->pc.valid = false; }
     else if (k == "block_fusion") { c->block_fusion = value != 0; c->pc.valid = false; }
     else if (k == "low_remap") { c->low_remap = value != 0; c->pc.valid = false; }
+    else if (k == "remap_lookahead") { c->remap_lookahead = (int)std::max<int64_t>(0, std::min<int64_t>(value, 24)); c->pc.valid = false; }
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
@@ -1269,8 +1272,11 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     opt.fusion = (fusion & 3) != 0;
     opt.block_fusion = !(fusion & 0x100);
     opt.low_remap = !(fusion & 0x200);
+    if ((fusion >> 12) & 31) opt.remap_lookahead = ((fusion >> 12) & 31) - 1;
     opt.global_policy = (fusion >> 4) & 3 ? ((fusion >> 4) & 3) - 1 : GP_AUTO;
+    const auto tp0 = std::chrono::steady_clock::now();
     P.plan(recs, opt, steps);
+    const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
     std::string jit_info;
     if ((fusion & 3) == 2) {  // also NVRTC-compile the pass-specialised kernels (host-only check)
         std::vector<const Step *> ps;
@@ -1285,7 +1291,7 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
         jit_info = ",\"jit\":{\"ok\":" + std::string(ok ? "true" : "false") + ",\"kernels\":" + std::to_string(nk) +
                    ",\"compile_ms\":" + std::to_string(ms) + ",\"error\":\"" + e + "\"}";
     }
-    std::string js = init + plan_to_json(P, steps) + jit_info + "}";
+    std::string js = init + plan_to_json(P, steps) + jit_info + ",\"plan_ms\":" + std::to_string(plan_ms) + "}";
     if (js.size() + 1 > buf_bytes) return QSIM_ERR_ARG;
     std::memcpy(buf, js.c_str(), js.size() + 1);
     return QSIM_OK;
