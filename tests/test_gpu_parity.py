@@ -431,3 +431,25 @@ def test_nccl_transport_single_rank(P, oracle_mod):
         sim.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_gpu_fuzz(P, oracle_mod, seed):
+    """Random circuits of every gate kind (tests/test_plan_fuzz.py) on the
+    GPU with the planner options varied, against the oracle."""
+    from tests.test_plan_fuzz import random_circuit
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.integers(12, 17))
+    ranks = int([1, 1, 2, 4, 8][rng.integers(0, 5)])
+    gates = random_circuit(n, 80, 5000 + seed)
+    init = int(rng.integers(0, 1 << n))
+    sim = P.QSim(n, n_ranks=ranks, transport="local" if ranks == 1 else "virtual")
+    sim.set_option("block_fusion", seed % 4 != 0)
+    sim.set_option("low_remap", (seed // 2) % 2 == 0)
+    sim.set_option("remap_lookahead", [0, 3, 6][seed % 3])
+    sim.set_option("jit", seed % 5 != 4)
+    if ranks > 1:
+        sim.set_option("global_policy", seed % 3)
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    assert_parity(sim, oracle_run(oracle_mod, n, init, gates), n)
