@@ -433,7 +433,7 @@ def test_nccl_transport_single_rank(P, oracle_mod):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("QSIM_FUZZ_SEEDS", "8"))))
 def test_gpu_fuzz(P, oracle_mod, seed):
     """Random circuits of every gate kind (tests/test_plan_fuzz.py) on the
     GPU with the planner options varied, against the oracle."""
