@@ -717,6 +717,45 @@ __global__ void __launch_bounds__(256) k_expect_chunk(const double2 *__restrict_
     __shared__ double red[32];
     const uint32_t E = 1u << cb;
     const uint64_t c = blockIdx.x;
+    if (cb == 12 && blockDim.x == 256) {
+        // one sweep: thread t holds elements e = 2t + {0,1} + 512 j (j < 8) via
+        // 256-bit loads; bit 0 of e is the pair element, bits 1-8 the thread,
+        // bits 9-11 j.  Per-bit sums of |a|^2 (+ the total) reduced with one
+        // barrier, in a fixed order (deterministic).
+        const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+        const double2 *src = st + (c << 12) + 2 * t;
+        double s[13];
+#pragma unroll
+        for (int b = 0; b < 13; b++) s[b] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            double2 x0, x1;
+            ld256(src + 512 * j, x0, x1);
+            const double p0 = x0.x * x0.x + x0.y * x0.y, p1 = x1.x * x1.x + x1.y * x1.y;
+            s[0] += p1;
+            s[12] += p0 + p1;
+#pragma unroll
+            for (int k = 0; k < 3; k++)
+                if ((j >> k) & 1) s[9 + k] += p0 + p1;
+        }
+#pragma unroll
+        for (int b = 1; b <= 8; b++) s[b] = ((t >> (b - 1)) & 1) ? s[12] : 0.0;
+#pragma unroll
+        for (int b = 0; b < 13; b++)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s[b] += __shfl_xor_sync(FULL, s[b], o);
+        double *ws = v;  // [8 warps][13]
+        if (lane == 0)
+#pragma unroll
+            for (int b = 0; b < 13; b++) ws[w * 13 + b] = s[b];
+        __syncthreads();
+        if (t < 13) {
+            double r = 0.0;
+            for (int k = 0; k < 8; k++) r += ws[k * 13 + t];
+            partial[c * 13 + t] = r;
+        }
+        return;
+    }
     for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
         const double2 x = st[(c << cb) + e];
         v[e] = x.x * x.x + x.y * x.y;
@@ -734,7 +773,6 @@ __global__ void __launch_bounds__(256) k_expect_chunk(const double2 *__restrict_
         if (threadIdx.x == 0) partial[c * (cb + 1) + b] = s;
     }
 }
-
 __global__ void __launch_bounds__(256) k_expect_final(const double *__restrict__ partial, int cb, int M,
                                                       double *__restrict__ out)
 {
