@@ -43,8 +43,13 @@ constexpr int kPassMinBlocks = kRegBits == 4 ? 8192 / kTileAmps : 3;
 constexpr int kPermTileBits = 12;
 constexpr int kPhaseRunMin = 4;             // k_perm tile (targets + low bits)
 constexpr int kPermTileAmps = 1 << kPermTileBits;
-// ops of one pass travel in the kernel parameter block (<= 32 KB on sm_100)
+// ops of one pass travel in the interpreter's kernel parameter block (<= 32 KB
+// on sm_100) up to kMaxPassOps; longer programs are read from global memory.
 constexpr int kMaxPassOps = 240;
+// planner limits per pass: gates (ops before re-layouts) and an estimate of the
+// JIT tier's parameter bytes (matrices, phase angles, out-of-tile predicates)
+constexpr int kMaxPassPops = 480;
+constexpr int kPassParamBudget = 28 * 1024;
 
 enum OpCode : int32_t {
     OPC_U2 = 0,     // general complex 2x2 on register bit k

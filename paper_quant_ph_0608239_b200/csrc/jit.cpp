@@ -43,17 +43,43 @@ int env_int(const char *k, int dflt)
     return v ? atoi(v) : dflt;
 }
 
-Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_idx)
+// Parameter block: out-of-tile predicates (mout, vout) deduplicated by value;
+// matrix rows of 8 doubles: a U2 takes a row, a U4 its row and its 3 OPC_DATA
+// rows; phases share rows (a multiplier takes 2 doubles, an accumulated
+// angle 1), so long phase runs (QFT ladders) fit the 32-KB parameter limit.
+// m_col[o]: first double of op o inside row m_idx[o].
+Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_idx, std::vector<int> &m_col)
 {
     Layout L;
     out_idx.assign(st.ops.size(), -1);
     m_idx.assign(st.ops.size(), -1);
+    m_col.assign(st.ops.size(), 0);
+    std::vector<std::pair<uint64_t, uint64_t>> outs;
+    int acc_row = -1, acc_col = 8, ph_row = -1, ph_col = 8;
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS || op.code == OPC_PHASE_FLUSH) continue;
-        if (op.mout) out_idx[o] = L.n_out++;
-        if (op.code != OPC_XS) m_idx[o] = L.n_m++;
+        if (op.mout) {
+            const std::pair<uint64_t, uint64_t> key{op.mout, op.vout};
+            size_t k = std::find(outs.begin(), outs.end(), key) - outs.begin();
+            if (k == outs.size()) outs.push_back(key);
+            out_idx[o] = (int)k;
+        }
+        if (op.code == OPC_XS) continue;
+        if (op.code == OPC_PHASE_ACC) {
+            if (acc_col >= 8) { acc_row = L.n_m++; acc_col = 0; }
+            m_idx[o] = acc_row;
+            m_col[o] = acc_col++;
+        } else if (op.code == OPC_PHASE) {
+            if (ph_col >= 8) { ph_row = L.n_m++; ph_col = 0; }
+            m_idx[o] = ph_row;
+            m_col[o] = ph_col;
+            ph_col += 2;
+        } else {
+            m_idx[o] = L.n_m++;
+        }
     }
+    L.n_out = (int)outs.size();
     L.off_m = L.off_out + 16 * (size_t)std::max(1, L.n_out);
     L.bytes = (L.off_m + 64 * (size_t)std::max(1, L.n_m) + 15) / 16 * 16;
     return L;
@@ -87,8 +113,8 @@ void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, 
 
 JitPass jit_generate(const Step &st)
 {
-    std::vector<int> out_idx, m_idx;
-    Layout L = layout_of(st, out_idx, m_idx);
+    std::vector<int> out_idx, m_idx, m_col;
+    Layout L = layout_of(st, out_idx, m_idx, m_col);
     std::ostringstream s;
     const int minb = env_int("QSIM_JIT_MINB", kPassMinBlocks);  // CTAs per SM (register cap)
     const bool pipe = jit_pipelined();
@@ -447,7 +473,7 @@ JitPass jit_generate(const Step &st)
         const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
         if (op.code == OPC_PHASE_ACC) {
             s << "  const unsigned long long K = " << (sel ? "tp ? " : "") << "(unsigned long long)__double_as_longlong("
-              << M << "[2])" << (sel ? " : 0ULL" : "") << ";\n";
+              << M << "[" << m_col[o] << "])" << (sel ? " : 0ULL" : "") << ";\n";
             const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
             for (uint32_t T = Z;; T = (T - 1) & Z) {
                 s << "  mo" << (O | T) << (__builtin_popcount(T) & 1 ? " -= K;\n" : " += K;\n");
@@ -457,12 +483,14 @@ JitPass jit_generate(const Step &st)
             for (int i = 0; i < kAmpsPerThread; i++) {
                 if ((i & op.mreg) != op.vreg) continue;
                 const std::string v = A(i);
-                s << "  { const double p1 = -" << M << "[1] * " << v << ".y, p2 = " << M << "[1] * " << v << ".x; ";
+                const std::string F0 = M + "[" + std::to_string(m_col[o]) + "]",
+                                  F1 = M + "[" + std::to_string(m_col[o] + 1) + "]";
+                s << "  { const double p1 = -" << F1 << " * " << v << ".y, p2 = " << F1 << " * " << v << ".x; ";
                 if (sel)
-                    s << "const double nx = fma(" << M << "[0], " << v << ".x, p1), ny = fma(" << M << "[0], " << v
+                    s << "const double nx = fma(" << F0 << ", " << v << ".x, p1), ny = fma(" << F0 << ", " << v
                       << ".y, p2); " << v << ".x = tp ? nx : " << v << ".x; " << v << ".y = tp ? ny : " << v << ".y; }\n";
                 else
-                    s << v << ".x = fma(" << M << "[0], " << v << ".x, p1); " << v << ".y = fma(" << M << "[0], " << v
+                    s << v << ".x = fma(" << F0 << ", " << v << ".x, p1); " << v << ".y = fma(" << F0 << ", " << v
                       << ".y, p2); }\n";
             }
         } else {
@@ -537,8 +565,8 @@ JitPass jit_generate(const Step &st)
 
 void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf)
 {
-    std::vector<int> out_idx, m_idx;
-    Layout L = layout_of(st, out_idx, m_idx);
+    std::vector<int> out_idx, m_idx, m_col;
+    Layout L = layout_of(st, out_idx, m_idx, m_col);
     buf.assign(L.bytes, 0);
     uint8_t *b = buf.data();
     std::memcpy(b + 0, &state, 8);
@@ -560,8 +588,10 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             std::memcpy(b + L.off_out + 16 * out_idx[o] + 8, &op.vout, 8);
         }
         if (m_idx[o] >= 0) {
-            std::memcpy(b + L.off_m + 64 * m_idx[o], op.m, 64);
-            if (op.code == OPC_PHASE_ACC) std::memcpy(b + L.off_m + 64 * m_idx[o] + 16, &op.cfg, 8);  // angle
+            uint8_t *row = b + L.off_m + 64 * m_idx[o];
+            if (op.code == OPC_PHASE_ACC) std::memcpy(row + 8 * m_col[o], &op.cfg, 8);       // angle
+            else if (op.code == OPC_PHASE) std::memcpy(row + 8 * m_col[o], op.m, 16);       // f
+            else std::memcpy(row, op.m, 64);
         }
     }
 }

@@ -260,9 +260,11 @@ struct PassParams {
     KOp ops[CAP];
 };
 
+// gops != nullptr: the op program is in global memory (programs longer than
+// the parameter block holds); otherwise P.ops
 template <int CAP, int MINB>
 __global__ void __launch_bounds__(kPassThreads, MINB)
-    k_pass(const __grid_constant__ PassParams<CAP> P, double2 *__restrict__ st)
+    k_pass(const __grid_constant__ PassParams<CAP> P, double2 *__restrict__ st, const KOp *__restrict__ gops)
 {
     const PassDesc &d = P.d;
     extern __shared__ double2 sm[];
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     }
 
     for (int o = 0; o < d.n_ops; o++) {
-        const KOp &op = P.ops[o];
+        const KOp &op = gops ? gops[o] : P.ops[o];
         const int code = op.code;
         if (code == OPC_TRANS) {
             int zt, zr[kRegBits];
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
         }
         if (code == OPC_PHASE_FLUSH || code == OPC_DATA) continue;
         if (code == OPC_U4) {
-            u4_op(a, &P.ops[o]);
+            u4_op(a, gops ? gops + o : &P.ops[o]);
             o += 3;
             continue;
         }
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
 }
 
 template <int CAP, int MINB>
-static void launch_pass_cap(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s)
+static void launch_pass_cap(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s, const KOp *gops)
 {
     static bool attr = false;
     if (!attr) {
@@ -342,24 +344,26 @@ static void launch_pass_cap(const PassDesc &d, const KOp *ops, double2 *st, cuda
     }
     PassParams<CAP> P;
     P.d = d;
-    for (int i = 0; i < d.n_ops; i++) P.ops[i] = ops[i];
+    if (!gops)
+        for (int i = 0; i < d.n_ops; i++) P.ops[i] = ops[i];
     const int smem = d.use_smem ? kTileAmps * (int)sizeof(double2) : 0;
-    k_pass<CAP, MINB><<<(unsigned)d.n_inst, kPassThreads, smem, s>>>(P, st);
+    k_pass<CAP, MINB><<<(unsigned)d.n_inst, kPassThreads, smem, s>>>(P, st, gops);
 }
 
 template <int MINB>
-static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s)
+static void launch_pass_minb(const PassDesc &d, const KOp *ops, double2 *st, cudaStream_t s, const KOp *gops)
 {
-    if (d.n_ops <= 32) launch_pass_cap<32, MINB>(d, ops, st, s);
-    else if (d.n_ops <= 96) launch_pass_cap<96, MINB>(d, ops, st, s);
-    else launch_pass_cap<kMaxPassOps, MINB>(d, ops, st, s);
+    if (gops) launch_pass_cap<1, MINB>(d, ops, st, s, gops);
+    else if (d.n_ops <= 32) launch_pass_cap<32, MINB>(d, ops, st, s, nullptr);
+    else if (d.n_ops <= 96) launch_pass_cap<96, MINB>(d, ops, st, s, nullptr);
+    else launch_pass_cap<kMaxPassOps, MINB>(d, ops, st, s, nullptr);
 }
 
-void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s)
+void launch_pass(const PassDesc &d, const KOp *ops, double2 *st, int variant, cudaStream_t s, const KOp *gops)
 {
     constexpr int kMinB = kPassMinBlocks;
-    if (variant == 1) launch_pass_minb<kMinB / 2>(d, ops, st, s);
-    else launch_pass_minb<kMinB>(d, ops, st, s);
+    if (variant == 1) launch_pass_minb<kMinB / 2>(d, ops, st, s, gops);
+    else launch_pass_minb<kMinB>(d, ops, st, s, gops);
 }
 
 int pass_regs_per_thread()

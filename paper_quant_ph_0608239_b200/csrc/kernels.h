@@ -22,7 +22,9 @@ struct ProbsDesc {
     int32_t freepos[64]; // chunk-index bit positions that are free
 };
 
-void launch_pass(const PassDesc &d, const KOp *ops /* host */, double2 *st, int variant, cudaStream_t s);
+// gops: the program in device memory (programs longer than kMaxPassOps), else nullptr
+void launch_pass(const PassDesc &d, const KOp *ops /* host */, double2 *st, int variant, cudaStream_t s,
+                 const KOp *gops = nullptr);
 void launch_gate_generic(double2 *st, int M, uint64_t rank_bits, int t, uint64_t cm, uint64_t cv, int code,
                          const double *m, cudaStream_t s);
 void launch_phase_generic(double2 *st, int M, uint64_t rank_bits, uint64_t cm, uint64_t cv, double fr, double fi,

@@ -683,14 +683,17 @@ static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::v
     const uint64_t all = n >= 64 ? ~0ULL : (bit(n) - 1);
     uint64_t bN = 0, bD = 0;
     int scanned = 0;
-    size_t taken = 0, npops = 0;
-    // each op may need a transpose in front of it: keep the lowered pass within kMaxPassOps
-    const size_t max_pops = kMaxPassOps / 2;
+    size_t taken = 0, npops = 0, pbytes = 0;
+    const size_t max_pops = kMaxPassPops;
     auto push = [&](const POp &p) {
         npops++;
+        // parameter bytes the JIT tier will need for it (upper estimate)
+        pbytes += (p.code == OPC_U4 ? 256 : p.code == OPC_PHASE ? 16 : 64) + (p.cm ? 16 : 0);
         if (pops) pops->push_back(p);
     };
-    for (size_t i = first; i < gates.size() && scanned < opt.max_scan && npops + 2 <= max_pops; i++) {
+    for (size_t i = first; i < gates.size() && scanned < opt.max_scan && npops + 2 <= max_pops &&
+                           pbytes + 512 <= (size_t)kPassParamBudget;
+         i++) {
         if (done[i]) continue;
         scanned++;
         const GateRec &g = gates[i];

@@ -65,7 +65,7 @@ struct qsim_ctx_s {
     std::vector<GateRec> queue;
     PlanCache pc;
     bool plan_cache = true;
-    // device program buffers
+    // device program buffers (d_ops: interpreter programs longer than its parameter block)
     KOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
     uint32_t *d_perm = nullptr;
@@ -478,12 +478,30 @@ static qsim_status exec_pairwise(qsim_ctx c, const Step &s)
 // ------------------------------------------------------------ flush
 static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 {
-    size_t nops = 0, nperm = 0;  // pass ops travel in the kernel parameter block
-    for (Step &s : steps)
+    // pass programs travel in the kernel parameter block, except interpreter
+    // programs longer than kMaxPassOps: those are read from global memory
+    size_t nops = 0, nperm = 0;
+    for (Step &s : steps) {
         if (s.type == ST_PERM || s.type == ST_PERMRUN) nperm += s.perm.size();
-    (void)nops;
-    if (nperm == 0) return QSIM_OK;
+        if (s.type == ST_PASS && s.ops.size() > (size_t)kMaxPassOps) nops += s.ops.size();
+    }
     qsim_status st;
+    if (nops) {
+        if ((st = ensure_host(c, c->h_ops, c->h_ops_cap, nops)) != QSIM_OK) return st;
+        if ((st = ensure_dev(c, c->d_ops, c->d_ops_cap, nops)) != QSIM_OK) return st;
+        if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));  // staging reuse
+        size_t q = 0;
+        for (Step &s : steps)
+            if (s.type == ST_PASS && s.ops.size() > (size_t)kMaxPassOps) {
+                std::copy(s.ops.begin(), s.ops.end(), c->h_ops + q);
+                s.t = (int)q;  // program offset
+                q += s.ops.size();
+            }
+        CK(c, cudaMemcpyAsync(c->d_ops, c->h_ops, nops * sizeof(KOp), cudaMemcpyHostToDevice, c->stream));
+        if (!c->upload_done) CK(c, cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
+        CK(c, cudaEventRecord(c->upload_done, c->stream));
+    }
+    if (nperm == 0) return QSIM_OK;
     if ((st = ensure_host(c, c->h_perm, c->h_perm_cap, nperm + 1)) != QSIM_OK) return st;
     if ((st = ensure_dev(c, c->d_perm, c->d_perm_cap, nperm + 1)) != QSIM_OK) return st;
     if (c->upload_done) CK(c, cudaEventSynchronize(c->upload_done));  // staging reuse
@@ -698,7 +716,8 @@ static qsim_status flush(qsim_ctx c)
                 } else {
                     PassDesc d = s.pass;
                     d.rank_bits = rb;
-                    launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream);
+                    launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream,
+                                s.ops.size() > (size_t)kMaxPassOps ? c->d_ops + s.t : nullptr);
                 }
                 LAUNCHED(c);
                 c->stats.passes++;
