@@ -95,10 +95,12 @@ struct PassDesc {
     uint64_t rank_bits;  // rank << M
     uint64_t n_inst;     // 2^(M-12) tile instances
     uint64_t cfg0;       // load config
+    uint64_t init_phys;  // fresh: the physical index of the basis state qsim_init_basis set
     int32_t M;
     int32_t n_ops;
     int32_t use_smem;
-    int32_t pad;
+    int32_t fresh;       // first data step after qsim_init_basis: synthesize the tile, no HBM read,
+                         // and the zero-fill pass is skipped
     int32_t tp[kTileBits];           // physical position of tile-local bit t (load)
     int32_t tile_sorted[kTileBits];  // tp sorted ascending (instance deposit)
     int32_t tp_out[kTileBits];       // physical position tile-local bit t is stored at (a

@@ -26,7 +26,7 @@ namespace {
 int nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
 int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
-constexpr size_t kOffTpm = 32, kOffTs = kOffTpm + 8 * kTileBits;
+constexpr size_t kOffInit = 32, kOffTpm = 40, kOffTs = kOffTpm + 8 * kTileBits;
 constexpr size_t kOffTpo = (kOffTs + 4 * kTileBits + 7) / 8 * 8;  // natural u64 alignment
 
 struct Layout {
@@ -120,7 +120,7 @@ JitPass jit_generate(const Step &st)
     const bool pipe = jit_pipelined();
     s << "// minb=" << minb << " pipe=" << pipe << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
-         "const double2 *ptab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
+         "const double2 *ptab; unsigned long long init_phys; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
@@ -254,7 +254,15 @@ JitPass jit_generate(const Step &st)
         return z;
     };
     uint64_t cur = st.pass.cfg0;
-    if (!pipe) {
+    if (st.pass.fresh) {
+        // first pass after qsim_init_basis: the tile is the basis state (one 1, else 0)
+        s << " {\n  const unsigned long long g0 = P.rank_bits | base | (" << gaddr(cur) << ");\n";
+        for (int j = 0; j < kAmpsPerThread / 2; j++)
+            s << "  { const unsigned long long g = g0 | (" << roff(cur, j) << "); " << A(2 * j)
+              << " = make_double2(g == P.init_phys ? 1.0 : 0.0, 0.0); " << A(2 * j + 1)
+              << " = make_double2((g | 1ULL) == P.init_phys ? 1.0 : 0.0, 0.0); }\n";
+        s << " }\n";
+    } else if (!pipe) {
         s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
         for (int j = 0; j < kAmpsPerThread / 2; j++)
             s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
@@ -574,6 +582,7 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     std::memcpy(b + 16, &st.pass.n_inst, 8);
     const void *tab = jit_phase_table();
     std::memcpy(b + 24, &tab, 8);
+    std::memcpy(b + kOffInit, &st.pass.init_phys, 8);
     for (int t = 0; t < kTileBits; t++) {
         const uint64_t m = 1ULL << st.pass.tp[t];
         std::memcpy(b + kOffTpm + 8 * t, &m, 8);
@@ -594,6 +603,11 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             else std::memcpy(row, op.m, 64);
         }
     }
+}
+
+void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys)
+{
+    if (buf.size() >= kOffInit + 8) std::memcpy(buf.data() + kOffInit, &init_phys, 8);
 }
 
 // e^{2 pi i k / 256}, k < 256 (device, one per process)
@@ -708,6 +722,7 @@ std::string jit_key(const Step &st)
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
     put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16) |
+        ((uint64_t)(st.pass.fresh != 0) << 48) |
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {

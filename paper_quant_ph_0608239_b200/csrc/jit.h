@@ -41,6 +41,8 @@ struct JitPass {
 JitPass jit_generate(const Step &st);
 // Pack the parameter block of a pass for one shard.
 void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf);
+// update the basis-state index a fresh pass (PassDesc::fresh) synthesises
+void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys);
 
 // NVRTC-compile the specialised kernels of `steps` without loading them
 // (host-only check; n = distinct structures)

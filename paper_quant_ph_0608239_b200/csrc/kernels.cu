@@ -280,9 +280,19 @@ __global__ void __launch_bounds__(kPassThreads, MINB)
     {
         uint64_t gt, g[kRegBits];
         global_coords(d.tp, cfg, lane, warp, gt, g);
-        const double2 *p = st + base + gt;
+        if (d.fresh) {  // first pass after qsim_init_basis: the basis state, no read
+            const uint64_t g0 = d.rank_bits | base | gt;
 #pragma unroll
-        for (int j = 0; j < kAmpsPerThread / 2; j++) ld256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);
+            for (int j = 0; j < kAmpsPerThread / 2; j++) {
+                const uint64_t gi = g0 | pair_off(j, g);
+                a[2 * j] = make_double2(gi == d.init_phys ? 1.0 : 0.0, 0.0);
+                a[2 * j + 1] = make_double2((gi | 1ULL) == d.init_phys ? 1.0 : 0.0, 0.0);
+            }
+        } else {
+            const double2 *p = st + base + gt;
+#pragma unroll
+            for (int j = 0; j < kAmpsPerThread / 2; j++) ld256(p + pair_off(j, g), a[2 * j], a[2 * j + 1]);
+        }
     }
 
     for (int o = 0; o < d.n_ops; o++) {

@@ -623,6 +623,7 @@ static qsim_status flush(qsim_ctx c)
     for (size_t i = 0; hit && i < c->queue.size(); i++) hit = same_gate(pc.queue[i], c->queue[i]);
     if (!hit) pc.valid = false;
     const bool with_init = c->init_pending;
+    uint64_t init_phys = 0;
     if (!hit) pc.phys_before = c->planner->phys_of;
     if (c->init_pending) {
         if (hit) {
@@ -632,15 +633,9 @@ static qsim_status flush(qsim_ctx c)
             c->planner->choose_initial_layout(c->queue);
             pc.phys_init = c->planner->phys_of;
         }
-        uint64_t phys = 0;
+        init_phys = 0;
         for (int q = 0; q < c->n; q++)
-            if ((c->init_index >> q) & 1) phys |= 1ULL << c->planner->phys_of[q];
-        const uint64_t owner = phys >> c->M, li = phys & ((1ULL << c->M) - 1);
-        for (int i = 0; i < n_local(c); i++) {
-            const bool mine = (uint64_t)local_ranks(c, i) == owner;
-            launch_init(c->shards[i], 1ULL << c->M, mine ? (int64_t)li : -1, c->stream);
-            LAUNCHED(c);
-        }
+            if ((c->init_index >> q) & 1) init_phys |= 1ULL << c->planner->phys_of[q];
         c->init_pending = false;
         c->initialized = true;
     }
@@ -659,6 +654,15 @@ static qsim_status flush(qsim_ctx c)
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
         c->planner->plan(c->queue, opt, steps);
+        // A plan that starts (after relabels) with a pass right after
+        // qsim_init_basis: that pass synthesises the basis state in registers
+        // instead of reading the shard, and the zero-fill is skipped.
+        if (with_init)
+            for (Step &s : steps) {
+                if (s.type == ST_RELABEL) continue;
+                if (s.type == ST_PASS) s.pass.fresh = 1;
+                break;
+            }
         pc.steps = std::move(steps);
         pc.queue.swap(c->queue);
         c->queue.clear();
@@ -671,6 +675,19 @@ static qsim_status flush(qsim_ctx c)
     c->stats.flushes++;
     c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     std::vector<Step> &steps = pc.steps;
+    if (with_init) {
+        bool fresh = false;
+        for (Step &s : steps)
+            if (s.type == ST_PASS && s.pass.fresh) { s.pass.init_phys = init_phys; fresh = true; break; }
+        if (!fresh) {
+            const uint64_t owner = init_phys >> c->M, li = init_phys & ((1ULL << c->M) - 1);
+            for (int i = 0; i < n_local(c); i++) {
+                const bool mine = (uint64_t)local_ranks(c, i) == owner;
+                launch_init(c->shards[i], 1ULL << c->M, mine ? (int64_t)li : -1, c->stream);
+                LAUNCHED(c);
+            }
+        }
+    }
     qsim_status st = upload_program(c, steps);
     if (st != QSIM_OK) return st;
     std::vector<std::string> &jkeys = pc.jkeys;
@@ -701,6 +718,7 @@ static qsim_status flush(qsim_ctx c)
                     auto &pp = pc.params[si];
                     if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
                     if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
+                    if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
                     size_t sz = pp[i].size();
                     void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                                      CU_LAUNCH_PARAM_END};
