@@ -215,6 +215,7 @@ typedef struct {
     double jit_compile_ms;     /* total NVRTC + module-load time in this process */
     double pass_fp64_slots;    /* algorithmic FP64 FMA-pipe instructions of the launched passes */
     uint64_t plan_cache_hits;  /* flushes that reused a cached plan */
+    uint64_t streamed_steps;   /* plan steps launched while the planner was still running */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);

@@ -44,7 +44,8 @@ class qsim_stats(ctypes.Structure):
                                                             ("jit_kernels", ctypes.c_uint64),
                                                             ("jit_compile_ms", ctypes.c_double),
                                                             ("pass_fp64_slots", ctypes.c_double),
-                                                            ("plan_cache_hits", ctypes.c_uint64)]
+                                                            ("plan_cache_hits", ctypes.c_uint64),
+                                                            ("streamed_steps", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmds.append([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-lineinfo", "-O3", "-std=c++17",
                          "-Xcompiler", "-fPIC", "-Xptxas", "-v", *inc, "-c", src, "-o", obj])
         elif f.endswith(".cpp"):
-            cmds.append(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", *inc,
+            cmds.append(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-Werror=return-type", "-Wno-unused-function", *inc,
                          "-c", src, "-o", obj])
         else:
             continue

@@ -229,12 +229,6 @@ uint64_t nondiag(const POp &p)
     return bit(p.t) | (p.t2 >= 0 ? bit(p.t2) : 0);
 }
 
-bool conflict(const POp &a, const POp &b)
-{
-    const uint64_t Na = nondiag(a), Nb = nondiag(b);
-    return (Na & (Nb | b.cm)) || (a.cm & Nb);
-}
-
 // ------------------------------------------------- two-qubit block fusion
 // On a fused random layer the pass is bound by the FP64 pipe (DESIGN.md
 // §5.2), not by HBM.  A cluster of gates acting only on two qubits {a, b} --
@@ -297,10 +291,10 @@ void embed4(const POp &p, int pa, int pb, cd E[4][4])
 }
 
 // absorb into the cluster seeded at g the ops on `mask` that can move next to it
-std::vector<size_t> cluster(const std::vector<POp> &ops, const std::vector<char> &used, size_t g, uint64_t mask,
-                            bool allow_pairs)
+void cluster(const std::vector<POp> &ops, const std::vector<char> &used, size_t g, uint64_t mask, bool allow_pairs,
+             std::vector<size_t> &got)
 {
-    std::vector<size_t> got{g};
+    got.assign(1, g);
     auto ok = [&](size_t h, uint64_t stopped) {
         const POp &p = ops[h];
         const uint64_t S = qset(p);
@@ -323,7 +317,6 @@ std::vector<size_t> cluster(const std::vector<POp> &ops, const std::vector<char>
         else stopped |= S & mask;
     }
     std::sort(got.begin(), got.end());
-    return got;
 }
 
 // Fuse `ops` in place.  cost[i] = FMA-pipe ops per amplitude of ops[i];
@@ -332,8 +325,10 @@ template <class PairOk>
 void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pair_ok)
 {
     const size_t n = ops.size();
-    std::vector<char> used(n, 0), has_repl(n, 0);
-    std::vector<POp> repl(n);
+    std::vector<char> used(n, 0);
+    std::vector<int> repl_of(n, -1);  // index into repl
+    std::vector<POp> repl;
+    std::vector<size_t> got;
     // two-qubit blocks
     for (size_t g = 0; g < n; g++) {
         const POp &s = ops[g];
@@ -350,7 +345,7 @@ void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pai
         }
         if (!pair_ok(pa) || !pair_ok(pb)) continue;
         const uint64_t mask = bit(pa) | bit(pb);
-        std::vector<size_t> got = cluster(ops, used, g, mask, true);
+        cluster(ops, used, g, mask, true, got);
         double before = 0;
         for (size_t h : got) before += cost[h];
         if (got.size() < 2 || before <= 16 + 2) continue;  // a 4x4 costs 16 + register copies
@@ -359,12 +354,15 @@ void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pai
             for (int q = 0; q < 4; q++) B[r][q] = r == q ? 1 : 0;
         for (size_t h : got) {  // B <- E_h B, in sequence order
             embed4(ops[h], pa, pb, E);
-            for (int r = 0; r < 4; r++)
-                for (int q = 0; q < 4; q++) {
-                    cd acc = 0;
-                    for (int k = 0; k < 4; k++) acc += E[r][k] * B[k][q];
-                    T[r][q] = acc;
+            for (int r = 0; r < 4; r++) {
+                for (int q = 0; q < 4; q++) T[r][q] = 0;
+                for (int k = 0; k < 4; k++) {
+                    const double er = E[r][k].real(), ei = E[r][k].imag();
+                    if (er == 0 && ei == 0) continue;  // embeddings are sparse
+                    for (int q = 0; q < 4; q++)
+                        T[r][q] += cd(er * B[k][q].real() - ei * B[k][q].imag(), er * B[k][q].imag() + ei * B[k][q].real());
                 }
+            }
             for (int r = 0; r < 4; r++)
                 for (int q = 0; q < 4; q++) B[r][q] = T[r][q];
         }
@@ -380,14 +378,14 @@ void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pai
                 u.m4[8 * r + 2 * q + 1] = B[r][q].imag();
             }
         for (size_t h : got) used[h] = 1;
-        repl[g] = u;
-        has_repl[g] = 1;
+        repl_of[g] = (int)repl.size();
+        repl.push_back(u);
     }
     // runs of one-qubit gates on one qubit
     for (size_t g = 0; g < n; g++) {
         const POp &s = ops[g];
         if (used[g] || s.code == OPC_PHASE || s.code == OPC_U4 || s.code == OP_BARRIER || s.cm) continue;
-        std::vector<size_t> got = cluster(ops, used, g, bit(s.t), false);
+        cluster(ops, used, g, bit(s.t), false, got);
         if (got.size() < 2) continue;
         cd U[2][2] = {{1, 0}, {0, 1}};
         double before = 0;
@@ -414,12 +412,14 @@ void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pai
         u.code = xs ? OPC_XS : real ? OPC_U2R : OPC_U2;
         if (op_cost(u) >= before) continue;
         for (size_t h : got) used[h] = 1;
-        repl[g] = u;
-        has_repl[g] = 1;
+        repl_of[g] = (int)repl.size();
+        repl.push_back(u);
     }
+    if (repl.empty()) return;
     std::vector<POp> out;
+    out.reserve(n);
     for (size_t g = 0; g < n; g++) {
-        if (has_repl[g]) out.push_back(repl[g]);
+        if (repl_of[g] >= 0) out.push_back(repl[repl_of[g]]);
         else if (!used[g]) out.push_back(ops[g]);
     }
     ops.swap(out);
@@ -486,15 +486,43 @@ std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_b
 static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &st, uint64_t &cfg0, const int *sb)
 {
     const size_t n = pops.size();
-    std::vector<std::vector<int>> preds(n);
-    for (size_t b = 0; b < n; b++)
-        for (size_t a = 0; a < b; a++)
-            if (conflict(pops[a], pops[b])) preds[b].push_back((int)a);
+    // Dependencies: a and b conflict when one acts non-diagonally on a qubit the
+    // other touches (target or control).  Reduced per qubit: an op non-diagonal
+    // on q waits for the last op non-diagonal on q and for the diagonal uses of
+    // q since; a diagonal use waits for the last non-diagonal op.  Same partial
+    // order as every conflicting pair, O(ops x qubits per op).
+    std::vector<int> npred(n, 0);
+    std::vector<std::vector<int>> succ(n);
+    {
+        std::vector<int> last_nd(64, -1);
+        std::vector<std::vector<int>> diag_since(64);
+        std::vector<int> dep;
+        for (size_t b = 0; b < n; b++) {
+            const uint64_t N = nondiag(pops[b]), D = pops[b].cm & ~N;
+            dep.clear();
+            for (uint64_t m = N; m; m &= m - 1) {
+                const int q = __builtin_ctzll(m);
+                if (last_nd[q] >= 0) dep.push_back(last_nd[q]);
+                dep.insert(dep.end(), diag_since[q].begin(), diag_since[q].end());
+                last_nd[q] = (int)b;
+                diag_since[q].clear();
+            }
+            for (uint64_t m = D; m; m &= m - 1) {
+                const int q = __builtin_ctzll(m);
+                if (last_nd[q] >= 0) dep.push_back(last_nd[q]);
+                diag_since[q].push_back((int)b);
+            }
+            std::sort(dep.begin(), dep.end());
+            dep.erase(std::unique(dep.begin(), dep.end()), dep.end());
+            for (int a : dep) succ[a].push_back((int)b);
+            npred[b] = (int)dep.size();
+        }
+    }
     std::vector<char> done(n, 0);
-    auto ready = [&](size_t b) {
-        for (int a : preds[b])
-            if (!done[a]) return false;
-        return true;
+    auto ready = [&](size_t b) { return npred[b] == 0; };
+    auto finish = [&](size_t b) {
+        done[b] = 1;
+        for (int c : succ[b]) npred[c]--;
     };
     auto tl = [&](const POp &p) { return tl_of[p.t]; };
     auto in_regs = [&](const Cfg &c, const POp &p) {
@@ -510,17 +538,16 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
             for (size_t b = 0; b < n && reg.size() < (size_t)kRegBits; b++) {
                 if (done[b] || pops[b].code == OPC_PHASE) continue;
                 if ((pass == 0) != ready(b)) continue;
-                std::vector<int> need;
-                need.push_back(tl(pops[b]));
-                if (pops[b].t2 >= 0) need.push_back(tl_of[pops[b].t2]);
+                const int need[2] = {tl(pops[b]), pops[b].t2 >= 0 ? tl_of[pops[b].t2] : -1};
+                const int nn = need[1] >= 0 ? 2 : 1;
                 bool skip = false;
-                for (int t : need) skip |= store && (t == lb[1] || t == lb[2]);
+                for (int i = 0; i < nn; i++) skip |= store && (need[i] == lb[1] || need[i] == lb[2]);
                 if (skip) continue;
-                std::vector<int> add;
-                for (int t : need)
-                    if (std::find(reg.begin(), reg.end(), t) == reg.end()) add.push_back(t);
-                if (reg.size() + add.size() > (size_t)kRegBits) continue;  // a block needs both of its bits at once
-                for (int t : add) reg.push_back(t);
+                int add[2], na = 0;
+                for (int i = 0; i < nn; i++)
+                    if (std::find(reg.begin(), reg.end(), need[i]) == reg.end()) add[na++] = need[i];
+                if (reg.size() + na > (size_t)kRegBits) continue;  // a block needs both of its bits at once
+                for (int i = 0; i < na; i++) reg.push_back(add[i]);
             }
         for (int t = 3; reg.size() < (size_t)kRegBits && t < kTileBits; t++)
             if (std::find(reg.begin(), reg.end(), t) == reg.end()) reg.push_back(t);
@@ -610,7 +637,7 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
                 st.op_cm.push_back(0);
                 st.op_cv.push_back(0);
             }
-            done[pick] = 1;
+            finish(pick);
             left--;
             continue;
         }
@@ -630,13 +657,17 @@ static void lower_pass(const std::vector<POp> &pops, const int tl_of[64], Step &
         st.op_t2.push_back(-1);
         st.op_cm.push_back(p.cm);
         st.op_cv.push_back(p.cv);
-        done[pick] = 1;
+        finish(pick);
         left--;
     }
     // mark runs of consecutive phases for angle accumulation (JIT tier)
     for (size_t a = 0; a < st.ops.size();) {
         size_t b = a;
         while (b < st.ops.size() && st.ops[b].code == OPC_PHASE) b++;
+        if (b - a < (size_t)kPhaseRunMin) {
+            a = b == a ? a + 1 : b;
+            continue;
+        }
         const PhaseRunPlan pr = plan_phase_run(st.ops.data() + a, b - a);
         const double direct = pr.direct, acc = pr.acc;
         if (b - a >= (size_t)kPhaseRunMin && acc < 0.8 * direct) {
@@ -685,11 +716,11 @@ static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::v
     int scanned = 0;
     size_t taken = 0, npops = 0, pbytes = 0;
     const size_t max_pops = kMaxPassPops;
-    auto push = [&](const POp &p) {
+    // count an op (a dry run builds no POp)
+    auto account = [&](int code, uint64_t cm) {
         npops++;
         // parameter bytes the JIT tier will need for it (upper estimate)
-        pbytes += (p.code == OPC_U4 ? 256 : p.code == OPC_PHASE ? 16 : 64) + (p.cm ? 16 : 0);
-        if (pops) pops->push_back(p);
+        pbytes += (code == OPC_U4 ? 256 : code == OPC_PHASE ? 16 : 64) + (cm ? 16 : 0);
     };
     for (size_t i = first; i < gates.size() && scanned < opt.max_scan && npops + 2 <= max_pops &&
                            pbytes + 512 <= (size_t)kPassParamBudget;
@@ -717,14 +748,16 @@ static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::v
             if ((int)freeb.size() + extra > kTileBits - 3) { block(); continue; }
             for (int t : {t0, t1})
                 if (!in_tile[t]) { in_tile[t] = true; freeb.push_back(t); }
-            POp p{};
-            p.code = OPC_U4;
-            p.t = t0;
-            p.t2 = t1;
-            if (pops)
+            account(OPC_U4, 0);
+            if (pops) {
+                POp p{};
+                p.code = OPC_U4;
+                p.t = t0;
+                p.t2 = t1;
                 for (int k = 0; k < 32; k++) p.m4[k] = g.u4[k];
-            p.gid = g.id;
-            push(p);
+                p.gid = g.id;
+                pops->push_back(p);
+            }
             done[i] = 1;
             taken++;
             continue;
@@ -733,17 +766,17 @@ static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::v
         for (int c : g.controls) cm |= bit(phys_of[c]);
         if (g.cls == CLS_DIAG) {
             uint64_t tb = bit(phys_of[g.target]);
-            POp p{};
-            p.code = OPC_PHASE;
-            p.gid = g.id;
-            p.t = -1;
-            if (!(g.u[0] == 1 && g.u[1] == 0)) {
-                p.cm = cm | tb; p.cv = cm; p.m[0] = g.u[0]; p.m[1] = g.u[1];
-                push(p);
-            }
-            if (!(g.u[6] == 1 && g.u[7] == 0)) {
-                p.cm = cm | tb; p.cv = cm | tb; p.m[0] = g.u[6]; p.m[1] = g.u[7];
-                push(p);
+            for (int side = 0; side < 2; side++) {
+                const double fr = g.u[side ? 6 : 0], fi = g.u[side ? 7 : 1];
+                if (fr == 1 && fi == 0) continue;
+                account(OPC_PHASE, cm | tb);
+                if (!pops) continue;
+                POp p{};
+                p.code = OPC_PHASE;
+                p.gid = g.id;
+                p.t = -1;
+                p.cm = cm | tb; p.cv = cm | (side ? tb : 0); p.m[0] = fr; p.m[1] = fi;
+                pops->push_back(p);
             }
             done[i] = 1;
             taken++;
@@ -756,12 +789,15 @@ static size_t collect_pass(Planner &P, const std::vector<GateRec> &gates, std::v
             in_tile[t] = true;
             freeb.push_back(t);
         }
-        POp p{};
-        set_u2_code(g, p);
-        p.t = t;
-        p.cm = p.cv = cm;
-        p.gid = g.id;
-        push(p);
+        account(OPC_U2, cm);
+        if (pops) {
+            POp p{};
+            set_u2_code(g, p);
+            p.t = t;
+            p.cm = p.cv = cm;
+            p.gid = g.id;
+            pops->push_back(p);
+        }
         done[i] = 1;
         taken++;
     }
@@ -1104,15 +1140,18 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
     // nonlocal qubit (more exchanges); plan both ways (the second keeps the
     // pass-local fusion of build_pass) and keep the cheaper by the cost model.
     const Planner start = *this;
+    PlanOptions o2 = opt;
+    o2.sink = nullptr;  // neither list is final until both are costed
     std::vector<Step> a, b;
-    plan_list(blocked, opt, a);
+    plan_list(blocked, o2, a);
     const Planner after_a = *this;
     *this = start;
-    plan_list(user_gates, opt, b);
+    plan_list(user_gates, o2, b);
     const bool take_a = plan_cost(a, M) <= plan_cost(b, M);
     if (take_a) *this = after_a;
     std::vector<Step> &pick = take_a ? a : b;
     for (Step &s : pick) out.push_back(std::move(s));
+    if (opt.sink) opt.sink(out);
 }
 
 void Planner::plan_list(const std::vector<GateRec> &gates, const PlanOptions &opt, std::vector<Step> &out)
@@ -1121,6 +1160,7 @@ void Planner::plan_list(const std::vector<GateRec> &gates, const PlanOptions &op
     std::vector<char> done(gates.size(), 0);
     size_t first = 0;
     while (true) {
+        if (opt.sink) opt.sink(out);
         while (first < gates.size() && done[first]) first++;
         if (first >= gates.size()) break;
         const GateRec &g = gates[first];

@@ -2,6 +2,7 @@
 // planner.  Pure C++, no CUDA.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -84,6 +85,10 @@ struct PlanOptions {
     int remap_lookahead = 6;   // candidates searched for those three (<= 3: the first three needed)
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
+    // called with the step list each time the planner has appended finished
+    // steps (earlier steps never change again): the runtime launches them
+    // while planning continues
+    std::function<void(std::vector<Step> &)> sink;
 };
 
 class Planner {

@@ -611,6 +611,93 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     return QSIM_OK;
 }
 
+// Launch step si of the plan (its uploads done, its JIT kernel compiled).
+static qsim_status exec_step(qsim_ctx c, size_t si)
+{
+    PlanCache &pc = c->pc;
+    const Step &s = pc.steps[si];
+    const int M = c->M;
+    qsim_status st;
+    switch (s.type) {
+    case ST_PASS: {
+        RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
+        CUfunction fn = c->jit ? jit_cache().find(pc.jkeys[si]) : nullptr;
+        for (int i = 0; i < n_local(c); i++) {
+            const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
+            if (fn) {
+                auto &pp = pc.params[si];
+                if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
+                if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
+                if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
+                size_t sz = pp[i].size();
+                void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
+                                 CU_LAUNCH_PARAM_END};
+                unsigned grid, block, smem;
+                jit_launch_dims(s, c->n_sm, grid, block, smem);
+                CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)c->stream, nullptr,
+                                                 extra);
+                if (cr != CUDA_SUCCESS) {
+                    c->poisoned = true;
+                    FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
+                }
+                c->stats.jit_launches++;
+            } else {
+                PassDesc d = s.pass;
+                d.rank_bits = rb;
+                launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream,
+                            s.ops.size() > (size_t)kMaxPassOps ? c->d_ops + s.t : nullptr);
+            }
+            LAUNCHED(c);
+            c->stats.passes++;
+            c->stats.pass_fp64_slots += pass_fp64_slots(s, M);
+        }
+        break;
+    }
+    case ST_GENERIC:
+    case ST_PHASE: {
+        RangeGuard rg(c, 1, 0);
+        for (int i = 0; i < n_local(c); i++) {
+            const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
+            if (s.type == ST_GENERIC)
+                launch_gate_generic(c->shards[i], M, rb, s.t, s.cm, s.cv, s.code, s.m, c->stream);
+            else
+                launch_phase_generic(c->shards[i], M, rb, s.cm, s.cv, s.m[0], s.m[1], c->stream);
+            LAUNCHED(c);
+            c->stats.generic_launches++;
+        }
+        break;
+    }
+    case ST_PERM:
+        if ((st = exec_perm(c, s)) != QSIM_OK) return st;
+        break;
+    case ST_PERMRUN:
+        if ((st = exec_perm_run(c, s)) != QSIM_OK) return st;
+        break;
+    case ST_EXCHANGE:
+        if ((st = exec_exchange(c, s)) != QSIM_OK) return st;
+        break;
+    case ST_RELABEL:
+        c->stats.relabels++;
+        break;
+    case ST_PAIRWISE:
+        if ((st = exec_pairwise(c, s)) != QSIM_OK) return st;
+        break;
+    }
+    return QSIM_OK;
+}
+
+// Whether step s can launch with nothing uploaded or compiled first: no
+// permutation tables, no interpreter program in global memory, and (JIT
+// tier) its kernel already in the cache.  key: the JIT key of a pass.
+static bool launchable_now(qsim_ctx c, const Step &s, std::string &key)
+{
+    if (s.type == ST_PERM || s.type == ST_PERMRUN) return false;
+    if (s.type != ST_PASS) return true;
+    if (!c->jit) return s.ops.size() <= (size_t)kMaxPassOps;
+    key = jit_key(s);
+    return jit_cache().find(key) != nullptr;
+}
+
 static qsim_status flush(qsim_ctx c)
 {
     if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
@@ -621,10 +708,12 @@ static qsim_status flush(qsim_ctx c)
     bool hit = c->plan_cache && pc.valid && pc.with_init == c->init_pending && pc.queue.size() == c->queue.size() &&
                (c->init_pending || pc.phys_before == c->planner->phys_of);
     for (size_t i = 0; hit && i < c->queue.size(); i++) hit = same_gate(pc.queue[i], c->queue[i]);
-    if (!hit) pc.valid = false;
     const bool with_init = c->init_pending;
     uint64_t init_phys = 0;
-    if (!hit) pc.phys_before = c->planner->phys_of;
+    if (!hit) {
+        pc.valid = false;
+        pc.phys_before = c->planner->phys_of;
+    }
     if (c->init_pending) {
         if (hit) {
             c->planner->phys_of = pc.phys_init;
@@ -639,13 +728,56 @@ static qsim_status flush(qsim_ctx c)
         c->init_pending = false;
         c->initialized = true;
     }
+    std::vector<Step> &steps = pc.steps;
+    // After qsim_init_basis: a plan that starts (after relabels) with a pass
+    // synthesises the basis state in that pass's registers instead of reading
+    // the shard, and the zero-fill is skipped; otherwise the init kernel runs
+    // before the first data step.
+    bool init_left = with_init;
+    auto mark_fresh = [&](size_t from) {
+        if (!init_left) return;
+        for (size_t i = from; i < steps.size(); i++) {
+            if (steps[i].type == ST_RELABEL) continue;
+            if (steps[i].type == ST_PASS) { steps[i].pass.fresh = 1; steps[i].pass.init_phys = init_phys; }
+            return;
+        }
+    };
+    auto launch_init_all = [&]() -> qsim_status {
+        init_left = false;
+        const uint64_t owner = init_phys >> c->M, li = init_phys & ((1ULL << c->M) - 1);
+        for (int k = 0; k < n_local(c); k++) {
+            const bool mine = (uint64_t)local_ranks(c, k) == owner;
+            launch_init(c->shards[k], 1ULL << c->M, mine ? (int64_t)li : -1, c->stream);
+            LAUNCHED(c);
+        }
+        return QSIM_OK;
+    };
+    auto launch_one = [&](size_t i) -> qsim_status {
+        if (init_left && steps[i].type != ST_RELABEL) {
+            if (steps[i].type == ST_PASS && steps[i].pass.fresh) init_left = false;
+            else if (qsim_status e = launch_init_all()) return e;
+        }
+        return exec_step(c, i);
+    };
+    size_t next = 0;  // first step not launched yet
     if (hit) {
         c->planner->phys_of = pc.phys_after;
         for (int q = 0; q < c->n; q++) c->planner->qubit_at[pc.phys_after[q]] = q;
         c->queue.clear();
         c->stats.plan_cache_hits++;
+        c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     } else {
-        std::vector<Step> steps;
+        // Plan, launching each step as soon as the planner emits it when it
+        // needs nothing uploaded or compiled: the device runs the first
+        // passes while the host plans the rest.  The first step that needs an
+        // upload or a new JIT kernel ends the streaming; the rest of the plan
+        // then goes the batch way below (one upload, parallel NVRTC).
+        steps.clear();
+        pc.jkeys.clear();
+        pc.params.clear();
+        bool streaming = true;
+        qsim_status err = QSIM_OK;
+        double launch_ms = 0;
         PlanOptions opt;
         opt.fusion = c->fusion;
         opt.block_fusion = c->block_fusion;
@@ -653,128 +785,56 @@ static qsim_status flush(qsim_ctx c)
         opt.remap_lookahead = c->remap_lookahead;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
-        c->planner->plan(c->queue, opt, steps);
-        // A plan that starts (after relabels) with a pass right after
-        // qsim_init_basis: that pass synthesises the basis state in registers
-        // instead of reading the shard, and the zero-fill is skipped.
-        if (with_init)
-            for (Step &s : steps) {
-                if (s.type == ST_RELABEL) continue;
-                if (s.type == ST_PASS) s.pass.fresh = 1;
-                break;
+        opt.sink = [&](std::vector<Step> &out) {
+            if (!streaming || err != QSIM_OK) return;
+            const auto tl = std::chrono::steady_clock::now();
+            for (; next < out.size(); next++) {
+                mark_fresh(next);
+                std::string key;
+                if (!launchable_now(c, out[next], key)) { streaming = false; break; }
+                if (pc.jkeys.size() < out.size()) { pc.jkeys.resize(out.size()); pc.params.resize(out.size()); }
+                pc.jkeys[next] = key;
+                if ((err = launch_one(next)) != QSIM_OK) break;
             }
-        pc.steps = std::move(steps);
+            launch_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+        };
+        c->planner->plan(c->queue, opt, steps);
         pc.queue.swap(c->queue);
         c->queue.clear();
         pc.with_init = with_init;
         pc.phys_after = c->planner->phys_of;
-        pc.jkeys.assign(pc.steps.size(), std::string());
-        pc.params.assign(pc.steps.size(), {});
+        c->stats.plan_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() - launch_ms;
+        if (err != QSIM_OK) return err;
+        pc.jkeys.resize(steps.size());
+        pc.params.resize(steps.size());
         pc.valid = true;
+        c->stats.streamed_steps += next;
     }
     c->stats.flushes++;
-    c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    std::vector<Step> &steps = pc.steps;
-    if (with_init) {
-        bool fresh = false;
-        for (Step &s : steps)
-            if (s.type == ST_PASS && s.pass.fresh) { s.pass.init_phys = init_phys; fresh = true; break; }
-        if (!fresh) {
-            const uint64_t owner = init_phys >> c->M, li = init_phys & ((1ULL << c->M) - 1);
-            for (int i = 0; i < n_local(c); i++) {
-                const bool mine = (uint64_t)local_ranks(c, i) == owner;
-                launch_init(c->shards[i], 1ULL << c->M, mine ? (int64_t)li : -1, c->stream);
-                LAUNCHED(c);
-            }
-        }
+    if (next == steps.size()) {
+        return init_left ? launch_init_all() : QSIM_OK;  // no data step (only relabels, or no gates)
     }
+    mark_fresh(next);
     qsim_status st = upload_program(c, steps);
     if (st != QSIM_OK) return st;
-    std::vector<std::string> &jkeys = pc.jkeys;
     if (c->jit && !hit) {
         std::vector<const Step *> ps;
-        for (const Step &s : steps)
-            if (s.type == ST_PASS) ps.push_back(&s);
-        std::string err;
+        for (size_t i = next; i < steps.size(); i++)
+            if (steps[i].type == ST_PASS) ps.push_back(&steps[i]);
+        std::string jerr;
         auto tj = std::chrono::steady_clock::now();
-        if (!jit_cache().compile(ps, err)) {
+        if (!jit_cache().compile(ps, jerr)) {
             c->jit = 0;  // keep running on the interpreter tier, but say why
-            c->last_error = err;
+            c->last_error = jerr;
         }
         c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj).count();
-        for (size_t i = 0; i < steps.size(); i++)
-            if (steps[i].type == ST_PASS) jkeys[i] = jit_key(steps[i]);
+        for (size_t i = next; i < steps.size(); i++)
+            if (steps[i].type == ST_PASS) pc.jkeys[i] = jit_key(steps[i]);
     }
-    const int M = c->M;
-    for (size_t si = 0; si < steps.size(); si++) {
-        const Step &s = steps[si];
-        switch (s.type) {
-        case ST_PASS: {
-            RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
-            CUfunction fn = c->jit ? jit_cache().find(jkeys[si]) : nullptr;
-            for (int i = 0; i < n_local(c); i++) {
-                const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
-                if (fn) {
-                    auto &pp = pc.params[si];
-                    if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
-                    if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
-                    if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
-                    size_t sz = pp[i].size();
-                    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
-                                     CU_LAUNCH_PARAM_END};
-                    unsigned grid, block, smem;
-                    jit_launch_dims(s, c->n_sm, grid, block, smem);
-                    CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)c->stream, nullptr,
-                                                     extra);
-                    if (cr != CUDA_SUCCESS) {
-                        c->poisoned = true;
-                        FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
-                    }
-                    c->stats.jit_launches++;
-                } else {
-                    PassDesc d = s.pass;
-                    d.rank_bits = rb;
-                    launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream,
-                                s.ops.size() > (size_t)kMaxPassOps ? c->d_ops + s.t : nullptr);
-                }
-                LAUNCHED(c);
-                c->stats.passes++;
-                c->stats.pass_fp64_slots += pass_fp64_slots(s, M);
-            }
-            break;
-        }
-        case ST_GENERIC:
-        case ST_PHASE: {
-            RangeGuard rg(c, 1, 0);
-            for (int i = 0; i < n_local(c); i++) {
-                const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
-                if (s.type == ST_GENERIC)
-                    launch_gate_generic(c->shards[i], M, rb, s.t, s.cm, s.cv, s.code, s.m, c->stream);
-                else
-                    launch_phase_generic(c->shards[i], M, rb, s.cm, s.cv, s.m[0], s.m[1], c->stream);
-                LAUNCHED(c);
-                c->stats.generic_launches++;
-            }
-            break;
-        }
-        case ST_PERM:
-            if ((st = exec_perm(c, s)) != QSIM_OK) return st;
-            break;
-        case ST_PERMRUN:
-            if ((st = exec_perm_run(c, s)) != QSIM_OK) return st;
-            break;
-        case ST_EXCHANGE:
-            if ((st = exec_exchange(c, s)) != QSIM_OK) return st;
-            break;
-        case ST_RELABEL:
-            c->stats.relabels++;
-            break;
-        case ST_PAIRWISE:
-            if ((st = exec_pairwise(c, s)) != QSIM_OK) return st;
-            break;
-        }
-    }
-    return QSIM_OK;
+    for (size_t i = next; i < steps.size(); i++)
+        if ((st = launch_one(i)) != QSIM_OK) return st;
+    return init_left ? launch_init_all() : QSIM_OK;
 }
 
 // ------------------------------------------------------------ ABI

@@ -161,6 +161,32 @@ def test_perm_run_parity(P, oracle_mod, n, ranks):
     assert_parity(sim, oracle_run(oracle_mod, n, 3, gates), n)
 
 
+@pytest.mark.parametrize("ranks", [1, 4])
+def test_streamed_flush_parity(P, oracle_mod, ranks):
+    """Steps launched while the planner still runs (runtime.cpp flush): with
+    the JIT kernels cached and the plan cache off, the passes before the
+    permutation stream, the rest goes the batch way (upload + launch); both
+    runs, and a third through the plan cache, match the oracle."""
+    n = 16
+    gates = (C.random_brickwork(n, 6, seed=7) + [G.perm_gate((3,), (0, 1, 2), np.array([3, 0, 7, 1, 2, 6, 4, 5], np.uint32))]
+             + C.qft_ladder(list(range(n)), swaps=True) + C.random_brickwork(n, 2, seed=8))
+    ref = oracle_run(oracle_mod, n, 5, gates)
+    sim = P.QSim(n, n_ranks=ranks, transport="virtual" if ranks > 1 else "local")
+    sim.set_option("plan_cache", 0)
+    for rep in range(2):
+        sim.init_basis(5)
+        sim.run_circuit(gates)
+        assert_parity(sim, ref, n)
+    st = sim.stats()
+    assert st["streamed_steps"] > 0 and st["perm_launches"] > 0
+    sim.set_option("plan_cache", 1)
+    for rep in range(2):
+        sim.init_basis(5)
+        sim.run_circuit(gates)
+        assert_parity(sim, ref, n)
+    assert sim.stats()["plan_cache_hits"] >= 1
+
+
 @pytest.mark.parametrize("ranks,n", [(2, 14), (4, 15), (8, 16), (8, 12), (4, 9)])
 def test_every_gate_sharded_virtual(P, oracle_mod, ranks, n):
     gates = kitchen_sink(n, seed=100 + n)
