@@ -328,12 +328,96 @@ JitPass jit_generate(const Step &st)
         }
         u4_heavy = w4 >= 2 * w2;
     }
-    bool in_run = false;
-    size_t run_begin = 0;
+    // Phase runs (OPC_PHASE_ACC): per-thread integer angle accumulators, one
+    // per monomial S of the register bits (plan.h PhaseRunPlan), live across
+    // the whole pass.  Flushed lazily: an op on register bit k first flushes
+    // only the monomials containing k (the others commute with it); a
+    // re-layout and the store flush all.  The planner's OPC_PHASE_FLUSH marks
+    // are not needed here.
+    uint32_t acc_used = 0, live = 0;
+    for (const KOp &op : st.ops)
+        if (op.code == OPC_PHASE_ACC) {
+            const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
+            for (uint32_t T = Z;; T = (T - 1) & Z) {
+                acc_used |= 1u << (O | T);
+                if (!T) break;
+            }
+        }
+    if (acc_used) {
+        s << " unsigned long long";
+        bool first_decl = true;
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+            if ((acc_used >> S) & 1) { s << (first_decl ? " mo" : ", mo") << S << " = 0"; first_decl = false; }
+        s << ";\n";
+    }
+    auto touching = [](uint32_t bits) {  // monomials that contain one of the register bits
+        uint32_t F = 0;
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+            if (S & bits) F |= 1u << S;
+        return F;
+    };
+    auto flush = [&](uint32_t F) {
+        F &= live;
+        if (!F) return;
+        s << " { // flush monomials 0x" << std::hex << F << std::dec << "\n";
+        // e^{i theta_i}, theta_i = sum of acc[S] over S in F, S subset of i: per
+        // distinct register angle (A) or per monomial (B), the cheaper
+        const double kExp = 20, kMul = 4;
+        auto key_of = [&](uint32_t i) {
+            uint32_t key = 0;
+            for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+                if (((F >> S) & 1) && (S & i) == S) key |= 1u << S;
+            return key;
+        };
+        std::vector<uint32_t> keys;
+        int nregs = 0;
+        for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++) {
+            const uint32_t key = key_of(i);
+            if (!key) continue;
+            nregs++;
+            if (std::find(keys.begin(), keys.end(), key) == keys.end()) keys.push_back(key);
+        }
+        const double costA = keys.size() * kExp + nregs * kMul;
+        double costB = 0;
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+            if ((F >> S) & 1) costB += kExp + kMul * (double)(kAmpsPerThread >> __builtin_popcount(S));
+        auto mul = [&](const std::string &e, const std::string &v) {
+            s << "  { const double p1 = -" << e << ".y * " << v << ".y, p2 = " << e << ".y * " << v << ".x; " << v
+              << ".x = fma(" << e << ".x, " << v << ".x, p1); " << v << ".y = fma(" << e << ".x, " << v
+              << ".y, p2); }\n";
+        };
+        if (costB >= costA) {
+            std::vector<char> emitted(keys.size(), 0);
+            for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++) {
+                const uint32_t key = key_of(i);
+                if (!key) continue;
+                const size_t k = std::find(keys.begin(), keys.end(), key) - keys.begin();
+                if (!emitted[k]) {
+                    std::string e;
+                    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+                        if ((key >> S) & 1) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
+                    s << "  const double2 ex" << k << " = qexp(" << e << ", P.ptab);\n";
+                    emitted[k] = 1;
+                }
+                mul("ex" + std::to_string(k), A(i));
+            }
+        } else {
+            for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+                if ((F >> S) & 1) s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n";
+            for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++)
+                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+                    if (((F >> S) & 1) && (S & i) == S) mul("em" + std::to_string(S), A(i));
+        }
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+            if ((F >> S) & 1) s << "  mo" << S << " = 0;\n";
+        s << " }\n";
+        live &= ~F;
+    };
     const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
     for (size_t o = o_first; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
+            flush(live);
             s << " {\n";
             smem_z(cur, "a");
             const uint64_t cfa = cur;
@@ -346,47 +430,12 @@ JitPass jit_generate(const Step &st)
             s << "  " << BAR << "\n }\n";
             continue;
         }
-        if (op.code == OPC_PHASE_FLUSH) {
-            materialize((1u << kRegBits) - 1);
-            const PhaseRunPlan pr = plan_phase_run(st.ops.data() + run_begin, o - run_begin);
-            auto sum_below = [&](uint32_t i) {  // theta_i = sum of acc[S], S subset of i
-                std::string e;
-                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                    if (((pr.used >> S) & 1) && (S & i) == S) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
-                return e;
-            };
-            auto mul = [&](const std::string &e, const std::string &v) {
-                s << "  { const double p1 = -" << e << ".y * " << v << ".y, p2 = " << e << ".y * " << v << ".x; " << v
-                  << ".x = fma(" << e << ".x, " << v << ".x, p1); " << v << ".y = fma(" << e << ".x, " << v
-                  << ".y, p2); }\n";
-            };
-            if (pr.mode == 0) {
-                std::vector<std::string> sums;
-                for (int i = 0; i < kAmpsPerThread; i++) {
-                    const std::string e = sum_below((uint32_t)i);
-                    if (e.empty()) continue;
-                    size_t k = std::find(sums.begin(), sums.end(), e) - sums.begin();
-                    if (k == sums.size()) {
-                        sums.push_back(e);
-                        s << "  const double2 ex" << k << " = qexp(" << e << ", P.ptab);\n";
-                    }
-                    mul("ex" + std::to_string(k), A(i));
-                }
-            } else {
-                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                    if ((pr.used >> S) & 1) s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n";
-                for (int i = 0; i < kAmpsPerThread; i++)
-                    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                        if (((pr.used >> S) & 1) && (S & (uint32_t)i) == S) mul("em" + std::to_string(S), A(i));
-            }
-            s << " }\n";
-            in_run = false;
-            continue;
-        }
+        if (op.code == OPC_PHASE_FLUSH) continue;  // lazy flush (above)
         if (op.code == OPC_DATA) continue;  // rows 1..3 of the preceding OPC_U4
         if (op.code == OPC_U4) {
             // same FMA chains, in the same order, as kernels.cu u4_apply
             const int k = op.k, k2 = (int)op.cfg;
+            flush(touching((1u << k) | (1u << k2)));
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
             // groups whose chains are emitted interleaved: 2 on passes dominated by
@@ -450,18 +499,6 @@ JitPass jit_generate(const Step &st)
             s << " }\n";
             continue;
         }
-        if (op.code == OPC_PHASE_ACC && !in_run) {
-            // open the run scope and declare the monomial accumulators it uses
-            size_t e = o;
-            while (e < st.ops.size() && st.ops[e].code == OPC_PHASE_ACC) e++;
-            const PhaseRunPlan pr = plan_phase_run(st.ops.data() + o, e - o);
-            s << " {";
-            for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                if ((pr.used >> S) & 1) s << " unsigned long long mo" << S << " = 0;";
-            s << "\n";
-            run_begin = o;
-            in_run = true;
-        }
         const bool plw = op.mlane || op.mwarp;  // thread-dependent predicate
         const bool pout = op.mout != 0;         // CTA-uniform predicate
         std::ostringstream pr;
@@ -470,11 +507,13 @@ JitPass jit_generate(const Step &st)
         if (op.mwarp) pr << " && ((warp & " << op.mwarp << ") == " << op.vwarp << ")";
         if (pout) pr << " && ((gcta & P.out[" << out_idx[o] << "][0]) == P.out[" << out_idx[o] << "][1])";
         const bool sel = plw || (pout && op.code == OPC_XS);  // select-based (no branch)
+        const bool is_phase = op.code == OPC_PHASE || op.code == OPC_PHASE_ACC;
+        if (!is_phase) flush(touching(1u << op.k));
         if (op.code == OPC_XS && sel && op.mreg == 0) {  // defer (see Flip)
             flips.push_back({op.k, pr.str()});
             continue;
         }
-        materialize(op.mreg | (op.code == OPC_PHASE || op.code == OPC_PHASE_ACC ? 0u : 1u << op.k));
+        materialize(op.mreg | (is_phase ? 0u : 1u << op.k));
         s << " { // op " << o << " code " << op.code << "\n";
         if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
         if (pout && !sel) s << "  if (tp) {\n";
@@ -485,6 +524,7 @@ JitPass jit_generate(const Step &st)
             const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
             for (uint32_t T = Z;; T = (T - 1) & Z) {
                 s << "  mo" << (O | T) << (__builtin_popcount(T) & 1 ? " -= K;\n" : " += K;\n");
+                live |= 1u << (O | T);
                 if (!T) break;
             }
         } else if (op.code == OPC_PHASE) {
@@ -550,6 +590,7 @@ JitPass jit_generate(const Step &st)
         if (pout && !sel) s << "  }\n";
         s << " }\n";
     }
+    flush(live);
     materialize(1);  // register bit 0 lies inside one 256-bit store
     s << " {\n  double2 *p = P.st + base + (" << gaddr(cur, "TPO") << ");\n";
     {
