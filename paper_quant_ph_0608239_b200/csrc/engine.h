@@ -20,6 +20,7 @@
 // amplitude pairs, whole 128-B lines per 4 lanes).
 // A config is packed in nibbles: r0 .. r(kRegBits-1) l0 .. l4 w0 .. w(kWarpBits-1).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 namespace qsb {
@@ -134,6 +135,13 @@ struct PermDesc {
 // y^(2^j) mod G) applied in one pass (k_perm_run): each element
 // gathers through the inverse tables of the perms whose controls it satisfies.
 constexpr int kMaxPermRun = 32;
+// shared memory of one k_perm_run CTA: two staged tiles (16 B per element),
+// one control mask per extra-bit pattern, R tables of 2^t uint16
+constexpr size_t kPermRunSmemMax = 227 * 1024;
+QSB_HD size_t perm_run_smem_bytes(int tile_bits, int t, int R)
+{
+    return ((size_t)32 << tile_bits) + ((size_t)4 << (tile_bits - t)) + (size_t)R * ((size_t)2 << t);
+}
 struct PermRunDesc {
     uint64_t rank_bits;
     uint64_t n_inst;

@@ -495,14 +495,25 @@ __global__ void __launch_bounds__(256) k_perm(const __grid_constant__ PermDesc d
 // out[x, w] = in[x, P_j1^-1(... P_jk^-1(w))].  Controls are never targets, so
 // the active set depends only on the non-target bits, shared by an element
 // and its source.  Elements no perm touches are neither read nor written.
+// Tiles are double-buffered: the cp.async copies of a CTA's next tile are in
+// flight while it gathers the current one (the gather is a short chain of
+// shared-memory lookups; the HBM latency of the staging was the bound).
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRunDesc d, double2 *__restrict__ st,
                                                   const uint32_t *__restrict__ tabs)
 {
     extern __shared__ __align__(16) unsigned char smraw[];
     const uint32_t E = 1u << d.tile_bits, TT = 1u << d.t, T = TT - 1, NX = E >> d.t;
-    double2 *sm = reinterpret_cast<double2 *>(smraw);
-    uint32_t *xmask = reinterpret_cast<uint32_t *>(smraw + (size_t)E * sizeof(double2));  // NX entries
-    uint16_t *tab = reinterpret_cast<uint16_t *>(xmask + NX);                            // R * TT entries
+    double2 *bufs = reinterpret_cast<double2 *>(smraw);                                        // 2 x E
+    uint32_t *xmask = reinterpret_cast<uint32_t *>(smraw + 2 * (size_t)E * sizeof(double2));  // NX entries
+    uint16_t *tab = reinterpret_cast<uint16_t *>(xmask + NX);                                // R * TT entries
     for (uint32_t i = threadIdx.x; i < (uint32_t)d.R * TT; i += blockDim.x) tab[i] = (uint16_t)__ldg(tabs + d.tab_offset + i);
     // in-tile control predicates of every extra-bit pattern x (tile-local e = x << t | w)
     for (uint32_t x = threadIdx.x; x < NX; x += blockDim.x) {
@@ -512,60 +523,55 @@ __global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRu
         xmask[x] = m;
     }
     __syncthreads();
-    for (uint64_t inst = blockIdx.x; inst < d.n_inst; inst += gridDim.x) {
-        uint64_t base = inst;
-        for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
-        uint32_t A = 0;  // perms whose out-of-tile controls this tile satisfies
-        for (int j = 0; j < d.R; j++)
-            if (((d.rank_bits | base) & d.m_out[j]) == d.v_out[j]) A |= 1u << j;
-        if (!A) continue;  // uniform: no barrier skipped by part of the CTA
-        if (d.contiguous) {
-            const double2 *src = st + base;
-            for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
-                if (!(A & xmask[e >> d.t])) continue;
-                double2 x0, x1;
-                ld256(src + e, x0, x1);
-                sm[e] = x0;
-                sm[e + 1] = x1;
-            }
-        } else {
-            for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
-                if (A & xmask[e >> d.t]) sm[e] = st[base + dep_tile(e, d.tile_pos, d.tile_bits)];
+    // this CTA's next tile (from `inst` on) that some perm touches; CTA-uniform
+    auto next_tile = [&](uint64_t inst, uint64_t &base, uint32_t &A) {
+        for (; inst < d.n_inst; inst += gridDim.x) {
+            base = inst;
+            for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
+            A = 0;  // perms whose out-of-tile controls this tile satisfies
+            for (int j = 0; j < d.R; j++)
+                if (((d.rank_bits | base) & d.m_out[j]) == d.v_out[j]) A |= 1u << j;
+            if (A) break;
         }
+        return inst;
+    };
+    auto stage = [&](double2 *buf, uint64_t base, uint32_t A) {
+        for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
+            if (A & xmask[e >> d.t])
+                cp_async16(buf + e, st + base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits)));
+    };
+    uint64_t base, nbase = 0;
+    uint32_t A, nA = 0;
+    uint64_t inst = next_tile(blockIdx.x, base, A);
+    if (inst < d.n_inst) stage(bufs, base, A);
+    cp_async_commit();
+    for (int b = 0; inst < d.n_inst; b ^= 1) {
+        const uint64_t ninst = next_tile(inst + gridDim.x, nbase, nA);
+        if (ninst < d.n_inst) stage(bufs + (size_t)(b ^ 1) * E, nbase, nA);
+        cp_async_commit();  // (possibly empty) group of the next tile
+        cp_async_wait1();   // this thread's copies of the current tile landed
         __syncthreads();
-        if (d.contiguous && d.t >= 3) {
-            // 8 consecutive elements share the non-target bits: 8 independent
-            // lookup chains per step hide the shared-memory latency
+        const double2 *sm = bufs + (size_t)b * E;
+        if (d.contiguous && d.t >= 2) {
+            // 4 consecutive elements share the non-target bits: 4 independent
+            // lookup chains per thread
             double2 *dst = st + base;
-            for (uint32_t e = 8 * threadIdx.x; e < E; e += 8 * blockDim.x) {
+            for (uint32_t e = 4 * threadIdx.x; e < E; e += 4 * blockDim.x) {
                 uint32_t act = A & xmask[e >> d.t];
                 if (!act) continue;
-                uint32_t w[8];
+                uint32_t w[4];
 #pragma unroll
-                for (int i = 0; i < 8; i++) w[i] = (e + i) & T;
+                for (int i = 0; i < 4; i++) w[i] = (e + i) & T;
                 while (act) {
                     const int j = 31 - __clz(act);  // latest active perm first (inverse order)
                     const uint16_t *tj = tab + j * TT;
 #pragma unroll
-                    for (int i = 0; i < 8; i++) w[i] = tj[w[i]];
+                    for (int i = 0; i < 4; i++) w[i] = tj[w[i]];
                     act &= ~(1u << j);
                 }
-#pragma unroll
-                for (int i = 0; i < 8; i += 2) st256(dst + e + i, sm[(e & ~T) | w[i]], sm[(e & ~T) | w[i + 1]]);
-            }
-        } else if (d.contiguous) {
-            double2 *dst = st + base;
-            for (uint32_t e = 2 * threadIdx.x; e < E; e += 2 * blockDim.x) {
-                const uint32_t act0 = A & xmask[e >> d.t];  // e, e+1 differ in target bit 0 only
-                if (!act0) continue;
-                uint32_t w0 = e & T, w1 = (e + 1) & T, act = act0;
-                while (act) {
-                    const int j = 31 - __clz(act);
-                    w0 = tab[j * TT + w0];
-                    w1 = tab[j * TT + w1];
-                    act &= ~(1u << j);
-                }
-                st256(dst + e, sm[(e & ~T) | w0], sm[((e + 1) & ~T) | w1]);
+                const uint32_t hi = e & ~T;
+                st256(dst + e, sm[hi | w[0]], sm[hi | w[1]]);
+                st256(dst + e + 2, sm[hi | w[2]], sm[hi | w[3]]);
             }
         } else {
             for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
@@ -577,18 +583,17 @@ __global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRu
                     w = tab[j * TT + w];
                     act &= ~(1u << j);
                 }
-                st[base + dep_tile(e, d.tile_pos, d.tile_bits)] = sm[(e & ~T) | w];
+                st[base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits))] = sm[(e & ~T) | w];
             }
         }
-        __syncthreads();
+        __syncthreads();  // the buffer is refilled two tiles on
+        inst = ninst;
+        base = nbase;
+        A = nA;
     }
 }
 
-size_t perm_run_smem(const PermRunDesc &d)
-{
-    const size_t E = (size_t)1 << d.tile_bits;
-    return E * sizeof(double2) + (E >> d.t) * sizeof(uint32_t) + (size_t)d.R * ((size_t)1 << d.t) * sizeof(uint16_t);
-}
+size_t perm_run_smem(const PermRunDesc &d) { return perm_run_smem_bytes(d.tile_bits, d.t, d.R); }
 
 void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab, int n_sm, cudaStream_t s)
 {

@@ -975,10 +975,12 @@ size_t Planner::emit_perm_run(const std::vector<GateRec> &gates, std::vector<cha
 {
     const GateRec &g = gates[first];
     std::vector<size_t> run{first};
+    const int t = (int)g.targets.size();
     for (size_t i = first + 1; i < gates.size() && run.size() < (size_t)kMaxPermRun; i++) {
         if (done[i]) continue;
         const GateRec &h = gates[i];
         if (h.kind != GK_PERM || h.targets != g.targets) break;
+        if (perm_run_smem_bytes(t, t, (int)run.size() + 1) > kPermRunSmemMax) break;  // tables + tiles fit one CTA
         run.push_back(i);
     }
     if (run.size() < 2 || g.targets.size() > 16) {

@@ -530,12 +530,14 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
     const int M = c->M, t = (int)s.ptargets.size();
     // smaller tiles than k_perm's: the run's tables share the shared memory,
     // and more resident CTAs hide the load latency of the gather
-    static const int run_tb = [] { const char *e = getenv("QSIM_PERMRUN_TILE"); return e ? atoi(e) : 10; }();
+    static const int run_tb = [] { const char *e = getenv("QSIM_PERMRUN_TILE"); return e ? atoi(e) : 11; }();
     int tb = std::max(std::min(run_tb, M), t);
+    const int R = (int)s.run_cm.size();
+    while (tb > t && perm_run_smem_bytes(tb, t, R) > kPermRunSmemMax) tb--;
     d.M = M;
     d.t = t;
     d.tile_bits = tb;
-    d.R = (int)s.run_cm.size();
+    d.R = R;
     d.tab_offset = s.t;
     bool used[64] = {false};
     for (int i = 0; i < t; i++) { d.tile_pos[i] = s.ptargets[i]; used[s.ptargets[i]] = true; }
@@ -559,7 +561,7 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
             if (tl >= 0) { d.m_tile[j] |= 1u << tl; d.v_tile[j] |= 1u << tl; }
             else { d.m_out[j] |= 1ULL << b; d.v_out[j] |= 1ULL << b; }
         }
-    if (perm_run_smem(d) > 200 * 1024) FAIL(c, QSIM_ERR_ARG, "permutation run too large for shared memory");
+    if (perm_run_smem(d) > kPermRunSmemMax) FAIL(c, QSIM_ERR_ARG, "permutation run too large for shared memory");
     RangeGuard rg(c, 2, 0);
     for (int i = 0; i < n_local(c); i++) {
         d.rank_bits = (uint64_t)local_ranks(c, i) << M;

@@ -158,6 +158,19 @@ def test_plan_perm_run(pkg, oracle_mod, P):
     assert [len(s["gates"]) for s in d["plan"]["steps"] if s["type"] == "permrun"] == [7]
 
 
+def test_plan_perm_run_fits_shared_memory(pkg, oracle_mod):
+    """A run's R tables of 2^t uint16 and its two staged tiles must fit one
+    CTA's shared memory (engine.h perm_run_smem_bytes): 20 perms on a 12-qubit
+    register split into runs of 12 and 8 (227 KB >= 128 KB + 4 B + R * 8 KB)."""
+    r = np.random.default_rng(9)
+    n, tg = 16, tuple(range(12))
+    gates = [G.one_q(q, G.H) for q in range(12, 16)]
+    for j in range(20):
+        gates.append(G.perm_gate((12 + j % 4,), tg, r.permutation(1 << 12).astype(np.uint32)))
+    d = _check_plan(pkg, oracle_mod, n, 1, 5, gates)
+    assert [len(s["gates"]) for s in d["plan"]["steps"] if s["type"] == "permrun"] == [12, 8]
+
+
 def test_plan_qft_sharded(pkg, oracle_mod):
     w = C.qft_basis(14, 12345)
     d = _check_plan(pkg, oracle_mod, 14, 4, w.init, w.gates)

@@ -161,6 +161,19 @@ def test_perm_run_parity(P, oracle_mod, n, ranks):
     assert_parity(sim, oracle_run(oracle_mod, n, 3, gates), n)
 
 
+def test_perm_run_max_shared_memory(P, oracle_mod):
+    """12-qubit register, 20 controlled perms: runs of 12 and 8 whose tables
+    and double-buffered tiles take up to 224 KB of shared memory per CTA."""
+    r = np.random.default_rng(9)
+    n, tg = 16, tuple(range(12))
+    gates = [G.one_q(q, G.haar_u2(G.SplitMix64(q))) for q in range(n)]
+    for j in range(20):
+        gates.append(G.perm_gate((12 + j % 4,), tg, r.permutation(1 << 12).astype(np.uint32)))
+    sim = gpu_run(P, n, 5, gates)
+    assert_parity(sim, oracle_run(oracle_mod, n, 5, gates), n)
+    assert sim.stats()["perm_launches"] == 2
+
+
 @pytest.mark.parametrize("ranks", [1, 4])
 def test_streamed_flush_parity(P, oracle_mod, ranks):
     """Steps launched while the planner still runs (runtime.cpp flush): with

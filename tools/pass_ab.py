@@ -19,6 +19,8 @@ elif wl.startswith("chain"):  # config-5 family at n qubits, e.g. chain28
     w = C.Workload("chain", n, 0, C.random_chain(n, 10, seed=5, sweep=True), {})
 elif wl.startswith("qft"):
     w = C.qft_basis(int(wl[3:]), 12345)
+elif wl == "shor":  # config 3 (28 q)
+    w = C.config3_shor()
 else:
     raise SystemExit("unknown PASS_AB_WORKLOAD " + wl)
 packed = pack_gates(w.gates)
@@ -33,13 +35,13 @@ for combo in itertools.product(*[opts[k] for k in keys]) if keys else [()]:
         sim.set_option(k, v)
     sim.set_option("timing", 1)
     for _ in range(3):
-        sim.init_basis(0); sim.run_circuit(w.gates, packed=packed); sim.sync()
+        sim.init_basis(w.init); sim.run_circuit(w.gates, packed=packed); sim.sync()
     sim.reset_stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K = 5
     e0.record(sim.stream)
     for _ in range(K):
-        sim.init_basis(0); sim.run_circuit(w.gates, packed=packed)
+        sim.init_basis(w.init); sim.run_circuit(w.gates, packed=packed)
         sim.sync()
     e1.record(sim.stream)
     torch.cuda.synchronize()
@@ -49,4 +51,4 @@ for combo in itertools.product(*[opts[k] for k in keys]) if keys else [()]:
                       "agu_per_s": len(w.gates) * 2 ** w.n / (ms / 1e3),
                       "pass_ms_per_launch": st["pass_ms"] / max(1, st["passes"]),
                       "passes_per_step": st["passes"] / K, "pass_GBps": st["pass_amp_bytes"] / (st["pass_ms"] / 1e3) / 1e9,
-                      "plan_ms": st["plan_ms"] / K}))
+                      "perm_ms": st["perm_ms"] / K, "plan_ms": st["plan_ms"] / K}))
