@@ -111,6 +111,16 @@ void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, 
     }
 }
 
+// An unpredicated Hadamard-form real 2x2, h [[1, 1], [1, -1]]: the JIT tier
+// applies the unnormalised sum/difference (2 adds per component instead of
+// 2 multiplies + 2 FMAs) and multiplies the product of the h's in once
+// before the store (every op is linear, so the scale commutes).
+static bool jit_hadamard(const KOp &op)
+{
+    return op.code == OPC_U2R && !op.mreg && !op.mlane && !op.mwarp && !op.mout && op.m[1] == 0 && op.m[3] == 0 &&
+           op.m[5] == 0 && op.m[7] == 0 && op.m[0] == op.m[2] && op.m[0] == op.m[4] && op.m[6] == -op.m[0];
+}
+
 JitPass jit_generate(const Step &st)
 {
     std::vector<int> out_idx, m_idx, m_col;
@@ -413,6 +423,9 @@ JitPass jit_generate(const Step &st)
         s << " }\n";
         live &= ~F;
     };
+    int n_had = 0;
+    for (const KOp &op : st.ops) n_had += jit_hadamard(op);
+    if (n_had) s << " double hs = 1.0;  // product of the Hadamard-form scales applied so far\n";
     const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
     for (size_t o = o_first; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
@@ -541,6 +554,15 @@ JitPass jit_generate(const Step &st)
                     s << v << ".x = fma(" << F0 << ", " << v << ".x, p1); " << v << ".y = fma(" << F0 << ", " << v
                       << ".y, p2); }\n";
             }
+        } else if (jit_hadamard(op)) {
+            const int k = op.k;
+            for (int p = 0; p < kAmpsPerThread / 2; p++) {
+                const int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1)), i1 = i0 | (1 << k);
+                const std::string x = A(i0), y = A(i1);
+                s << "  { const double2 t = " << x << "; " << x << ".x = t.x + " << y << ".x; " << x << ".y = t.y + "
+                  << y << ".y; " << y << ".x = t.x - " << y << ".x; " << y << ".y = t.y - " << y << ".y; }\n";
+            }
+            s << "  hs *= " << M << "[0];\n";
         } else {
             const int k = op.k;
             for (int p = 0; p < kAmpsPerThread / 2; p++) {
@@ -591,6 +613,8 @@ JitPass jit_generate(const Step &st)
         s << " }\n";
     }
     flush(live);
+    if (n_had)
+        for (int i = 0; i < kAmpsPerThread; i++) s << " " << A(i) << ".x *= hs; " << A(i) << ".y *= hs;\n";
     materialize(1);  // register bit 0 lies inside one 256-bit store
     s << " {\n  double2 *p = P.st + base + (" << gaddr(cur, "TPO") << ");\n";
     {
@@ -767,7 +791,8 @@ std::string jit_key(const Step &st)
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
     for (const KOp &op : st.ops) {
-        put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16));
+        put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16) |
+            ((uint64_t)jit_hadamard(op) << 17));
         put((uint64_t)op.mreg | ((uint64_t)op.vreg << 8) | ((uint64_t)op.mlane << 16) | ((uint64_t)op.vlane << 24) |
             ((uint64_t)op.mwarp << 32) | ((uint64_t)op.vwarp << 40));
         if (op.code == OPC_TRANS || op.code == OPC_U4) put(op.cfg);
