@@ -137,14 +137,15 @@ JitPass jit_generate(const Step &st)
          "#pragma unroll\n for (int j = 0; j < " << kTileBits << "; j++) { const int t = ts[j]; "
          "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
     // e^{2 pi i t / 2^64}: table of the top 8 bits x Taylor series of the rest (|x| < 2pi/256)
+    // e^{2 pi i t / 2^64}: the nearest table angle k/256 times e^{i x}, |x| <=
+    // pi/256, by Taylor to x^6 (cos) and x^5 (sin): truncation < 1e-17
     s << "__device__ __forceinline__ double2 qexp(unsigned long long t, const double2 *tab)\n{\n"
-         " const double2 b = __ldg(tab + (t >> 56));\n"
-         " const double x = (double)(t & 0x00FFFFFFFFFFFFFFULL) * 3.4061215800865545e-19;\n"  // 2pi / 2^64
+         " const unsigned long long k = (t + (1ULL << 55)) >> 56;\n"
+         " const double2 b = __ldg(tab + k);\n"
+         " const double x = (double)(long long)(t - (k << 56)) * 3.4061215800865545e-19;\n"  // 2pi / 2^64
          " const double x2 = x * x;\n"
-         " const double c = fma(x2, fma(x2, fma(x2, fma(x2, 2.48015873015873e-05, -1.3888888888888889e-03), "
-         "4.1666666666666664e-02), -0.5), 1.0);\n"
-         " const double s = x * fma(x2, fma(x2, fma(x2, fma(x2, 2.7557319223985893e-06, -1.9841269841269841e-04), "
-         "8.3333333333333332e-03), -1.6666666666666666e-01), 1.0);\n"
+         " const double c = fma(x2, fma(x2, fma(x2, -1.3888888888888889e-03, 4.1666666666666664e-02), -0.5), 1.0);\n"
+         " const double s = x * fma(x2, fma(x2, 8.3333333333333332e-03, -1.6666666666666666e-01), 1.0);\n"
          " return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));\n}\n";
     const int NT = kPassThreads, ROWS = kTileAmps / 8;
     std::string BAR = "__syncthreads();";
