@@ -117,6 +117,16 @@ typedef struct {
 qsim_status qsim_create(int n_qubits, int n_gpus, qsim_ctx *out);
 /* General creation; see qsim_config. */
 qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out);
+/* SPMD creation of rank `rank` of n_gpus (NCCL transport, one process per
+ * GPU): the shorthand of qsim_create_ext for that case.
+ * nccl_unique_id: the 128 bytes rank 0 drew with qsim_get_unique_id (every
+ * rank passes the same bytes).  shard/scratch/cuda_stream may be NULL (the
+ * library allocates/creates); caller-supplied ones must outlive the context
+ * and shard_bytes must be 16 * 2^(n - log2 n_gpus).  n_gpus == 1 makes a
+ * LOCAL context (nccl_unique_id ignored). */
+qsim_status qsim_create_rank(int n_qubits, int n_gpus, int rank, const void *nccl_unique_id, void *shard,
+                             size_t shard_bytes, void *scratch, size_t scratch_bytes, void *cuda_stream,
+                             qsim_ctx *out);
 /* Recommended scratch bytes for (n, P). */
 size_t qsim_scratch_bytes(int n_qubits, int n_ranks);
 /* ncclUniqueId (128 bytes) for rank 0 to broadcast. */

@@ -52,7 +52,7 @@ class qsim_stats(ctypes.Structure):
 
 
 EXPORTS = [
-    "qsim_create", "qsim_create_ext", "qsim_scratch_bytes", "qsim_get_unique_id", "qsim_destroy",
+    "qsim_create", "qsim_create_ext", "qsim_create_rank", "qsim_scratch_bytes", "qsim_get_unique_id", "qsim_destroy",
     "qsim_init_basis", "qsim_apply_1q", "qsim_apply_controlled", "qsim_apply_perm", "qsim_apply_swap",
     "qsim_remap", "qsim_run_circuit", "qsim_probabilities", "qsim_expectations", "qsim_measure",
     "qsim_get_amplitudes", "qsim_sync", "qsim_get_layout", "qsim_set_option", "qsim_get_stats",
@@ -76,6 +76,8 @@ def lib():
     sig = {
         "qsim_create": ([i, i, P(ctx)], st),
         "qsim_create_ext": ([P(qsim_config), P(ctx)], st),
+        "qsim_create_rank": ([i, i, i, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                              ctypes.c_size_t, ctypes.c_void_p, P(ctx)], st),
         "qsim_scratch_bytes": ([i, i], ctypes.c_size_t),
         "qsim_get_unique_id": ([ctypes.c_void_p], st),
         "qsim_destroy": ([ctx], st),

@@ -879,6 +879,29 @@ qsim_status qsim_get_unique_id(void *out128)
     return QSIM_OK;
 }
 
+qsim_status qsim_create_rank(int n_qubits, int n_gpus, int rank, const void *nccl_unique_id, void *shard,
+                             size_t shard_bytes, void *scratch, size_t scratch_bytes, void *cuda_stream,
+                             qsim_ctx *out)
+{
+    if (!out || n_gpus < 1 || (n_gpus & (n_gpus - 1)) || n_gpus > 64) return QSIM_ERR_ARG;
+    if (n_gpus > 1 && !nccl_unique_id) return QSIM_ERR_ARG;
+    const int G = ilog2(n_gpus);
+    if (n_qubits - G < 1 || n_qubits > 62) return QSIM_ERR_ARG;
+    if (shard && shard_bytes != ((size_t)16 << (n_qubits - G))) return QSIM_ERR_ARG;
+    qsim_config cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.n_qubits = n_qubits;
+    cfg.n_ranks = n_gpus;
+    cfg.rank = n_gpus > 1 ? rank : 0;
+    cfg.transport = n_gpus > 1 ? QSIM_TRANSPORT_NCCL : QSIM_TRANSPORT_LOCAL;
+    cfg.shards[0] = shard;
+    cfg.scratch = scratch;
+    cfg.scratch_bytes = scratch_bytes;
+    cfg.stream = cuda_stream;
+    if (n_gpus > 1) std::memcpy(cfg.nccl_id, nccl_unique_id, sizeof(cfg.nccl_id));
+    return qsim_create_ext(&cfg, out);
+}
+
 qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
 {
     if (!cfg || !out) return QSIM_ERR_ARG;

@@ -62,5 +62,16 @@ int main(void)
     printf("abi_client ok: gates=%llu passes=%llu kernels=%llu\n", (unsigned long long)st.gates,
            (unsigned long long)st.passes, (unsigned long long)st.kernel_launches);
     CHECK(qsim_destroy(ctx));
+    /* the SPMD shorthand with one rank: a LOCAL context */
+    qsim_ctx c1 = NULL;
+    if (qsim_create_rank(10, 3, 0, NULL, NULL, 0, NULL, 0, NULL, &c1) != QSIM_ERR_ARG) return 8;
+    CHECK(qsim_create_rank(10, 1, 0, NULL, NULL, 0, NULL, 0, NULL, &c1));
+    CHECK(qsim_init_basis(c1, 0));
+    for (int q = 0; q < 10; q++) CHECK(qsim_apply_1q(c1, q, H));
+    double nrm;
+    CHECK(qsim_probabilities(c1, NULL, 0, &nrm));
+    CHECK(qsim_get_amplitudes(c1, 1023, 1, &a[0]));
+    if (fabs(nrm - 1.0) > 1e-14 || fabs(a[0].re - 1.0 / 32.0) > 1e-15) return 9;
+    CHECK(qsim_destroy(c1));
     return 0;
 }

@@ -257,6 +257,19 @@ def _build_c_client(pkg, tmp_path):
     return exe
 
 
+def test_create_rank_argument_errors(pkg):
+    """qsim_create_rank rejects bad rank counts, a missing NCCL id and a
+    wrong shard size before touching the device."""
+    import ctypes
+    from paper_quant_ph_0608239_b200 import _native as N
+    lib = N.lib()
+    ctx = ctypes.c_void_p()
+    assert lib.qsim_create_rank(20, 3, 0, None, None, 0, None, 0, None, ctypes.byref(ctx)) == 1
+    assert lib.qsim_create_rank(20, 2, 0, None, None, 0, None, 0, None, ctypes.byref(ctx)) == 1
+    assert lib.qsim_create_rank(20, 1, 0, None, ctypes.c_void_p(256), 123, None, 0, None, ctypes.byref(ctx)) == 1
+    assert lib.qsim_create_rank(1, 4, 0, b"x" * 128, None, 0, None, 0, None, ctypes.byref(ctx)) == 1
+
+
 def test_c_client_compiles_and_links(pkg, tmp_path):
     """A plain C program builds against include/qsim.h + libqsim_b200.so."""
     assert os.path.exists(_build_c_client(pkg, tmp_path))
