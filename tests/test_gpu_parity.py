@@ -491,4 +491,11 @@ def test_gpu_fuzz(P, oracle_mod, seed):
         sim.set_option("global_policy", seed % 3)
     sim.init_basis(init)
     sim.run_circuit(gates)
-    assert_parity(sim, oracle_run(oracle_mod, n, init, gates), n)
+    o = oracle_run(oracle_mod, n, init, gates)
+    assert_parity(sim, o, n)
+    # again with the kernels cached: plan cache on (replay) or off (re-plan,
+    # streamed launches)
+    sim.set_option("plan_cache", seed % 2)
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    assert_parity(sim, o, n)
