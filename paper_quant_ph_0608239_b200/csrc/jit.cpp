@@ -15,6 +15,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <functional>
 #include <sstream>
 #include <thread>
@@ -367,10 +368,96 @@ JitPass jit_generate(const Step &st)
             if (S & bits) F |= 1u << S;
         return F;
     };
+    // CTA-uniform phase terms: an OPC_PHASE_ACC whose predicate is on
+    // out-of-tile bits only (a QFT's controlled phases with the far qubits)
+    // adds the same angle in every thread of the CTA.  Rather than every warp
+    // evaluating all of them, the warps split them, sum per (monomial, flush
+    // epoch) slot, and reduce through shared memory once per tile; the flush
+    // of a monomial adds its slot in.  The epochs come from a dry run of the
+    // lazy-flush rules below.
+    const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
+    auto uniform_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && op.mout && !op.mlane && !op.mwarp; };
+    std::vector<std::vector<std::pair<int, int>>> uterms(st.ops.size());  // (slot, sign) per term
+    std::vector<uint32_t> slot_S;
+    std::map<std::pair<uint32_t, int>, int> slot_of;  // (monomial, flush epoch) -> slot
+    int epoch[kAmpsPerThread] = {0};
+    {
+        int n_uni = 0;
+        for (const KOp &op : st.ops) n_uni += uniform_acc(op);
+        if (!pipe && n_uni >= 8) {
+            uint32_t sim_live = 0;
+            auto sim_flush = [&](uint32_t F) {
+                F &= sim_live;
+                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+                    if ((F >> S) & 1) epoch[S]++;
+                sim_live &= ~F;
+            };
+            for (size_t o = o_first; o < st.ops.size(); o++) {
+                const KOp &op = st.ops[o];
+                if (op.code == OPC_TRANS) { sim_flush(~0u); continue; }
+                if (op.code == OPC_PHASE_FLUSH || op.code == OPC_DATA || op.code == OPC_PHASE) continue;
+                if (op.code == OPC_U4) { sim_flush(touching((1u << op.k) | (1u << (int)op.cfg))); continue; }
+                if (op.code == OPC_PHASE_ACC) {
+                    const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
+                    for (uint32_t T = Z;; T = (T - 1) & Z) {
+                        const uint32_t S = O | T;
+                        if (uniform_acc(op)) {
+                            auto key = std::make_pair(S, epoch[S]);
+                            auto it = slot_of.find(key);
+                            if (it == slot_of.end()) {
+                                it = slot_of.emplace(key, (int)slot_S.size()).first;
+                                slot_S.push_back(S);
+                            }
+                            uterms[o].push_back({it->second, __builtin_popcount(T) & 1 ? -1 : 1});
+                        }
+                        sim_live |= 1u << S;
+                        if (!T) break;
+                    }
+                    continue;
+                }
+                sim_flush(touching(1u << op.k));
+            }
+            for (int &e : epoch) e = 0;
+        }
+    }
+    const int NS = (int)slot_S.size(), NW = kPassThreads / 32;
+    if (NS) {
+        s << " __shared__ unsigned long long uw[" << NW * NS << "], utot[" << NS << "];\n";
+        s << " {\n";
+        for (int k = 0; k < NS; k++) s << "  unsigned long long u" << k << " = 0;\n";
+        s << "  switch (warp) {\n";
+        int next_w = 0;
+        std::vector<std::vector<size_t>> by_warp(NW);
+        for (size_t o = o_first; o < st.ops.size(); o++)
+            if (!uterms[o].empty()) { by_warp[next_w].push_back(o); next_w = (next_w + 1) % NW; }
+        for (int w = 0; w < NW; w++) {
+            s << "  case " << w << ": {\n";
+            for (size_t o : by_warp[w]) {
+                const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
+                s << "   { const unsigned long long K = ((gcta & P.out[" << out_idx[o] << "][0]) == P.out[" << out_idx[o]
+                  << "][1]) ? (unsigned long long)__double_as_longlong(" << M << "[" << m_col[o] << "]) : 0ULL;";
+                for (auto &t : uterms[o]) s << " u" << t.first << (t.second < 0 ? " -= K;" : " += K;");
+                s << " }\n";
+            }
+            s << "   break; }\n";
+        }
+        s << "  }\n  if (lane == 0) {";
+        for (int k = 0; k < NS; k++) s << " uw[warp * " << NS << " + " << k << "] = u" << k << ";";
+        s << " }\n }\n __syncthreads();\n";
+        s << " for (int k = warp; k < " << NS << "; k += " << NW << ") {\n"
+             "  unsigned long long v = lane < " << NW << " ? uw[lane * " << NS << " + k] : 0ULL;\n";
+        for (int d = 1; d < NW; d <<= 1) s << "  v += __shfl_xor_sync(0xffffffffu, v, " << d << ");\n";
+        s << "  if (lane == 0) utot[k] = v;\n }\n __syncthreads();\n";
+    }
     auto flush = [&](uint32_t F) {
         F &= live;
         if (!F) return;
         s << " { // flush monomials 0x" << std::hex << F << std::dec << "\n";
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++) {
+            if (!((F >> S) & 1)) continue;
+            auto it = slot_of.find(std::make_pair(S, epoch[S]++));
+            if (it != slot_of.end()) s << "  mo" << S << " += utot[" << it->second << "];\n";
+        }
         // e^{i theta_i}, theta_i = sum of acc[S] over S in F, S subset of i: per
         // distinct register angle (A) or per monomial (B), the cheaper
         const double kExp = 20, kMul = 4;
@@ -427,7 +514,6 @@ JitPass jit_generate(const Step &st)
     int n_had = 0;
     for (const KOp &op : st.ops) n_had += jit_hadamard(op);
     if (n_had) s << " double hs = 1.0;  // product of the Hadamard-form scales applied so far\n";
-    const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
     for (size_t o = o_first; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
@@ -528,6 +614,14 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         materialize(op.mreg | (is_phase ? 0u : 1u << op.k));
+        if (!uterms[o].empty()) {  // summed in the CTA-uniform prologue, added at the flush
+            const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
+            for (uint32_t T = Z;; T = (T - 1) & Z) {
+                live |= 1u << (O | T);
+                if (!T) break;
+            }
+            continue;
+        }
         s << " { // op " << o << " code " << op.code << "\n";
         if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
         if (pout && !sel) s << "  if (tp) {\n";
