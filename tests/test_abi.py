@@ -219,6 +219,10 @@ def test_jit_kernels_compile_for_sm100a(pkg):
     d = json.loads(_plan(pkg, 14, 2, gates, fusion=2))
     assert d["jit"]["ok"], d["jit"]["error"]
     assert d["jit"]["kernels"] >= 1
+    # QFT passes: lazy phase flushes, the CTA-uniform phase prologue, Hadamard form
+    w = C.qft_basis(20, 777)
+    d = json.loads(_plan(pkg, 20, 1, w.gates, fusion=2))
+    assert d["jit"]["ok"], d["jit"]["error"]
 
 
 @pytest.mark.parametrize("policy", ["remap", "pairwise", "auto"])
