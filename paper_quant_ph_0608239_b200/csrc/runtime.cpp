@@ -1103,17 +1103,17 @@ qsim_status qsim_run_circuit(qsim_ctx c, const qsim_gate *gates, size_t n_gates)
     GUARD(c);
     if (n_gates && !gates) return QSIM_ERR_ARG;
     if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "gate before qsim_init_basis");
-    std::vector<GateRec> recs(n_gates);
+    // validated straight into the queue; on an error the queue is cut back
+    const size_t q0 = c->queue.size();
+    c->queue.resize(q0 + n_gates);
     for (size_t i = 0; i < n_gates; i++) {
-        qsim_status s = to_rec(c, c->n, gates[i], recs[i]);
+        qsim_status s = to_rec(c, c->n, gates[i], c->queue[q0 + i]);
         if (s != QSIM_OK) {
+            c->queue.resize(q0);
             std::string e = c->last_error;
             FAIL(c, s, "gate %zu: %s", i, e.c_str());
         }
-    }
-    for (auto &r : recs) {
-        r.id = (int)c->queue.size();
-        c->queue.push_back(std::move(r));
+        c->queue[q0 + i].id = (int)(q0 + i);
     }
     c->stats.gates += n_gates;
     return QSIM_OK;
