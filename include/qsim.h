@@ -178,6 +178,12 @@ qsim_status qsim_probabilities(qsim_ctx ctx, const int *qubits, int k, double *o
 /* <Q_i> = sum_k p_k k_i for every qubit i (Eq. Shor7); host
  * array of n doubles.  Non-collapsing. */
 qsim_status qsim_expectations(qsim_ctx ctx, double *out);
+/* The same, enqueued: returns once the reduction and the copy into `out`
+ * are on the context's stream; `out` holds the result after qsim_sync (or
+ * any later synchronising call).  With pinned (page-locked) `out` the host
+ * can enqueue the next circuit while this one runs; with pageable memory
+ * the copy, and so the call, waits for the device. */
+qsim_status qsim_expectations_async(qsim_ctx ctx, double *out);
 
 /* n_shots basis states of the listed qubits drawn with probability
  * |<x|Phi>|^2 by inverse CDF with the counter-based

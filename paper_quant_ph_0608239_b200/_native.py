@@ -54,7 +54,8 @@ class qsim_stats(ctypes.Structure):
 EXPORTS = [
     "qsim_create", "qsim_create_ext", "qsim_create_rank", "qsim_scratch_bytes", "qsim_get_unique_id", "qsim_destroy",
     "qsim_init_basis", "qsim_apply_1q", "qsim_apply_controlled", "qsim_apply_perm", "qsim_apply_swap",
-    "qsim_remap", "qsim_run_circuit", "qsim_probabilities", "qsim_expectations", "qsim_measure",
+    "qsim_remap", "qsim_run_circuit", "qsim_probabilities", "qsim_expectations", "qsim_expectations_async",
+    "qsim_measure",
     "qsim_get_amplitudes", "qsim_sync", "qsim_get_layout", "qsim_set_option", "qsim_get_stats",
     "qsim_reset_stats", "qsim_status_str", "qsim_last_error", "qsim_plan_json", "qsim_exchange_peers",
 ]
@@ -90,6 +91,7 @@ def lib():
         "qsim_run_circuit": ([ctx, P(qsim_gate), ctypes.c_size_t], st),
         "qsim_probabilities": ([ctx, P(i), i, P(d)], st),
         "qsim_expectations": ([ctx, P(d)], st),
+        "qsim_expectations_async": ([ctx, ctypes.c_void_p], st),
         "qsim_measure": ([ctx, P(i), i, u64, u64, P(u64)], st),
         "qsim_get_amplitudes": ([ctx, u64, u64, P(c128)], st),
         "qsim_sync": ([ctx], st),

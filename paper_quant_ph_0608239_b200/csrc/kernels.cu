@@ -816,6 +816,28 @@ void launch_expect(const double2 *st, int M, double *partial, double *out, cudaS
     k_expect_final<<<M + 1, 256, 0, s>>>(partial, cb, M, out);
 }
 
+// <Q_q> in logical order from S shards' physical-bit sums (phys[s*(M+1) + p],
+// p < M: bit p set, p == M: total), shard s holding rank s:
+// out[q] = sum over s in order of (p < M ? phys_s[p] : rank bit p-M of s ? phys_s[M] : 0)
+__global__ void k_expect_logical(const double *__restrict__ phys, const __grid_constant__ ExpectMap m,
+                                 double *__restrict__ out)
+{
+    const int q = threadIdx.x;
+    if (q >= m.n) return;
+    const int p = m.phys_of[q];
+    double a = 0.0;
+    for (int r = 0; r < m.S; r++) {
+        const double *v = phys + (size_t)r * (m.M + 1);
+        a += p < m.M ? v[p] : (((r >> (p - m.M)) & 1) ? v[m.M] : 0.0);
+    }
+    out[q] = a;
+}
+
+void launch_expect_logical(const double *phys, const ExpectMap &m, double *out, cudaStream_t s)
+{
+    k_expect_logical<<<1, 64, 0, s>>>(phys, m, out);
+}
+
 // ------------------------------------------------------------- sampling
 __device__ __forceinline__ uint64_t sm64_dev(uint64_t z)
 {

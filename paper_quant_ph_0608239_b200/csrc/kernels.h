@@ -35,6 +35,12 @@ void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab
 void launch_init(double2 *st, uint64_t n_amps, int64_t one_at, cudaStream_t s);
 void launch_probs(const double2 *st, const ProbsDesc &d, double *partial, double *out, cudaStream_t s);
 void launch_expect(const double2 *st, int M, double *partial, double *out /* M+1 */, cudaStream_t s);
+struct ExpectMap {
+    int n, M, S;          // logical qubits, local bits, shards (rank s = index s)
+    int phys_of[64];      // logical qubit -> physical bit
+};
+void launch_expect_logical(const double *phys /* S x (M+1) */, const ExpectMap &m, double *out /* n */,
+                           cudaStream_t s);
 void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *out,
                    cudaStream_t s);
 void launch_gather(double2 *out, uint64_t first, uint64_t count, double2 *const *shards_dev, int virt, int my_rank,

@@ -1240,32 +1240,54 @@ qsim_status qsim_probabilities(qsim_ctx c, const int *qubits, int k, double *out
     return probabilities_impl(c, qubits, k, out);
 }
 
-qsim_status qsim_expectations(qsim_ctx c, double *out)
+// <Q_i> (Eq. Shor7): per-shard physical-bit sums on the device, rank order
+// sum + logical order on the device (k_expect_logical; same additions in the
+// same order as a host loop), then one D2H of n doubles into `out`.
+static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
 {
-    GUARD(c);
     if (!out) return QSIM_ERR_ARG;
     if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
     qsim_status s = flush(c);
     if (s != QSIM_OK) return s;
-    const int M = c->M, cb = std::min(12, M), n = c->n;
+    const int M = c->M, cb = std::min(12, M), n = c->n, S = c->transport == QSIM_TRANSPORT_NCCL ? c->P : n_local(c);
     const uint64_t nch = 1ULL << (M - cb);
-    const size_t plen = nch * (cb + 1);
-    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, plen + M + 1)) != QSIM_OK) return s;
-    std::vector<std::vector<double>> per(n_local(c), std::vector<double>(n, 0.0));
-    std::vector<double> phys(M + 1);
+    const size_t plen = nch * (cb + 1), vlen = (size_t)M + 1;
+    // partial sums | this process's shard vectors | all ranks' vectors (NCCL) | logical result
+    const size_t need = plen + (size_t)n_local(c) * vlen + (size_t)S * vlen + n;
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
+    double *own = c->d_red + plen, *all = own + (size_t)n_local(c) * vlen, *res = all + (size_t)S * vlen;
     RangeGuard rg(c, 4, 0);
     for (int i = 0; i < n_local(c); i++) {
-        launch_expect(c->shards[i], M, c->d_red, c->d_red + plen, c->stream);
+        launch_expect(c->shards[i], M, c->d_red, own + (size_t)i * vlen, c->stream);
         LAUNCHED(c);
-        CK(c, cudaMemcpyAsync(phys.data(), c->d_red + plen, (M + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
-        const uint64_t r = (uint64_t)local_ranks(c, i);
-        for (int q = 0; q < n; q++) {
-            const int p = c->planner->phys_of[q];
-            per[i][q] = p < M ? phys[p] : (((r >> (p - M)) & 1) ? phys[M] : 0.0);
-        }
     }
-    return sum_over_ranks(c, per, out, n);
+    const double *phys = own;
+    if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1) {
+        CKN(c, ncclAllGather(own, all, vlen, ncclDouble, c->comm, c->stream));
+        phys = all;
+    }
+    ExpectMap m{};
+    m.n = n;
+    m.M = M;
+    m.S = S;
+    for (int q = 0; q < n; q++) m.phys_of[q] = c->planner->phys_of[q];
+    launch_expect_logical(phys, m, res, c->stream);
+    LAUNCHED(c);
+    CK(c, cudaMemcpyAsync(out, res, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (sync) CK(c, cudaStreamSynchronize(c->stream));
+    return QSIM_OK;
+}
+
+qsim_status qsim_expectations(qsim_ctx c, double *out)
+{
+    GUARD(c);
+    return expectations_impl(c, out, true);
+}
+
+qsim_status qsim_expectations_async(qsim_ctx c, double *out)
+{
+    GUARD(c);
+    return expectations_impl(c, out, false);
 }
 
 qsim_status qsim_measure(qsim_ctx c, const int *qubits, int k, uint64_t seed, uint64_t n_shots, uint64_t *out)

@@ -16,6 +16,11 @@ from . import _native as N
 G_1Q, G_CTRL, G_PERM, G_SWAP = 0, 1, 2, 3
 
 
+def torch_float64():
+    import torch
+    return torch.float64
+
+
 class QsimError(RuntimeError):
     def __init__(self, status: int, msg: str):
         name = N.STATUS[status] if 0 <= status < len(N.STATUS) else str(status)
@@ -238,6 +243,14 @@ class QSim:
         self._check(self.lib.qsim_expectations(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))),
                     "qsim_expectations")
         return out
+
+    def expectations_async(self, out) -> None:
+        """Enqueue <Q_i> into `out` (a pinned CPU torch tensor of n float64,
+        valid after sync()); the host can go on enqueuing work meanwhile."""
+        if out.dtype != torch_float64() or out.numel() != self.n or out.device.type != "cpu" or not out.is_contiguous():
+            raise ValueError("out must be a contiguous CPU float64 tensor of n elements")
+        self._check(self.lib.qsim_expectations_async(self.ctx, ctypes.c_void_p(out.data_ptr())),
+                    "qsim_expectations_async")
 
     def measure(self, qubits: Sequence[int], seed: int, shots: int) -> np.ndarray:
         k = len(qubits)

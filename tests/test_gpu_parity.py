@@ -161,6 +161,29 @@ def test_perm_run_parity(P, oracle_mod, n, ranks):
     assert_parity(sim, oracle_run(oracle_mod, n, 3, gates), n)
 
 
+@pytest.mark.parametrize("ranks", [1, 4])
+def test_expectations_async(P, oracle_mod, ranks):
+    """qsim_expectations_async into pinned memory, several circuits enqueued
+    back to back before one sync: each buffer holds its own circuit's <Q_i>,
+    bitwise equal to the synchronous call, and equal to the oracle's."""
+    import torch
+    n = 14
+    sim = P.QSim(n, n_ranks=ranks, transport="virtual" if ranks > 1 else "local")
+    circuits = [C.random_brickwork(n, 3, seed=s) for s in range(3)]
+    bufs = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in circuits]
+    for g, b in zip(circuits, bufs):
+        sim.init_basis(3)
+        sim.run_circuit(g)
+        sim.expectations_async(b)
+    sim.sync()
+    for g, b in zip(circuits, bufs):
+        sim.init_basis(3)
+        sim.run_circuit(g)
+        ex = sim.expectations()
+        assert np.array_equal(b.numpy(), ex)
+        assert np.max(np.abs(ex - oracle_run(oracle_mod, n, 3, g).expectations())) <= 1e-12
+
+
 def test_perm_run_max_shared_memory(P, oracle_mod):
     """12-qubit register, 20 controlled perms: runs of 12 and 8 whose tables
     and double-buffered tiles take up to 224 KB of shared memory per CTA."""
