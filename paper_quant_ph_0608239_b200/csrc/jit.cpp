@@ -7,6 +7,9 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdio>
+#include <unistd.h>
+#include <sys/stat.h>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -877,6 +880,70 @@ static bool nvrtc_compile(const std::string &src, std::vector<char> &cubin, std:
     return true;
 }
 
+// On-disk cubin cache for the pass kernels, so that a new process does not
+// recompile the structures an earlier one built: $QSIM_JIT_CACHE_DIR (default
+// $XDG_CACHE_HOME/qsim_b200_jit or ~/.cache/qsim_b200_jit; "off" disables).
+// An entry stores its full source, compared on load (no trust in the hash).
+static const char kJitCacheTag[] = "qsim_b200 jit v1 sm_100a --std=c++17 -default-device\n";
+
+static std::string jit_cache_dir()
+{
+    static const std::string dir = []() -> std::string {
+        const char *e = getenv("QSIM_JIT_CACHE_DIR");
+        if (e) return std::string(e) == "off" ? std::string() : std::string(e);
+        const char *x = getenv("XDG_CACHE_HOME");
+        const char *h = getenv("HOME");
+        std::string base = x && *x ? std::string(x) : h && *h ? std::string(h) + "/.cache" : std::string();
+        return base.empty() ? base : base + "/qsim_b200_jit";
+    }();
+    return dir;
+}
+
+static std::string jit_cache_path(const std::string &src)
+{
+    uint64_t h = 1469598103934665603ULL;  // FNV-1a over tag + source
+    for (const char *p : {kJitCacheTag, src.c_str()})
+        for (; *p; p++) h = (h ^ (unsigned char)*p) * 1099511628211ULL;
+    char name[32];
+    snprintf(name, sizeof(name), "/%016llx.bin", (unsigned long long)h);
+    return jit_cache_dir() + name;
+}
+
+static bool disk_load(const std::string &src, std::vector<char> &cubin)
+{
+    if (jit_cache_dir().empty()) return false;
+    FILE *f = fopen(jit_cache_path(src).c_str(), "rb");
+    if (!f) return false;
+    bool ok = false;
+    uint64_t ns = 0, nc = 0;
+    if (fread(&ns, 8, 1, f) == 1 && ns == src.size() + sizeof(kJitCacheTag) - 1) {
+        std::string stored(ns, '\0');
+        if (fread(&stored[0], 1, ns, f) == ns && stored == kJitCacheTag + src && fread(&nc, 8, 1, f) == 1 &&
+            nc > 0 && nc < (1ULL << 30)) {
+            cubin.resize(nc);
+            ok = fread(cubin.data(), 1, nc, f) == nc;
+        }
+    }
+    fclose(f);
+    return ok;
+}
+
+static void disk_store(const std::string &src, const std::vector<char> &cubin)
+{
+    const std::string dir = jit_cache_dir();
+    if (dir.empty()) return;
+    mkdir(dir.c_str(), 0755);  // the parent must exist; failures only lose the cache
+    const std::string path = jit_cache_path(src), tmp = path + "." + std::to_string(getpid()) + ".tmp";
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const std::string stored = kJitCacheTag + src;
+    const uint64_t ns = stored.size(), nc = cubin.size();
+    const bool ok = fwrite(&ns, 8, 1, f) == 1 && fwrite(stored.data(), 1, ns, f) == ns && fwrite(&nc, 8, 1, f) == 1 &&
+                    fwrite(cubin.data(), 1, nc, f) == nc;
+    if (fclose(f) == 0 && ok) rename(tmp.c_str(), path.c_str());
+    else remove(tmp.c_str());
+}
+
 std::string jit_key(const Step &st)
 {
     std::string k;
@@ -922,7 +989,11 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
     std::atomic_size_t next{0};
     for (size_t w = 0; w < nthreads; w++)
         th.emplace_back([&]() {
-            for (size_t i; (i = next++) < srcs.size();) ok[i] = nvrtc_compile(srcs[i], bins[i], logs[i]);
+            for (size_t i; (i = next++) < srcs.size();) {
+                if (disk_load(srcs[i], bins[i])) { ok[i] = 1; continue; }
+                ok[i] = nvrtc_compile(srcs[i], bins[i], logs[i]);
+                if (ok[i]) disk_store(srcs[i], bins[i]);
+            }
         });
     for (auto &t : th) t.join();
     for (size_t i = 0; i < srcs.size(); i++) {

@@ -33,7 +33,8 @@ for first in range(0, 1 << n, chunk):
     err = max(err, float(np.max(np.abs(g - view[first:first + g.size]))))
 st = sim.stats()
 print(json.dumps({{"n": n, "shards": shards, "gates": len(gates), "max_abs_diff": err, "norm_dev": abs(1 - nrm),
-                  "exchanges": st["exchanges"], "passes": st["passes"]}}))
+                  "exchanges": st["exchanges"], "passes": st["passes"], "jit_compile_ms": st["jit_compile_ms"],
+                  "jit_kernels": st["jit_kernels"]}}))
 '''
 
 
@@ -70,3 +71,18 @@ def test_large_full_state_parity():
     d = _run(n, 8, "chain", timeout=3600)
     print(json.dumps(d))
     assert d["max_abs_diff"] <= 1e-11 and d["norm_dev"] <= 1e-12 and d["exchanges"] >= 1
+
+
+def test_jit_disk_cache(tmp_path):
+    """The pass kernels a process compiled are loaded from the on-disk cache
+    by the next process (no NVRTC), with the same results; QSIM_JIT_CACHE_DIR=off
+    bypasses it."""
+    env = {"QSIM_JIT_CACHE_DIR": str(tmp_path)}
+    a = _run(18, 1, "chain", env)
+    files = [f for f in os.listdir(tmp_path) if f.endswith(".bin")]
+    assert len(files) == a["jit_kernels"] > 0
+    b = _run(18, 1, "chain", env)
+    assert b["max_abs_diff"] == a["max_abs_diff"] <= 1e-11
+    assert b["jit_compile_ms"] < 0.25 * a["jit_compile_ms"], (a["jit_compile_ms"], b["jit_compile_ms"])
+    c = _run(18, 1, "chain", {"QSIM_JIT_CACHE_DIR": "off"})
+    assert c["max_abs_diff"] == a["max_abs_diff"] and c["jit_compile_ms"] > 2 * b["jit_compile_ms"]
