@@ -540,17 +540,36 @@ __global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRu
             if (A & xmask[e >> d.t])
                 cp_async16(buf + e, st + base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits)));
     };
-    uint64_t base, nbase = 0;
-    uint32_t A, nA = 0;
-    uint64_t inst = next_tile(blockIdx.x, base, A);
+    // tile k+1's (instance, base, active set) is found by one thread while the
+    // CTA gathers tile k-1, and read by all from a two-slot ring
+    __shared__ unsigned long long s_inst[2], s_base[2];
+    __shared__ uint32_t s_A[2];
+    if (threadIdx.x == 0) {
+        uint64_t b0, b1;
+        uint32_t a0, a1;
+        const uint64_t i0 = next_tile(blockIdx.x, b0, a0);
+        const uint64_t i1 = next_tile(i0 + gridDim.x, b1, a1);
+        s_inst[0] = i0; s_base[0] = b0; s_A[0] = a0;
+        s_inst[1] = i1; s_base[1] = b1; s_A[1] = a1;
+    }
+    __syncthreads();
+    uint64_t inst = s_inst[0], base = s_base[0];
+    uint32_t A = s_A[0];
     if (inst < d.n_inst) stage(bufs, base, A);
     cp_async_commit();
     for (int b = 0; inst < d.n_inst; b ^= 1) {
-        const uint64_t ninst = next_tile(inst + gridDim.x, nbase, nA);
+        const uint64_t ninst = s_inst[b ^ 1], nbase = s_base[b ^ 1];
+        const uint32_t nA = s_A[b ^ 1];
         if (ninst < d.n_inst) stage(bufs + (size_t)(b ^ 1) * E, nbase, nA);
         cp_async_commit();  // (possibly empty) group of the next tile
         cp_async_wait1();   // this thread's copies of the current tile landed
         __syncthreads();
+        if (threadIdx.x == 0) {  // slot b (this tile's) is free: every thread read it last iteration
+            uint64_t b2;
+            uint32_t a2;
+            const uint64_t i2 = next_tile(ninst + gridDim.x, b2, a2);
+            s_inst[b] = i2; s_base[b] = b2; s_A[b] = a2;
+        }
         const double2 *sm = bufs + (size_t)b * E;
         if (d.contiguous && d.t >= 2) {
             // 4 consecutive elements share the non-target bits: 4 independent
@@ -586,7 +605,7 @@ __global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRu
                 st[base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits))] = sm[(e & ~T) | w];
             }
         }
-        __syncthreads();  // the buffer is refilled two tiles on
+        __syncthreads();  // the buffer is refilled two tiles on; slot b is visible
         inst = ninst;
         base = nbase;
         A = nA;
