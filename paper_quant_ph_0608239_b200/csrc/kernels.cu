@@ -506,7 +506,8 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__global__ void __launch_bounds__(256) k_perm_run(const __grid_constant__ PermRunDesc d, double2 *__restrict__ st,
+constexpr int kPermRunThreads = 512;
+__global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_constant__ PermRunDesc d, double2 *__restrict__ st,
                                                   const uint32_t *__restrict__ tabs)
 {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -619,12 +620,12 @@ void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab
     const size_t smem = perm_run_smem(d);
     cudaFuncSetAttribute(k_perm_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_perm_run, 256, smem) != cudaSuccess || per_sm < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_perm_run, kPermRunThreads, smem) != cudaSuccess || per_sm < 1) {
         cudaGetLastError();
         per_sm = 1;
     }
     const uint64_t grid = std::min<uint64_t>(d.n_inst, (uint64_t)per_sm * (uint64_t)n_sm);
-    k_perm_run<<<(unsigned)grid, 256, smem, s>>>(d, st, perm_tab);
+    k_perm_run<<<(unsigned)grid, kPermRunThreads, smem, s>>>(d, st, perm_tab);
 }
 
 void launch_perm(const PermDesc &d, double2 *st, const uint32_t *perm_tab, cudaStream_t s)
