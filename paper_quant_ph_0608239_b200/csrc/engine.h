@@ -137,7 +137,7 @@ struct PermDesc {
 constexpr int kMaxPermRun = 32;
 // shared memory of one k_perm_run CTA: two staged tiles (16 B per element),
 // one control mask per extra-bit pattern, R tables of 2^t uint16
-constexpr size_t kPermRunSmemMax = 227 * 1024;
+constexpr size_t kPermRunSmemMax = 226 * 1024;  // 227 KB per block less room for the kernel's static smem
 QSB_HD size_t perm_run_smem_bytes(int tile_bits, int t, int R)
 {
     return ((size_t)32 << tile_bits) + ((size_t)4 << (tile_bits - t)) + (size_t)R * ((size_t)2 << t);

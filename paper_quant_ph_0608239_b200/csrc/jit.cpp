@@ -932,7 +932,8 @@ static void disk_store(const std::string &src, const std::vector<char> &cubin)
 {
     const std::string dir = jit_cache_dir();
     if (dir.empty()) return;
-    mkdir(dir.c_str(), 0755);  // the parent must exist; failures only lose the cache
+    for (size_t i = 1; i <= dir.size(); i++)  // mkdir -p; failures only lose the cache
+        if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
     const std::string path = jit_cache_path(src), tmp = path + "." + std::to_string(getpid()) + ".tmp";
     FILE *f = fopen(tmp.c_str(), "wb");
     if (!f) return;

@@ -161,7 +161,7 @@ def test_plan_perm_run(pkg, oracle_mod, P):
 def test_plan_perm_run_fits_shared_memory(pkg, oracle_mod):
     """A run's R tables of 2^t uint16 and its two staged tiles must fit one
     CTA's shared memory (engine.h perm_run_smem_bytes): 20 perms on a 12-qubit
-    register split into runs of 12 and 8 (227 KB >= 128 KB + 4 B + R * 8 KB)."""
+    register split into runs of 12 and 8 (226 KB >= 128 KB + 4 B + R * 8 KB)."""
     r = np.random.default_rng(9)
     n, tg = 16, tuple(range(12))
     gates = [G.one_q(q, G.H) for q in range(12, 16)]
