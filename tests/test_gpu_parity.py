@@ -522,3 +522,20 @@ def test_gpu_fuzz(P, oracle_mod, seed):
     sim.init_basis(init)
     sim.run_circuit(gates)
     assert_parity(sim, o, n)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("QSIM_FUZZ_LONG_SEEDS", "2"))))
+def test_gpu_fuzz_long(P, oracle_mod, seed):
+    """Long random circuits (600-1500 gates of every kind plus a QFT ladder):
+    passes that hit the per-pass op and parameter budgets, long phase runs
+    with lazy flushes and CTA-uniform terms, 1 or 4 shards."""
+    from tests.test_plan_fuzz import random_circuit
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.integers(16, 21))
+    ranks = int([1, 4][seed % 2])
+    gates = random_circuit(n, int(rng.integers(600, 1500)), 9000 + seed) + C.qft_ladder(list(range(n)), swaps=True)
+    init = int(rng.integers(0, 1 << n))
+    sim = P.QSim(n, n_ranks=ranks, transport="local" if ranks == 1 else "virtual")
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    assert_parity(sim, oracle_run(oracle_mod, n, init, gates), n)
