@@ -30,7 +30,7 @@ namespace {
 int nib(uint64_t c, int j) { return (int)((c >> (4 * j)) & 15); }
 int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
-constexpr size_t kOffInit = 32, kOffTpm = 40, kOffTs = kOffTpm + 8 * kTileBits;
+constexpr size_t kOffInit = 32, kOffTtab = 40, kOffTpm = 48, kOffTs = kOffTpm + 8 * kTileBits;
 constexpr size_t kOffTpo = (kOffTs + 4 * kTileBits + 7) / 8 * 8;  // natural u64 alignment
 
 struct Layout {
@@ -134,7 +134,7 @@ JitPass jit_generate(const Step &st)
     const bool pipe = jit_pipelined();
     s << "// minb=" << minb << " pipe=" << pipe << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
-         "const double2 *ptab; unsigned long long init_phys; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
+         "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
@@ -380,14 +380,20 @@ JitPass jit_generate(const Step &st)
     // lazy-flush rules below.
     const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
     auto uniform_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && op.mout && !op.mlane && !op.mwarp; };
-    std::vector<std::vector<std::pair<int, int>>> uterms(st.ops.size());  // (slot, sign) per term
-    std::vector<uint32_t> slot_S;
-    std::map<std::pair<uint32_t, int>, int> slot_of;  // (monomial, flush epoch) -> slot
+    // Per-thread phase terms (a predicate on lane/warp bits only) are the same
+    // for every tile: a companion kernel (qsim_pass_tab, one CTA, launched
+    // before the pass) sums them per (monomial, flush epoch) slot and thread
+    // into P.ttab, and the flush adds the thread's entry.
+    auto thread_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && !op.mout && (op.mlane || op.mwarp); };
+    std::vector<std::vector<std::pair<int, int>>> uterms(st.ops.size()), tterms(st.ops.size());  // (slot, sign)
+    std::vector<uint32_t> slot_S, tslot_S;
+    std::map<std::pair<uint32_t, int>, int> slot_of, tslot_of;  // (monomial, flush epoch) -> slot
     int epoch[kAmpsPerThread] = {0};
     {
-        int n_uni = 0;
-        for (const KOp &op : st.ops) n_uni += uniform_acc(op);
-        if (!pipe && n_uni >= 8) {
+        int n_uni = 0, n_thr = 0;
+        for (const KOp &op : st.ops) { n_uni += uniform_acc(op); n_thr += thread_acc(op); }
+        const bool use_u = !pipe && n_uni >= 8, use_t = !pipe && n_thr >= 8;
+        if (use_u || use_t) {
             uint32_t sim_live = 0;
             auto sim_flush = [&](uint32_t F) {
                 F &= sim_live;
@@ -404,14 +410,17 @@ JitPass jit_generate(const Step &st)
                     const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
                     for (uint32_t T = Z;; T = (T - 1) & Z) {
                         const uint32_t S = O | T;
-                        if (uniform_acc(op)) {
+                        const bool u = use_u && uniform_acc(op), th = use_t && thread_acc(op);
+                        if (u || th) {
+                            auto &of = u ? slot_of : tslot_of;
+                            auto &sv = u ? slot_S : tslot_S;
                             auto key = std::make_pair(S, epoch[S]);
-                            auto it = slot_of.find(key);
-                            if (it == slot_of.end()) {
-                                it = slot_of.emplace(key, (int)slot_S.size()).first;
-                                slot_S.push_back(S);
+                            auto it = of.find(key);
+                            if (it == of.end()) {
+                                it = of.emplace(key, (int)sv.size()).first;
+                                sv.push_back(S);
                             }
-                            uterms[o].push_back({it->second, __builtin_popcount(T) & 1 ? -1 : 1});
+                            (u ? uterms : tterms)[o].push_back({it->second, __builtin_popcount(T) & 1 ? -1 : 1});
                         }
                         sim_live |= 1u << S;
                         if (!T) break;
@@ -458,8 +467,12 @@ JitPass jit_generate(const Step &st)
         s << " { // flush monomials 0x" << std::hex << F << std::dec << "\n";
         for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++) {
             if (!((F >> S) & 1)) continue;
-            auto it = slot_of.find(std::make_pair(S, epoch[S]++));
+            auto it = slot_of.find(std::make_pair(S, epoch[S]));
             if (it != slot_of.end()) s << "  mo" << S << " += utot[" << it->second << "];\n";
+            auto jt = tslot_of.find(std::make_pair(S, epoch[S]));
+            if (jt != tslot_of.end())
+                s << "  mo" << S << " += __ldg(P.ttab + " << jt->second * kPassThreads << " + threadIdx.x);\n";
+            epoch[S]++;
         }
         // e^{i theta_i}, theta_i = sum of acc[S] over S in F, S subset of i: per
         // distinct register angle (A) or per monomial (B), the cheaper
@@ -617,7 +630,7 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         materialize(op.mreg | (is_phase ? 0u : 1u << op.k));
-        if (!uterms[o].empty()) {  // summed in the CTA-uniform prologue, added at the flush
+        if (!uterms[o].empty() || !tterms[o].empty()) {  // summed per slot elsewhere, added at the flush
             const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
             for (uint32_t T = Z;; T = (T - 1) & Z) {
                 live |= 1u << (O | T);
@@ -728,9 +741,30 @@ JitPass jit_generate(const Step &st)
     // a thread must not exit with its copies (for the other group's tile) in flight
     if (pipe) s << " asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
     s << "}\n";
+    const int NTS = (int)tslot_S.size();
+    if (NTS) {
+        // companion kernel: the per-thread phase slots, once per launch (not per tile)
+        s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads
+          << ") qsim_pass_tab(const __grid_constant__ JP P)\n{\n"
+             " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+        for (int k = 0; k < NTS; k++) s << " unsigned long long t" << k << " = 0;\n";
+        for (size_t o = 0; o < st.ops.size(); o++) {
+            if (tterms[o].empty()) continue;
+            const KOp &op = st.ops[o];
+            s << " { const unsigned long long K = (true";
+            if (op.mlane) s << " && ((lane & " << op.mlane << ") == " << op.vlane << ")";
+            if (op.mwarp) s << " && ((warp & " << op.mwarp << ") == " << op.vwarp << ")";
+            s << ") ? (unsigned long long)__double_as_longlong(P.m[" << m_idx[o] << "][" << m_col[o] << "]) : 0ULL;";
+            for (auto &t : tterms[o]) s << " t" << t.first << (t.second < 0 ? " -= K;" : " += K;");
+            s << " }\n";
+        }
+        for (int k = 0; k < NTS; k++) s << " P.ttab[" << k * kPassThreads << " + threadIdx.x] = t" << k << ";\n";
+        s << "}\n";
+    }
     JitPass jp;
     jp.src = s.str();
     jp.param_bytes = L.bytes;
+    jp.n_tslots = NTS;
     return jp;
 }
 
@@ -766,6 +800,11 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             else std::memcpy(row, op.m, 64);
         }
     }
+}
+
+void jit_set_ttab(std::vector<uint8_t> &buf, void *ttab)
+{
+    if (buf.size() >= kOffTtab + 8) std::memcpy(buf.data() + kOffTtab, &ttab, 8);
 }
 
 void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys)
@@ -975,10 +1014,15 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
         }
     }
     if (keys.empty()) return true;
+    std::vector<int> ntab;
     for (const Step *st : steps) {
         std::string k = jit_key(*st);
         auto it = std::find(keys.begin(), keys.end(), k);
-        if (it != keys.end() && srcs.size() == (size_t)(it - keys.begin())) srcs.push_back(jit_generate(*st).src);
+        if (it != keys.end() && srcs.size() == (size_t)(it - keys.begin())) {
+            JitPass jp = jit_generate(*st);
+            srcs.push_back(jp.src);
+            ntab.push_back(jp.n_tslots);
+        }
     }
     auto t0 = std::chrono::steady_clock::now();
     std::vector<std::vector<char>> bins(srcs.size());
@@ -1015,9 +1059,14 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
             return false;
         }
         D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, jit_pipelined() ? 3 * kTileAmps * 16 : kTileAmps * 16);
+        CUfunction tab = nullptr;
+        if (ntab[i] && D.moduleGetFunction(&tab, mod, "qsim_pass_tab") != CUDA_SUCCESS) {
+            err = "cuModuleGetFunction(qsim_pass_tab) failed";
+            return false;
+        }
         std::lock_guard<std::mutex> g(mu_);
         mods_.push_back(mod);
-        fns_[keys[i]] = fn;
+        fns_[keys[i]] = Fn{fn, tab, ntab[i]};
         compiled++;
     }
     compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1072,7 +1121,15 @@ CUfunction JitCache::find(const std::string &key)
 {
     std::lock_guard<std::mutex> g(mu_);
     auto it = fns_.find(key);
-    return it == fns_.end() ? nullptr : it->second;
+    return it == fns_.end() ? nullptr : it->second.pass;
+}
+
+CUfunction JitCache::find_tab(const std::string &key, int &n_tslots)
+{
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = fns_.find(key);
+    n_tslots = it == fns_.end() ? 0 : it->second.n_tslots;
+    return it == fns_.end() ? nullptr : it->second.tab;
 }
 
 size_t JitCache::size()

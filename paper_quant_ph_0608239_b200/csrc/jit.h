@@ -35,6 +35,7 @@ const void *jit_phase_table();
 struct JitPass {
     std::string src;     // generated source (cache key)
     size_t param_bytes;  // size of the parameter block
+    int n_tslots = 0;    // per-thread phase slots the companion kernel qsim_pass_tab fills (0: none)
 };
 
 // Generate the specialised kernel source for a pass step.
@@ -43,14 +44,16 @@ JitPass jit_generate(const Step &st);
 void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf);
 // update the basis-state index a fresh pass (PassDesc::fresh) synthesises
 void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys);
+// device table (n_tslots x kPassThreads uint64) qsim_pass_tab writes and the pass reads
+void jit_set_ttab(std::vector<uint8_t> &buf, void *ttab);
 
 // NVRTC-compile the specialised kernels of `steps` without loading them
 // (host-only check; n = distinct structures)
 bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms);
 
 // Kernel variant: pipelined = persistent CTA per SM, two thread groups on
-// alternate tiles, tiles staged in shared memory by cp.async.bulk (default;
-// QSIM_JIT_PIPE=0 selects one non-persistent CTA per tile, loads to registers).
+// alternate tiles, tiles staged in shared memory by cp.async (QSIM_JIT_PIPE=1;
+// the default is one non-persistent CTA per tile, loads to registers).
 bool jit_pipelined();
 void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, unsigned &smem);
 
@@ -63,13 +66,19 @@ public:
     // parallel host threads); false + err on failure
     bool compile(const std::vector<const Step *> &steps, std::string &err);
     CUfunction find(const std::string &key);
+    // the companion per-thread phase-table kernel of a pass (nullptr: none)
+    CUfunction find_tab(const std::string &key, int &n_tslots);
     size_t size();
     double compile_ms = 0;
     int compiled = 0;
 
 private:
     std::mutex mu_;
-    std::unordered_map<std::string, CUfunction> fns_;
+    struct Fn {
+        CUfunction pass = nullptr, tab = nullptr;
+        int n_tslots = 0;
+    };
+    std::unordered_map<std::string, Fn> fns_;
     std::vector<CUmodule> mods_;
 };
 

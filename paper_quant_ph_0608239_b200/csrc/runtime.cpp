@@ -67,6 +67,8 @@ struct qsim_ctx_s {
     bool plan_cache = true;
     // device program buffers (d_ops: interpreter programs longer than its parameter block)
     KOp *d_ops = nullptr;
+    unsigned long long *d_ttab = nullptr;  // per-thread phase slots of the current JIT pass (qsim_pass_tab)
+    size_t d_ttab_cap = 0;
     size_t d_ops_cap = 0;
     uint32_t *d_perm = nullptr;
     size_t d_perm_cap = 0;
@@ -624,6 +626,9 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
     case ST_PASS: {
         RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
         CUfunction fn = c->jit ? jit_cache().find(pc.jkeys[si]) : nullptr;
+        int nts = 0;
+        CUfunction tabfn = fn ? jit_cache().find_tab(pc.jkeys[si], nts) : nullptr;
+        if (tabfn && (st = ensure_dev(c, c->d_ttab, c->d_ttab_cap, (size_t)nts * kPassThreads)) != QSIM_OK) return st;
         for (int i = 0; i < n_local(c); i++) {
             const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
             if (fn) {
@@ -631,9 +636,19 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
                 if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
                 if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
                 if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
+                if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
                 size_t sz = pp[i].size();
                 void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                                  CU_LAUNCH_PARAM_END};
+                if (tabfn && i == 0) {  // the per-thread phase slots (the same for every shard), once per step
+                    CUresult ct = drv().launchKernel(tabfn, 1, 1, 1, kPassThreads, 1, 1, 0, (CUstream)c->stream,
+                                                     nullptr, extra);
+                    if (ct != CUDA_SUCCESS) {
+                        c->poisoned = true;
+                        FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass table) failed: %d", (int)ct);
+                    }
+                    LAUNCHED(c);
+                }
                 unsigned grid, block, smem;
                 jit_launch_dims(s, c->n_sm, grid, block, smem);
                 CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)c->stream, nullptr,
@@ -999,6 +1014,7 @@ qsim_status qsim_destroy(qsim_ctx c)
         for (double2 *p : c->shards) cudaFree(p);
     if (c->own_scratch) cudaFree(c->scratch);
     if (c->d_ops) cudaFree(c->d_ops);
+    if (c->d_ttab) cudaFree(c->d_ttab);
     if (c->d_perm) cudaFree(c->d_perm);
     if (c->d_red) cudaFree(c->d_red);
     if (c->d_shard_ptrs) cudaFree(c->d_shard_ptrs);
