@@ -229,7 +229,7 @@ typedef struct {
     uint64_t jit_launches;     /* passes run by a pass-specialised (NVRTC) kernel */
     uint64_t jit_kernels;      /* specialised kernels in the process cache */
     double jit_compile_ms;     /* total NVRTC + module-load time in this process */
-    double pass_fp64_slots;    /* algorithmic FP64 FMA-pipe instructions of the launched passes */
+    double pass_fp64_slots;    /* algorithmic FP64 FMA-pipe instructions of the timed passes (timing=1) */
     uint64_t plan_cache_hits;  /* flushes that reused a cached plan */
     uint64_t streamed_steps;   /* plan steps launched while the planner was still running */
 } qsim_stats;

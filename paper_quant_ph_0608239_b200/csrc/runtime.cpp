@@ -666,7 +666,7 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
             }
             LAUNCHED(c);
             c->stats.passes++;
-            c->stats.pass_fp64_slots += pass_fp64_slots(s, M);
+            if (c->timing) c->stats.pass_fp64_slots += pass_fp64_slots(s, M);  // pairs with pass_ms
         }
         break;
     }
