@@ -2,7 +2,10 @@
 // See jit.h.  The generated kernel is the k_pass of kernels.cu with the op
 // loop unrolled at generation time: register bits, predicates and shared-
 // memory re-layouts become constants, the CNOT/Toffoli register swap becomes
-// a renaming, and the matrices are read as constant-bank operands.
+// a renaming, and the matrices are read as constant-bank operands.  Beyond
+// k_pass: deferred predicated swaps folded into store addresses, lazy phase
+// flushes with CTA-uniform / per-thread term slots (qsim_pass_tab), the
+// Hadamard form, the fresh (basis-state) first pass and low-qubit stores.
 #include "jit.h"
 
 #include <cuda_runtime.h>

@@ -5,9 +5,12 @@
 // compiled with NVRTC for sm_100a; the per-pass DATA (matrices, phases,
 // tile bit positions, out-of-tile predicates) travels in the kernel
 // parameter block.  Structures repeat across passes/circuits, so compiled
-// kernels are cached by source text.  Arithmetic is the same expression
-// sequence as the interpreter k_pass, so both tiers give bitwise-identical
-// states.
+// kernels are cached by structure (and on disk by source text).  General
+// gates use the same expression sequence as the interpreter k_pass (bitwise-
+// identical states); phase runs (exact integer angle accumulation per
+// monomial, lazily flushed, CTA-uniform and per-thread terms summed once per
+// tile / launch) and Hadamard-form gates (sum/difference, one scale at the
+// store) round differently and agree to 1e-13.
 #pragma once
 #include <cuda.h>
 
