@@ -322,7 +322,7 @@ void cluster(const std::vector<POp> &ops, const std::vector<char> &used, size_t 
 // Fuse `ops` in place.  cost[i] = FMA-pipe ops per amplitude of ops[i];
 // pair_ok(c) says whether bit c may be one of a block's two qubits.
 template <class PairOk>
-void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pair_ok)
+void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pair_ok, double margin = 2)
 {
     const size_t n = ops.size();
     std::vector<char> used(n, 0);
@@ -348,7 +348,7 @@ void fuse_ops(std::vector<POp> &ops, const std::vector<double> &cost, PairOk pai
         cluster(ops, used, g, mask, true, got);
         double before = 0;
         for (size_t h : got) before += cost[h];
-        if (got.size() < 2 || before <= 16 + 2) continue;  // a 4x4 costs 16 + register copies
+        if (got.size() < 2 || before <= 16 + margin) continue;  // a 4x4 costs 16 + register copies
         cd B[4][4], E[4][4], T[4][4];
         for (int r = 0; r < 4; r++)
             for (int q = 0; q < 4; q++) B[r][q] = r == q ? 1 : 0;
@@ -433,7 +433,7 @@ void fuse_blocks(std::vector<POp> &ops, const int tl_of[64])
 }
 
 // the same fusion on the LOGICAL gate list (qubit numbers as bits)
-std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_blocks_on)
+std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_blocks_on, double margin)
 {
     std::vector<POp> ops(gates.size());
     std::vector<double> cost(gates.size());
@@ -456,7 +456,7 @@ std::vector<GateRec> fuse_gates(const std::vector<GateRec> &gates, uint64_t no_b
         const double touched = std::ldexp(1.0, -(int)g.controls.size());
         cost[i] = (g.cls == CLS_GENERAL ? 8 : g.cls == CLS_XS ? 0 : 4) * touched;
     }
-    fuse_ops(ops, cost, [&](int q) { return !((no_blocks_on >> q) & 1); });
+    fuse_ops(ops, cost, [&](int q) { return !((no_blocks_on >> q) & 1); }, margin);
     std::vector<GateRec> out;
     out.reserve(ops.size());
     for (const POp &p : ops) {
@@ -1133,7 +1133,21 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
     // inside a 4x4 block it would be a non-diagonal target.
     uint64_t no_blocks_on = 0;
     for (int p = M; p < n; p++) no_blocks_on |= bit(qubit_at[p]);
-    const std::vector<GateRec> blocked = fuse_gates(user_gates, no_blocks_on);
+    // Blocks must save FP64 work (cost > 16 + 2) -- unless that leaves most
+    // general one-qubit gates unfused (chain-like circuits, where a U2, CNOT,
+    // U2 cluster costs exactly a block's 16): then break-even blocks are kept
+    // too, because a block needs no re-layout between its gates and packs
+    // more of the circuit into each pass (config-5 family: 15 -> 10 passes).
+    // On a brickwork the strict rule already absorbs every U2 into blocks of
+    // two layers, which break-even blocks would cut apart.
+    auto general_u2 = [](const std::vector<GateRec> &gs) {
+        size_t k = 0;
+        for (const GateRec &g : gs) k += g.kind == GK_U2 && g.controls.empty() && g.cls == CLS_GENERAL;
+        return k;
+    };
+    std::vector<GateRec> blocked = fuse_gates(user_gates, no_blocks_on, 2.0);
+    const size_t u2_before = general_u2(user_gates);
+    if (u2_before && general_u2(blocked) * 4 > u2_before) blocked = fuse_gates(user_gates, no_blocks_on, -0.5);
     if (G == 0) {
         plan_list(blocked, opt, out);
         return;
