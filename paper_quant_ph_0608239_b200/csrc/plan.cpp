@@ -1133,40 +1133,50 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
     // inside a 4x4 block it would be a non-diagonal target.
     uint64_t no_blocks_on = 0;
     for (int p = M; p < n; p++) no_blocks_on |= bit(qubit_at[p]);
-    // Blocks must save FP64 work (cost > 16 + 2) -- unless that leaves most
+    // Blocks must save FP64 work (cost > 16 + 2).  When that leaves most
     // general one-qubit gates unfused (chain-like circuits, where a U2, CNOT,
-    // U2 cluster costs exactly a block's 16): then break-even blocks are kept
-    // too, because a block needs no re-layout between its gates and packs
-    // more of the circuit into each pass (config-5 family: 15 -> 10 passes).
-    // On a brickwork the strict rule already absorbs every U2 into blocks of
-    // two layers, which break-even blocks would cut apart.
+    // U2 cluster costs exactly a block's 16), break-even blocks are tried
+    // too: same FP64 work, but a block needs no re-layout between its gates
+    // and passes hold more of the circuit (config-5 family: 15 -> 10 passes);
+    // on other circuits they can cost passes (a QFT adder: 2 -> 3), so the
+    // cost model decides.  On a brickwork the strict rule already absorbs
+    // every U2 into two-layer blocks and only it is planned.
     auto general_u2 = [](const std::vector<GateRec> &gs) {
         size_t k = 0;
         for (const GateRec &g : gs) k += g.kind == GK_U2 && g.controls.empty() && g.cls == CLS_GENERAL;
         return k;
     };
-    std::vector<GateRec> blocked = fuse_gates(user_gates, no_blocks_on, 2.0);
+    std::vector<std::vector<GateRec>> lists;
+    lists.push_back(fuse_gates(user_gates, no_blocks_on, 2.0));
     const size_t u2_before = general_u2(user_gates);
-    if (u2_before && general_u2(blocked) * 4 > u2_before) blocked = fuse_gates(user_gates, no_blocks_on, -0.5);
-    if (G == 0) {
-        plan_list(blocked, opt, out);
+    if (u2_before && general_u2(lists[0]) * 4 > u2_before) lists.push_back(fuse_gates(user_gates, no_blocks_on, -0.5));
+    // Sharded: tying gates into blocks can change which of them meet a
+    // nonlocal qubit (more exchanges): the unblocked list (build_pass still
+    // fuses inside each pass) is a candidate too.
+    if (G > 0) lists.push_back(user_gates);
+    if (lists.size() == 1) {
+        plan_list(lists[0], opt, out);  // streams its steps (opt.sink)
         return;
     }
-    // Sharded: tying gates into blocks can change which of them meet a
-    // nonlocal qubit (more exchanges); plan both ways (the second keeps the
-    // pass-local fusion of build_pass) and keep the cheaper by the cost model.
     const Planner start = *this;
     PlanOptions o2 = opt;
-    o2.sink = nullptr;  // neither list is final until both are costed
-    std::vector<Step> a, b;
-    plan_list(blocked, o2, a);
-    const Planner after_a = *this;
-    *this = start;
-    plan_list(user_gates, o2, b);
-    const bool take_a = plan_cost(a, M) <= plan_cost(b, M);
-    if (take_a) *this = after_a;
-    std::vector<Step> &pick = take_a ? a : b;
-    for (Step &s : pick) out.push_back(std::move(s));
+    o2.sink = nullptr;  // no list is final until all are costed
+    std::vector<Step> best;
+    Planner after_best = start;
+    double best_cost = 0;
+    for (size_t i = 0; i < lists.size(); i++) {
+        *this = start;
+        std::vector<Step> cand;
+        plan_list(lists[i], o2, cand);
+        const double cost = plan_cost(cand, M);
+        if (i == 0 || cost < best_cost) {
+            best_cost = cost;
+            best.swap(cand);
+            after_best = *this;
+        }
+    }
+    *this = after_best;
+    for (Step &st : best) out.push_back(std::move(st));
     if (opt.sink) opt.sink(out);
 }
 
