@@ -171,6 +171,18 @@ def test_plan_perm_run_fits_shared_memory(pkg, oracle_mod):
     assert [len(s["gates"]) for s in d["plan"]["steps"] if s["type"] == "permrun"] == [12, 8]
 
 
+def test_plan_break_even_blocks(pkg, oracle_mod):
+    """Chain circuits: the strict block rule leaves most U2s unfused, so the
+    planner also plans with break-even blocks and keeps the cheaper plan
+    (fewer passes); the executed plan matches the oracle."""
+    gates = C.random_chain(18, 6, seed=11, sweep=False)
+    d = _check_plan(pkg, oracle_mod, 18, 1, 0, gates)
+    n_pass = sum(s["type"] == "pass" for s in d["plan"]["steps"])
+    strict = json.loads(_plan(pkg, 18, 1, gates, fusion=1 | 0x100))  # no gate-level blocks at all
+    assert n_pass <= sum(s["type"] == "pass" for s in strict["plan"]["steps"])
+    assert sum(op["code"] == 7 for op in _pass_ops(d)) > 0
+
+
 def test_plan_qft_sharded(pkg, oracle_mod):
     w = C.qft_basis(14, 12345)
     d = _check_plan(pkg, oracle_mod, 14, 4, w.init, w.gates)
