@@ -246,7 +246,10 @@ const char *qsim_last_error(qsim_ctx ctx);
  * relabels) into buf.  flags: bits 0-1 = fusion (0 off, 1 on, 2 on + NVRTC-
  * compile the pass kernels as a host-only check); bits 4-5 = global policy
  * + 1 (0 = default auto); bit 8 = no block fusion; bit 9 = no low-qubit
- * remap; bits 12-16 = remap look-ahead + 1 (0 = default 6).  Returns
+ * remap; bit 10 = generate the pass kernels' sources and check that equal
+ * kernel-cache keys mean equal sources (no compile; across every plan checked
+ * in this process; reported under "jit"); bits 12-16 = remap look-ahead + 1
+ * (0 = default 6).  Returns
  * QSIM_ERR_ARG if buf is too small. */
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
                            int flags, char *buf, size_t buf_bytes);

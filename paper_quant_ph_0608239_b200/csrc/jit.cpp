@@ -82,6 +82,14 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
             m_idx[o] = ph_row;
             m_col[o] = ph_col;
             ph_col += 2;
+        } else if (op.code == OPC_DATA) {
+            continue;  // rows 1..3 of an OPC_U4: the U4's own 6 rows hold its 3M constants
+        } else if (op.code == OPC_U4) {
+            m_idx[o] = L.n_m;  // A, -(A+B), B-A: 3 x 16 doubles
+            L.n_m += 6;
+        } else if (op.code == OPC_U2) {
+            m_idx[o] = L.n_m;  // A, -(A+B), B-A: 3 x 4 doubles
+            L.n_m += 2;
         } else {
             m_idx[o] = L.n_m++;
         }
@@ -94,28 +102,12 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
 
 }  // namespace
 
-// pipelined CTAs per SM: 3 staged tiles of 64 KB (12-bit tiles) fit once,
-// of 32 KB (11-bit tiles) twice, in the 227 KB of shared memory
-constexpr int kPipeCtasPerSm = kTileBits >= 12 ? 1 : 2;
-
-bool jit_pipelined()
-{
-    static const bool p = env_int("QSIM_JIT_PIPE", 0) != 0;
-    return p;
-}
-
 void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, unsigned &smem)
 {
-    if (jit_pipelined()) {
-        static const int cap = env_int("QSIM_PASS_GRID", 0);  // testing: fewer CTAs, more tiles each
-        grid = (unsigned)std::min<uint64_t>(st.pass.n_inst, (uint64_t)std::max(1, cap > 0 ? cap : kPipeCtasPerSm * n_sm));
-        block = 2 * kPassThreads;
-        smem = 3 * kTileAmps * 16;
-    } else {
-        grid = (unsigned)st.pass.n_inst;
-        block = kPassThreads;
-        smem = st.pass.use_smem ? kTileAmps * 16 : 0;
-    }
+    (void)n_sm;
+    grid = (unsigned)st.pass.n_inst;
+    block = kPassThreads;
+    smem = st.pass.use_smem ? kTileAmps * 16 : 0;
 }
 
 // An unpredicated Hadamard-form real 2x2, h [[1, 1], [1, -1]]: the JIT tier
@@ -133,9 +125,12 @@ JitPass jit_generate(const Step &st)
     std::vector<int> out_idx, m_idx, m_col;
     Layout L = layout_of(st, out_idx, m_idx, m_col);
     std::ostringstream s;
+    // FP64-pipe instructions per thread the generated code executes (DFMA,
+    // DMUL, DADD and the F64 conversion of qexp), for the roofline
+    double fpc = 0;
+    const int kQexpOps = 13;
     const int minb = env_int("QSIM_JIT_MINB", kPassMinBlocks);  // CTAs per SM (register cap)
-    const bool pipe = jit_pipelined();
-    s << "// minb=" << minb << " pipe=" << pipe << "\n";
+    s << "// minb=" << minb << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long n_inst; "
          "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits
       << "]; unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
@@ -154,85 +149,14 @@ JitPass jit_generate(const Step &st)
          " const double c = fma(x2, fma(x2, fma(x2, -1.3888888888888889e-03, 4.1666666666666664e-02), -0.5), 1.0);\n"
          " const double s = x * fma(x2, fma(x2, 8.3333333333333332e-03, -1.6666666666666666e-01), 1.0);\n"
          " return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));\n}\n";
-    const int NT = kPassThreads, ROWS = kTileAmps / 8;
-    std::string BAR = "__syncthreads();";
-    if (!pipe) {
-        s << "#define TPM P.tpm\n#define TSP P.ts\n#define TPO P.tpo\n";
-        s << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb
-          << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
-        s << " extern __shared__ double2 sm[];\n";
-        s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-        s << " { const unsigned long long inst = blockIdx.x;\n";
-    } else {
-        // Persistent, one CTA per SM, two thread groups of NT threads working on
-        // alternate tiles of this CTA (k = g, g+2, ...).  Tiles are staged in a
-        // ring of 3 shared-memory buffers by cp.async (16 B per thread and
-        // instruction, coalesced 512-B warp requests, written straight into
-        // the swizzled layout), completion tracked by one mbarrier per buffer
-        // (every thread of the issuing group arrives when its copies land).
-        // The group starting tile k issues tile k+1's copies, into the buffer
-        // its own tile k-2 used; the buffer of tile k then serves its
-        // re-layouts (named barrier per group).  So the HBM reads of one tile
-        // overlap the FP64 work and the stores of the others.
-        BAR = "asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + g), \"r\"(" + std::to_string(NT) + ") : \"memory\");";
-        const int JB = kTileBits - kRegBits;  // tile bits of the copy index j (thread covers bits 0..JB-1)
-        s << "__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }\n";
-        s << "__device__ __forceinline__ void issue_tile(const JP &P, unsigned long long inst, unsigned sbuf, unsigned mb, "
-             "int tidv, const volatile unsigned long long *tpmv, const int *tsv)\n{\n"
-             " int tid; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(tid) : \"r\"(tidv));\n"
-             " unsigned long long toff = (unsigned long long)(tid & 7);\n"
-             "#pragma unroll\n for (int b = 3; b < " << JB << "; b++) if ((tid >> b) & 1) toff |= tpmv[b];\n"
-             " const unsigned tsw = (unsigned)(tid ^ (((tid >> 3) ^ (tid >> 6) ^ (tid >> 9)) & 7));\n"
-             " const double2 *src = P.st + (qdep(inst, tsv) | toff);\n"
-             " unsigned long long h[" << kRegBits << "];\n#pragma unroll\n for (int b = 0; b < " << kRegBits << "; b++) h[b] = tpmv[" << JB << " + b];\n"
-          
-             "#pragma unroll\n for (int j = 0; j < " << kAmpsPerThread << "; j++) {\n"
-             "  unsigned long long o = 0;\n"
-             "#pragma unroll\n  for (int b = 0; b < " << kRegBits << "; b++) if ((j >> b) & 1) o |= h[b];\n"
-             "  const int sj = j << " << JB << ";\n"
-             "  const unsigned zj = (unsigned)(sj ^ (((sj >> 3) ^ (sj >> 6) ^ (sj >> 9)) & 7));\n"
-             "  asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sbuf + ((zj ^ tsw) << 4)), "
-             "\"l\"(src + o) : \"memory\");\n"
-             " }\n"
-             " asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(mb) : \"memory\");\n}\n";
-        s << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", " << kPipeCtasPerSm
-          << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
-        s << " extern __shared__ __align__(128) double2 smraw[];\n";
-        // mbarrier of tile k: k % 6 (not k % 3): a group can run one tile ahead
-        // of the other and wait for tile k+1 before it is issued; with 6
-        // barriers that barrier's previous phase (tile k-5) is known complete,
-        // so its parity cannot alias.
-        s << " __shared__ __align__(8) unsigned long long mbar[6];\n";
-        // tile bit positions in shared memory: the loop re-reads them after each
-        // barrier instead of holding (and spilling) copies in registers
-        s << " __shared__ volatile unsigned long long TPM[" << kTileBits << "], TPO[" << kTileBits << "];\n __shared__ int TSP["
-          << kTileBits << "];\n";
-        s << " if (threadIdx.x < " << kTileBits << ") { TPM[threadIdx.x] = P.tpm[threadIdx.x]; TPO[threadIdx.x] = P.tpo[threadIdx.x]; "
-             "TSP[threadIdx.x] = P.ts[threadIdx.x]; }\n";
-        s << " const int g = threadIdx.x / " << NT << ", tid = threadIdx.x % " << NT << ";\n";
-        s << " if (threadIdx.x == 0) {\n"
-             "  for (int i = 0; i < 6; i++) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
-          << ";\" :: \"r\"(su32(&mbar[i])) : \"memory\");\n"
-             "  asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n }\n";
-        s << " __syncthreads();\n";
-        s << " const unsigned long long G = gridDim.x;\n";
-        s << " const unsigned long long ntile = P.n_inst > blockIdx.x ? (P.n_inst - blockIdx.x + G - 1) / G : 0;\n";
-        s << " if (g == 0 && ntile > 0) issue_tile(P, blockIdx.x, su32(smraw), su32(&mbar[0]), tid, TPM, TSP);\n";
-        s << " for (unsigned long long k = g; k < ntile; k += 2) {\n";
-        s << " const int bk = (int)(k % 3);\n";
-        s << " double2 *sm = smraw + bk * " << kTileAmps << ";\n";
-        s << " " << BAR << "\n";
-        s << " if (k + 1 < ntile) { const int bn = (int)((k + 1) % 3); issue_tile(P, blockIdx.x + (k + 1) * G, su32(smraw + bn * "
-          << kTileAmps << "), su32(&mbar[(k + 1) % 6]), tid, TPM, TSP); }\n";
-        s << " { const unsigned mb = su32(&mbar[k % 6]), par = (unsigned)((k / 6) & 1); unsigned done = 0;\n"
-             "   while (!done) asm volatile(\"{\\n .reg .pred p;\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\\n selp.u32 %0, 1, 0, p;\\n}\" "
-             ": \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
-        s << " const unsigned long long inst = blockIdx.x + k * G;\n";
-        // re-derive the thread coordinates every tile (opaque to the compiler):
-        // hoisting the per-config address terms out of the loop spills them
-        s << " int tidk; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(tidk) : \"r\"(tid));\n";
-        s << " const int lane = tidk & 31, warp = tidk >> 5;\n";
-    }
+    const int NT = kPassThreads;
+    const std::string BAR = "__syncthreads();";
+    s << "#define TPM P.tpm\n#define TSP P.ts\n#define TPO P.tpo\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb
+      << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
+    s << " extern __shared__ double2 sm[];\n";
+    s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    s << " { const unsigned long long inst = blockIdx.x;\n";
     s << " const unsigned long long base = qdep(inst, TSP);\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0";
@@ -280,7 +204,7 @@ JitPass jit_generate(const Step &st)
               << " = make_double2(g == P.init_phys ? 1.0 : 0.0, 0.0); " << A(2 * j + 1)
               << " = make_double2((g | 1ULL) == P.init_phys ? 1.0 : 0.0, 0.0); }\n";
         s << " }\n";
-    } else if (!pipe) {
+    } else {
         s << " {\n  const double2 *p = P.st + base + (" << gaddr(cur) << ");\n";
         for (int j = 0; j < kAmpsPerThread / 2; j++)
             s << "  { double x0, x1, x2, x3; asm volatile(\"ld.global.v4.f64 {%0,%1,%2,%3}, [%4];\" : \"=d\"(x0), "
@@ -288,14 +212,6 @@ JitPass jit_generate(const Step &st)
               << roff(cur, j) << "))); " << A(2 * j) << " = make_double2(x0, x1); " << A(2 * j + 1)
               << " = make_double2(x2, x3); }\n";
         s << " }\n";
-    } else {
-        // the staged tile is in the swizzled layout: read it straight into the
-        // config of the first op (a leading re-layout is folded into the read)
-        if (!st.ops.empty() && st.ops[0].code == OPC_TRANS) cur = st.ops[0].cfg;
-        s << " {\n";
-        smem_z(cur, "s");
-        for (int i = 0; i < kAmpsPerThread; i++) s << "  " << A(i) << " = sm[zzs ^ " << zreg(cur, i) << "];\n";
-        s << "  " << BAR << "\n }\n";
     }
     // Deferred predicated swaps.  An exact-X op whose predicate depends on the
     // lane, warp or out-of-tile bits (a CNOT/Toffoli target in a register,
@@ -381,7 +297,7 @@ JitPass jit_generate(const Step &st)
     // epoch) slot, and reduce through shared memory once per tile; the flush
     // of a monomial adds its slot in.  The epochs come from a dry run of the
     // lazy-flush rules below.
-    const size_t o_first = pipe && !st.ops.empty() && st.ops[0].code == OPC_TRANS ? 1 : 0;
+    const size_t o_first = 0;
     auto uniform_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && op.mout && !op.mlane && !op.mwarp; };
     // Per-thread phase terms (a predicate on lane/warp bits only) are the same
     // for every tile: a companion kernel (qsim_pass_tab, one CTA, launched
@@ -395,7 +311,7 @@ JitPass jit_generate(const Step &st)
     {
         int n_uni = 0, n_thr = 0;
         for (const KOp &op : st.ops) { n_uni += uniform_acc(op); n_thr += thread_acc(op); }
-        const bool use_u = !pipe && n_uni >= 8, use_t = !pipe && n_thr >= 8;
+        const bool use_u = n_uni >= 8, use_t = n_thr >= 8;
         if (use_u || use_t) {
             uint32_t sim_live = 0;
             auto sim_flush = [&](uint32_t F) {
@@ -515,15 +431,17 @@ JitPass jit_generate(const Step &st)
                         if ((key >> S) & 1) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
                     s << "  const double2 ex" << k << " = qexp(" << e << ", P.ptab);\n";
                     emitted[k] = 1;
+                    fpc += kQexpOps;
                 }
                 mul("ex" + std::to_string(k), A(i));
+                fpc += 4;
             }
         } else {
             for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                if ((F >> S) & 1) s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n";
+                if ((F >> S) & 1) { s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n"; fpc += kQexpOps; }
             for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++)
                 for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                    if (((F >> S) & 1) && (S & i) == S) mul("em" + std::to_string(S), A(i));
+                    if (((F >> S) & 1) && (S & i) == S) { mul("em" + std::to_string(S), A(i)); fpc += 4; }
         }
         for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
             if ((F >> S) & 1) s << "  mo" << S << " = 0;\n";
@@ -552,70 +470,56 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_PHASE_FLUSH) continue;  // lazy flush (above)
         if (op.code == OPC_DATA) continue;  // rows 1..3 of the preceding OPC_U4
         if (op.code == OPC_U4) {
-            // same FMA chains, in the same order, as kernels.cu u4_apply
+            // 3M form of the complex 4x4: with U = A + iB and
+            // x = p + iq, Re(Ux) = A(p+q) - (A+B)q, Im(Ux) = A(p+q) + (B-A)p.
+            // Per output row 12 FP64 ops (4 for K = A(p+q), 4 + 4 continuing
+            // it) plus one add per amplitude for s = p + q: 13 per amplitude
+            // instead of 16.  The parameter rows hold A, -(A+B) and B-A
+            // (jit_pack_params).
             const int k = op.k, k2 = (int)op.cfg;
             flush(touching((1u << k) | (1u << k2)));
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
             // groups whose chains are emitted interleaved: 2 on passes dominated by
-            // blocks (config 2: -3%), 1 otherwise (register pressure: the chain
-            // circuit's U2-heavy passes ran 6% slower with 2)
+            // blocks, 1 otherwise (register pressure)
             const int il = env_int("QSIM_JIT_U4IL", u4_heavy ? 2 : 1);
-            if (il > 1) {
-                for (int p0 = 0; p0 < kAmpsPerThread / 4; p0 += il) {
-                    s << "  {\n";
-                    std::vector<std::array<int, 4>> gi;
-                    for (int p = p0; p < p0 + il && p < kAmpsPerThread / 4; p++) {
-                        int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
-                        i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
-                        gi.push_back({i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)});
-                    }
-                    for (size_t g = 0; g < gi.size(); g++)
-                        for (int c = 0; c < 4; c++) s << "   const double2 x" << g << "_" << c << " = " << A(gi[g][c]) << ";\n";
-                    for (int c = 0; c < 4; c++)
-                        for (size_t g = 0; g < gi.size(); g++)
-                            for (int r = 0; r < 4; r++) {
-                                const std::string R = "P.m[" + std::to_string(m_idx[o] + r) + "]";
-                                const std::string re = "re" + std::to_string(g) + "_" + std::to_string(r),
-                                                  im = "im" + std::to_string(g) + "_" + std::to_string(r),
-                                                  x = "x" + std::to_string(g) + "_" + std::to_string(c);
-                                if (c == 0)
-                                    s << "   double " << re << " = " << R << "[0] * " << x << ".x, " << im << " = " << R
-                                      << "[0] * " << x << ".y; " << re << " = fma(-" << R << "[1], " << x << ".y, " << re
-                                      << "); " << im << " = fma(" << R << "[1], " << x << ".x, " << im << ");\n";
-                                else
-                                    s << "   " << re << " = fma(" << R << "[" << 2 * c << "], " << x << ".x, " << re << "); "
-                                      << re << " = fma(-" << R << "[" << 2 * c + 1 << "], " << x << ".y, " << re << "); "
-                                      << im << " = fma(" << R << "[" << 2 * c << "], " << x << ".y, " << im << "); " << im
-                                      << " = fma(" << R << "[" << 2 * c + 1 << "], " << x << ".x, " << im << ");\n";
-                            }
-                    for (size_t g = 0; g < gi.size(); g++)
-                        for (int r = 0; r < 4; r++)
-                            s << "   " << A(gi[g][r]) << " = make_double2(re" << g << "_" << r << ", im" << g << "_" << r << ");\n";
-                    s << "  }\n";
+            auto C = [&](int table, int r, int c) {
+                const int idx = table * 16 + r * 4 + c;
+                return "P.m[" + std::to_string(m_idx[o] + (idx >> 3)) + "][" + std::to_string(idx & 7) + "]";
+            };
+            for (int p0 = 0; p0 < kAmpsPerThread / 4; p0 += il) {
+                s << "  {\n";
+                std::vector<std::array<int, 4>> gi;
+                for (int p = p0; p < p0 + il && p < kAmpsPerThread / 4; p++) {
+                    int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
+                    i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
+                    gi.push_back({i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)});
                 }
-                s << " }\n";
-                continue;
-            }
-            for (int p = 0; p < kAmpsPerThread / 4; p++) {
-                int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
-                i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
-                const int idx[4] = {i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)};
-                s << "  { const double2 x0 = " << A(idx[0]) << ", x1 = " << A(idx[1]) << ", x2 = " << A(idx[2])
-                  << ", x3 = " << A(idx[3]) << ";\n";
+                auto nm = [](const char *v, size_t g, int r) { return std::string(v) + std::to_string(g) + "_" + std::to_string(r); };
+                for (size_t g = 0; g < gi.size(); g++)
+                    for (int c = 0; c < 4; c++)
+                        s << "   const double2 " << nm("x", g, c) << " = " << A(gi[g][c]) << "; const double " << nm("s", g, c)
+                          << " = " << nm("x", g, c) << ".x + " << nm("x", g, c) << ".y;\n";
+                // row by row (an output row is written back as soon as it is
+                // formed: x and s are the only long-lived copies)
                 for (int r = 0; r < 4; r++) {
-                    const std::string R = "P.m[" + std::to_string(m_idx[o] + r) + "]";
-                    s << "   { double re = " << R << "[0] * x0.x, im = " << R << "[0] * x0.y; re = fma(-" << R
-                      << "[1], x0.y, re); im = fma(" << R << "[1], x0.x, im);";
-                    for (int c = 1; c < 4; c++)
-                        s << " re = fma(" << R << "[" << 2 * c << "], x" << c << ".x, re); re = fma(-" << R << "["
-                          << 2 * c + 1 << "], x" << c << ".y, re); im = fma(" << R << "[" << 2 * c << "], x" << c
-                          << ".y, im); im = fma(" << R << "[" << 2 * c + 1 << "], x" << c << ".x, im);";
-                    s << " " << A(idx[r]) << " = make_double2(re, im); }\n";
+                    for (size_t g = 0; g < gi.size(); g++) {
+                        const std::string kk = nm("k", g, r), re = nm("re", g, r), im = nm("im", g, r);
+                        s << "   { double " << kk << " = " << C(0, r, 0) << " * " << nm("s", g, 0) << ";";
+                        for (int c = 1; c < 4; c++) s << " " << kk << " = fma(" << C(0, r, c) << ", " << nm("s", g, c) << ", " << kk << ");";
+                        s << "\n     double " << re << " = " << kk << ", " << im << " = " << kk << ";";
+                        for (int c = 0; c < 4; c++) {
+                            const std::string x = nm("x", g, c);
+                            s << " " << re << " = fma(" << C(1, r, c) << ", " << x << ".y, " << re << "); " << im << " = fma("
+                              << C(2, r, c) << ", " << x << ".x, " << im << ");";
+                        }
+                        s << "\n     " << A(gi[g][r]) << " = make_double2(" << re << ", " << im << "); }\n";
+                    }
                 }
                 s << "  }\n";
             }
             s << " }\n";
+            fpc += 13.0 * kAmpsPerThread;
             continue;
         }
         const bool plw = op.mlane || op.mwarp;  // thread-dependent predicate
@@ -642,6 +546,9 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         s << " { // op " << o << " code " << op.code << "\n";
+        // FP64 ops per thread are counted as expected values: a branch on a
+        // CTA-uniform predicate runs in 2^-|mout| of the tiles
+        const double w = pout && !sel ? std::ldexp(1.0, -__builtin_popcountll(op.mout)) : 1.0;
         if (plw || pout) s << "  const bool tp = " << pr.str() << ";\n";
         if (pout && !sel) s << "  if (tp) {\n";
         const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
@@ -667,6 +574,7 @@ JitPass jit_generate(const Step &st)
                 else
                     s << v << ".x = fma(" << F0 << ", " << v << ".x, p1); " << v << ".y = fma(" << F0 << ", " << v
                       << ".y, p2); }\n";
+                fpc += 4 * w;
             }
         } else if (jit_hadamard(op)) {
             const int k = op.k;
@@ -675,8 +583,10 @@ JitPass jit_generate(const Step &st)
                 const std::string x = A(i0), y = A(i1);
                 s << "  { const double2 t = " << x << "; " << x << ".x = t.x + " << y << ".x; " << x << ".y = t.y + "
                   << y << ".y; " << y << ".x = t.x - " << y << ".x; " << y << ".y = t.y - " << y << ".y; }\n";
+                fpc += 4;
             }
             s << "  hs *= " << M << "[0];\n";
+            fpc += 1;
         } else {
             const int k = op.k;
             for (int p = 0; p < kAmpsPerThread / 2; p++) {
@@ -692,18 +602,33 @@ JitPass jit_generate(const Step &st)
                         std::swap(reg[i0], reg[i1]);
                     continue;
                 }
-                std::ostringstream pp;
-                if (op.code == OPC_U2R) {
-                    pp << "const double p1 = " << M << "[2] * " << y << ".x, p2 = " << M << "[2] * " << y << ".y, p3 = "
-                       << M << "[4] * " << x << ".x, p4 = " << M << "[4] * " << x << ".y; ";
-                } else {
-                    pp << "const double p1 = fma(-" << M << "[1], " << x << ".y, fma(" << M << "[2], " << y << ".x, -"
-                       << M << "[3] * " << y << ".y)); const double p2 = fma(" << M << "[1], " << x << ".x, fma(" << M
-                       << "[2], " << y << ".y, " << M << "[3] * " << y << ".x)); const double p3 = fma(" << M << "[4], "
-                       << x << ".x, fma(-" << M << "[5], " << x << ".y, -" << M << "[7] * " << y
-                       << ".y)); const double p4 = fma(" << M << "[4], " << x << ".y, fma(" << M << "[5], " << x
-                       << ".x, " << M << "[7] * " << y << ".x)); ";
+                if (op.code == OPC_U2) {
+                    // 3M form (as OPC_U4): s = p + q, k_r = sum_c A_rc s_c,
+                    // Re = k_r - sum_c (A+B)_rc q_c, Im = k_r + sum_c (B-A)_rc p_c;
+                    // 14 FP64 ops per pair instead of 16.  Parameter row pair:
+                    // [0..3] A, [4..7] -(A+B), [8..11] B-A (jit_pack_params).
+                    auto G = [&](int idx) {
+                        return "P.m[" + std::to_string(m_idx[o] + (idx >> 3)) + "][" + std::to_string(idx & 7) + "]";
+                    };
+                    s << "  { const double s0 = " << x << ".x + " << x << ".y, s1 = " << y << ".x + " << y << ".y; "
+                      << "const double k0 = fma(" << G(1) << ", s1, " << G(0) << " * s0), k1 = fma(" << G(3) << ", s1, "
+                      << G(2) << " * s0); "
+                      << "const double n0 = fma(" << G(4) << ", " << x << ".y, fma(" << G(5) << ", " << y << ".y, k0)); "
+                      << "const double n1 = fma(" << G(8) << ", " << x << ".x, fma(" << G(9) << ", " << y << ".x, k0)); "
+                      << "const double n2 = fma(" << G(6) << ", " << x << ".y, fma(" << G(7) << ", " << y << ".y, k1)); "
+                      << "const double n3 = fma(" << G(10) << ", " << x << ".x, fma(" << G(11) << ", " << y << ".x, k1)); ";
+                    if (sel)
+                        s << x << ".x = tp ? n0 : " << x << ".x; " << x << ".y = tp ? n1 : " << x << ".y; " << y
+                          << ".x = tp ? n2 : " << y << ".x; " << y << ".y = tp ? n3 : " << y << ".y; }\n";
+                    else
+                        s << x << ".x = n0; " << x << ".y = n1; " << y << ".x = n2; " << y << ".y = n3; }\n";
+                    fpc += 14 * w;
+                    continue;
                 }
+                // OPC_U2R
+                std::ostringstream pp;
+                pp << "const double p1 = " << M << "[2] * " << y << ".x, p2 = " << M << "[2] * " << y << ".y, p3 = "
+                   << M << "[4] * " << x << ".x, p4 = " << M << "[4] * " << x << ".y; ";
                 s << "  { " << pp.str();
                 const char *dst[4] = {".x", ".y", ".x", ".y"};
                 const std::string xs[4] = {x, x, y, y};
@@ -721,14 +646,17 @@ JitPass jit_generate(const Step &st)
                           << "); ";
                 }
                 s << "}\n";
+                fpc += 8 * w;
             }
         }
         if (pout && !sel) s << "  }\n";
         s << " }\n";
     }
     flush(live);
-    if (n_had)
+    if (n_had) {
         for (int i = 0; i < kAmpsPerThread; i++) s << " " << A(i) << ".x *= hs; " << A(i) << ".y *= hs;\n";
+        fpc += 2 * kAmpsPerThread;
+    }
     materialize(1);  // register bit 0 lies inside one 256-bit store
     s << " {\n  double2 *p = P.st + base + (" << gaddr(cur, "TPO") << ");\n";
     {
@@ -741,8 +669,6 @@ JitPass jit_generate(const Step &st)
           << ".y) : \"memory\");\n";
     s << " }\n";
     s << " }\n";
-    // a thread must not exit with its copies (for the other group's tile) in flight
-    if (pipe) s << " asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
     s << "}\n";
     const int NTS = (int)tslot_S.size();
     if (NTS) {
@@ -768,6 +694,7 @@ JitPass jit_generate(const Step &st)
     jp.src = s.str();
     jp.param_bytes = L.bytes;
     jp.n_tslots = NTS;
+    jp.fp64_per_thread = fpc;
     return jp;
 }
 
@@ -800,7 +727,20 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             uint8_t *row = b + L.off_m + 64 * m_idx[o];
             if (op.code == OPC_PHASE_ACC) std::memcpy(row + 8 * m_col[o], &op.cfg, 8);       // angle
             else if (op.code == OPC_PHASE) std::memcpy(row + 8 * m_col[o], op.m, 16);       // f
-            else std::memcpy(row, op.m, 64);
+            else if (op.code == OPC_U4 || op.code == OPC_U2) {
+                // 3M constants of U = A + iB: A, -(A+B), B-A (row-major entries)
+                const int dim = op.code == OPC_U4 ? 4 : 2;
+                double c[48];
+                for (int r = 0; r < dim; r++)
+                    for (int q = 0; q < dim; q++) {
+                        const double *m = op.code == OPC_U4 ? st.ops[o + r].m + 2 * q : op.m + 2 * (r * 2 + q);
+                        const int e = r * dim + q, D2 = dim * dim;
+                        c[e] = m[0];
+                        c[D2 + e] = -(m[0] + m[1]);
+                        c[2 * D2 + e] = m[1] - m[0];
+                    }
+                std::memcpy(row, c, 8 * 3 * dim * dim);
+            } else std::memcpy(row, op.m, 64);
         }
     }
 }
@@ -991,13 +931,19 @@ std::string jit_key(const Step &st)
 {
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
-    put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) | ((uint64_t)jit_pipelined() << 16) |
+    put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) |
         ((uint64_t)(st.pass.fresh != 0) << 48) |
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
-    for (const KOp &op : st.ops) {
+    // the generated source indexes the deduplicated out-of-tile predicates
+    // (P.out[out_idx[o]], and n_out sizes the parameter struct): the dedup
+    // pattern is part of the structure, not only whether an op has one
+    std::vector<int> out_idx, m_idx, m_col;
+    layout_of(st, out_idx, m_idx, m_col);
+    for (size_t o = 0; o < st.ops.size(); o++) {
+        const KOp &op = st.ops[o];
         put((uint64_t)op.code | ((uint64_t)op.k << 8) | ((uint64_t)(op.mout != 0) << 16) |
-            ((uint64_t)jit_hadamard(op) << 17));
+            ((uint64_t)jit_hadamard(op) << 17) | ((uint64_t)(uint32_t)(out_idx[o] + 1) << 32));
         put((uint64_t)op.mreg | ((uint64_t)op.vreg << 8) | ((uint64_t)op.mlane << 16) | ((uint64_t)op.vlane << 24) |
             ((uint64_t)op.mwarp << 32) | ((uint64_t)op.vwarp << 40));
         if (op.code == OPC_TRANS || op.code == OPC_U4) put(op.cfg);
@@ -1018,6 +964,7 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
     }
     if (keys.empty()) return true;
     std::vector<int> ntab;
+    std::vector<double> fps;
     for (const Step *st : steps) {
         std::string k = jit_key(*st);
         auto it = std::find(keys.begin(), keys.end(), k);
@@ -1025,6 +972,7 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
             JitPass jp = jit_generate(*st);
             srcs.push_back(jp.src);
             ntab.push_back(jp.n_tslots);
+            fps.push_back(jp.fp64_per_thread);
         }
     }
     auto t0 = std::chrono::steady_clock::now();
@@ -1061,7 +1009,7 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
             err = "cuModuleLoadData/cuModuleGetFunction failed";
             return false;
         }
-        D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, jit_pipelined() ? 3 * kTileAmps * 16 : kTileAmps * 16);
+        D.funcSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, kTileAmps * 16);
         CUfunction tab = nullptr;
         if (ntab[i] && D.moduleGetFunction(&tab, mod, "qsim_pass_tab") != CUDA_SUCCESS) {
             err = "cuModuleGetFunction(qsim_pass_tab) failed";
@@ -1069,7 +1017,7 @@ bool JitCache::compile(const std::vector<const Step *> &steps, std::string &err)
         }
         std::lock_guard<std::mutex> g(mu_);
         mods_.push_back(mod);
-        fns_[keys[i]] = Fn{fn, tab, ntab[i]};
+        fns_[keys[i]] = Fn{fn, tab, ntab[i], fps[i]};
         compiled++;
     }
     compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1087,17 +1035,39 @@ static void dump_source(const std::string &src, size_t idx)
     }
 }
 
-bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms)
+bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms, bool compile,
+                      std::vector<double> *fp64_per_amp)
 {
+    // process-wide key -> source record: equal keys must mean equal sources
+    // (the kernel cache is keyed by jit_key), across every plan checked here
+    static std::mutex seen_mu;
+    static std::unordered_map<std::string, std::string> seen;
     auto t0 = std::chrono::steady_clock::now();
     std::vector<std::string> keys, srcs;
     for (size_t i = 0; i < steps.size(); i++) {
         const Step *st = steps[i];
         std::string k = jit_key(*st);
-        dump_source(jit_generate(*st).src, i);
+        JitPass jp = jit_generate(*st);
+        std::string src = std::move(jp.src);
+        if (fp64_per_amp) fp64_per_amp->push_back(jp.fp64_per_thread / kAmpsPerThread);
+        dump_source(src, i);
+        {
+            std::lock_guard<std::mutex> g(seen_mu);
+            auto it = seen.find(k);
+            if (it == seen.end()) seen.emplace(k, src);
+            else if (it->second != src) {
+                err = "jit key collision: pass " + std::to_string(i) + " has the key of a different source";
+                return false;
+            }
+        }
         if (std::find(keys.begin(), keys.end(), k) != keys.end()) continue;
         keys.push_back(k);
-        srcs.push_back(jit_generate(*st).src);
+        srcs.push_back(std::move(src));
+    }
+    n = (int)srcs.size();
+    if (!compile) {
+        ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return true;
     }
     std::vector<std::vector<char>> bins(srcs.size());
     std::vector<std::string> logs(srcs.size());
@@ -1110,7 +1080,6 @@ bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, 
             for (size_t i; (i = next++) < srcs.size();) ok[i] = nvrtc_compile(srcs[i], bins[i], logs[i]);
         });
     for (auto &t : th) t.join();
-    n = (int)srcs.size();
     ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (size_t i = 0; i < srcs.size(); i++)
         if (!ok[i]) {
@@ -1133,6 +1102,13 @@ CUfunction JitCache::find_tab(const std::string &key, int &n_tslots)
     auto it = fns_.find(key);
     n_tslots = it == fns_.end() ? 0 : it->second.n_tslots;
     return it == fns_.end() ? nullptr : it->second.tab;
+}
+
+double JitCache::fp64_per_thread(const std::string &key)
+{
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = fns_.find(key);
+    return it == fns_.end() ? -1.0 : it->second.fp64;
 }
 
 size_t JitCache::size()

@@ -39,6 +39,7 @@ struct JitPass {
     std::string src;     // generated source (cache key)
     size_t param_bytes;  // size of the parameter block
     int n_tslots = 0;    // per-thread phase slots the companion kernel qsim_pass_tab fills (0: none)
+    double fp64_per_thread = 0;  // FP64-pipe instructions one thread executes per tile (expected value)
 };
 
 // Generate the specialised kernel source for a pass step.
@@ -52,12 +53,13 @@ void jit_set_ttab(std::vector<uint8_t> &buf, void *ttab);
 
 // NVRTC-compile the specialised kernels of `steps` without loading them
 // (host-only check; n = distinct structures)
-bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms);
+// compile=false: generate only.  Either way, fails on a jit_key collision
+// (two different sources under one key, across all plans checked in this process).
+// fp64_per_amp: FP64-pipe instructions per amplitude of each step's kernel.
+bool jit_compile_only(const std::vector<const Step *> &steps, std::string &err, int &n, double &ms,
+                      bool compile = true, std::vector<double> *fp64_per_amp = nullptr);
 
-// Kernel variant: pipelined = persistent CTA per SM, two thread groups on
-// alternate tiles, tiles staged in shared memory by cp.async (QSIM_JIT_PIPE=1;
-// the default is one non-persistent CTA per tile, loads to registers).
-bool jit_pipelined();
+// Launch shape: one non-persistent CTA per 2^12-amplitude tile, loads to registers.
 void jit_launch_dims(const Step &st, int n_sm, unsigned &grid, unsigned &block, unsigned &smem);
 
 // structural key of a pass (what the generated source depends on)
@@ -71,6 +73,8 @@ public:
     CUfunction find(const std::string &key);
     // the companion per-thread phase-table kernel of a pass (nullptr: none)
     CUfunction find_tab(const std::string &key, int &n_tslots);
+    // FP64-pipe instructions per thread and tile of a cached kernel (-1: not cached)
+    double fp64_per_thread(const std::string &key);
     size_t size();
     double compile_ms = 0;
     int compiled = 0;
@@ -80,6 +84,7 @@ private:
     struct Fn {
         CUfunction pass = nullptr, tab = nullptr;
         int n_tslots = 0;
+        double fp64 = 0;  // JitPass::fp64_per_thread
     };
     std::unordered_map<std::string, Fn> fns_;
     std::vector<CUmodule> mods_;

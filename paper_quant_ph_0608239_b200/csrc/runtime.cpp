@@ -133,10 +133,12 @@ struct qsim_ctx_s {
         (ctx)->stats.kernel_launches++;                                                       \
     } while (0)
 
-// algorithmic FP64 FMA-pipe instructions of one pass over a 2^M shard: per
-// touched amplitude 8 for a complex 2x2, 4 for a real 2x2, 4 for a phase,
-// 0 for an exact swap, 16 for a fused 4x4 block; the predicate bits (controls)
-// halve the touched set
+// FP64-pipe instructions the interpreter tier k_pass executes on one pass
+// over a 2^M shard: per touched amplitude 8 for a complex 2x2, 4 for a real
+// 2x2, 4 for a phase (OPC_PHASE_ACC is applied like OPC_PHASE there), 0 for
+// an exact swap, 16 for a fused 4x4 block; the predicate bits (controls)
+// halve the touched set.  The JIT tier's count comes from its generator
+// (JitPass::fp64_per_thread: 3M blocks, integer phase runs, lazy flushes).
 static double pass_fp64_slots(const Step &s, int M)
 {
     double tot = 0;
@@ -666,7 +668,10 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
             }
             LAUNCHED(c);
             c->stats.passes++;
-            if (c->timing) c->stats.pass_fp64_slots += pass_fp64_slots(s, M);  // pairs with pass_ms
+            if (c->timing) {  // executed FP64-pipe instructions, pairs with pass_ms
+                const double fpt = fn ? jit_cache().fp64_per_thread(pc.jkeys[si]) : -1.0;
+                c->stats.pass_fp64_slots += fpt >= 0 ? fpt * kPassThreads * (double)s.pass.n_inst : pass_fp64_slots(s, M);
+            }
         }
         break;
     }
@@ -1438,18 +1443,21 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     P.plan(recs, opt, steps);
     const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
     std::string jit_info;
-    if ((fusion & 3) == 2) {  // also NVRTC-compile the pass-specialised kernels (host-only check)
+    if ((fusion & 3) == 2 || (fusion & 0x400)) {  // NVRTC-compile (2) or only generate + key-check (bit 10) the pass kernels
         std::vector<const Step *> ps;
         for (const Step &s : steps)
             if (s.type == ST_PASS) ps.push_back(&s);
         std::string err;
         int nk = 0;
         double ms = 0;
-        bool ok = jit_compile_only(ps, err, nk, ms);
+        std::vector<double> fpa;
+        bool ok = jit_compile_only(ps, err, nk, ms, (fusion & 3) == 2, &fpa);
+        std::string fps;
+        for (size_t i = 0; i < fpa.size(); i++) fps += (i ? "," : "") + std::to_string(fpa[i]);
         std::string e;
         for (char ch : err) e += (ch == '"' || ch == '\\') ? ' ' : (ch == '\n' ? ' ' : ch);
         jit_info = ",\"jit\":{\"ok\":" + std::string(ok ? "true" : "false") + ",\"kernels\":" + std::to_string(nk) +
-                   ",\"compile_ms\":" + std::to_string(ms) + ",\"error\":\"" + e + "\"}";
+                   ",\"compile_ms\":" + std::to_string(ms) + ",\"fp64_per_amp\":[" + fps + "],\"error\":\"" + e + "\"}";
     }
     std::string js = init + plan_to_json(P, steps) + jit_info + ",\"plan_ms\":" + std::to_string(plan_ms) + "}";
     if (js.size() + 1 > buf_bytes) return QSIM_ERR_ARG;

@@ -298,3 +298,30 @@ def test_c_client_runs(pkg, tmp_path):
     r = subprocess.run([_build_c_client(pkg, tmp_path)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr + r.stdout
     assert "abi_client ok" in r.stdout
+
+
+def test_jit_key_implies_same_source(pkg):
+    """The pass-kernel cache is keyed by jit_key: two passes that
+    differ only in whether two ops share an out-of-tile control (one deduplicated
+    (mout, vout) predicate vs two) generate different sources, so they must not
+    share a key.  The planner's key check compares the generated source of every
+    pass against every earlier pass with the same key, across all plans below."""
+    rng = G.SplitMix64(11)
+    n = 16
+    base = [G.one_q(q, G.haar_u2(rng)) for q in range(4)]
+    shared = base + [G.ctrl([15], 0, G.haar_u2(rng)), G.ctrl([15], 1, G.haar_u2(rng))]
+    distinct = base + [G.ctrl([15], 0, G.haar_u2(rng)), G.ctrl([14], 1, G.haar_u2(rng))]
+    for gates in (shared, distinct, shared[::-1], distinct[::-1]):
+        js = json.loads(pkg.plan_json(n, 1, gates, key_check=True))
+        assert js["jit"]["ok"], js["jit"]["error"]
+    # the wider fuzz: circuits of every gate kind with out-of-tile controls
+    for seed in range(6):
+        gates = C.random_chain(n, 3, seed=seed, sweep=False)
+        r = G.SplitMix64(100 + seed)
+        for k in range(12):
+            c = [12 + (k + seed) % 4] + ([13 + (k * 3 + seed) % 3] if k % 3 == 0 else [])
+            c = sorted(set(c))
+            gates.append(G.ctrl(c, k % 12, G.haar_u2(r)))
+            gates.append(G.cphase(12 + (k + 2 * seed) % 4, k % 12, 0.1 * k + 0.05))
+        js = json.loads(pkg.plan_json(n, 1, gates, key_check=True))
+        assert js["jit"]["ok"], js["jit"]["error"]

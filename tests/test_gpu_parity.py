@@ -94,17 +94,17 @@ def test_every_gate_every_position(P, oracle_mod, n, fusion):
 
 @pytest.mark.parametrize("n,ranks", [(13, 1), (16, 1), (15, 4)])
 def test_jit_tier_matches_interpreter(P, oracle_mod, n, ranks):
-    """The NVRTC pass-specialised kernels and the interpreter k_pass: identical
-    bits on a circuit without phase runs (same expression sequence); with
-    phase runs the JIT tier accumulates exact integer angles (one sincospi per
-    amplitude) and the two agree to 1e-13; both match the oracle."""
+    """The NVRTC pass-specialised kernels and the interpreter k_pass.  They
+    round differently (the JIT tier applies general 2x2 and 4x4 blocks in the
+    3M form, accumulates exact integer phase angles and applies Hadamards as
+    sums/differences) and agree to 1e-13; both match the oracle."""
     plain = C.random_brickwork(n, 4, seed=n)
     s_int = gpu_run(P, n, 1, plain, ranks=ranks, jit=0)
     s_jit = gpu_run(P, n, 1, plain, ranks=ranks, jit=1)
     a_int, a_jit = s_int.get_amplitudes(), s_jit.get_amplitudes()
     assert s_jit.stats()["jit_launches"] > 0, s_jit.lib.qsim_last_error(s_jit.ctx).decode()[:3000]
     assert s_int.stats()["jit_launches"] == 0
-    assert np.array_equal(a_int, a_jit)
+    assert np.max(np.abs(a_int - a_jit)) <= 1e-13
     gates = kitchen_sink(n, seed=7 * n) + C.qft_ladder(list(range(n)), True) + plain
     s_int = gpu_run(P, n, 1, gates, ranks=ranks, jit=0)
     s_jit = gpu_run(P, n, 1, gates, ranks=ranks, jit=1)
