@@ -86,7 +86,11 @@ typedef enum {
     QSIM_TRANSPORT_LOCAL = 0,    /* one shard on the current device (P must be 1) */
     QSIM_TRANSPORT_VIRTUAL = 1,  /* P shards, all on the current device, exchanged by
                                     device copies: a test backend for the sharded path */
-    QSIM_TRANSPORT_NCCL = 2      /* one process per GPU, shard exchanges over NCCL */
+    QSIM_TRANSPORT_NCCL = 2,     /* one process per GPU, shard exchanges over NCCL */
+    QSIM_TRANSPORT_LOOPBACK = 3  /* SPMD ranks as host threads of ONE process on ONE device:
+                                    the NCCL transport's exchange / readout code with each
+                                    send-recv pair a device copy (comm id from
+                                    qsim_get_loopback_id); tests the SPMD path on one GPU */
 } qsim_transport;
 
 /* Creation parameters.  Device buffers and the stream may be supplied by the
@@ -98,7 +102,12 @@ typedef enum {
  *                 qsim_scratch_bytes() returns the recommended size
  *   stream      : cudaStream_t to enqueue all work on
  *   nccl_id     : 128-byte ncclUniqueId from qsim_get_unique_id on rank 0,
- *                 broadcast to all ranks by the caller (NCCL transport) */
+ *                 broadcast to all ranks by the caller (NCCL transport), or
+ *                 the id from qsim_get_loopback_id (LOOPBACK transport)
+ * SPMD transports (NCCL, LOOPBACK): every rank makes the same sequence of
+ * calls.  A rank that waits longer than the communication timeout (option
+ * "comm_timeout_ms", env QSIM_COMM_TIMEOUT_S; default 600 s) for its peers
+ * aborts the communicator and returns QSIM_ERR_COMM (context poisoned). */
 typedef struct {
     int32_t n_qubits;   /* 1 <= n <= 62 */
     int32_t n_ranks;    /* P in {1,2,4,...,64}, power of two, n - log2 P >= 1 */
@@ -131,6 +140,9 @@ qsim_status qsim_create_rank(int n_qubits, int n_gpus, int rank, const void *ncc
 size_t qsim_scratch_bytes(int n_qubits, int n_ranks);
 /* ncclUniqueId (128 bytes) for rank 0 to broadcast. */
 qsim_status qsim_get_unique_id(void *out128);
+/* Id (128 bytes) of a new loopback group: every rank's qsim_config.nccl_id
+ * carries it (QSIM_TRANSPORT_LOOPBACK). */
+qsim_status qsim_get_loopback_id(void *out128);
 qsim_status qsim_destroy(qsim_ctx ctx);
 
 /* |index> (INITIAL STATE).  Lazy: the initial sigma is chosen by
@@ -205,8 +217,10 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * generic kernel per gate), "block_fusion" (1 = inside a pass, gate clusters
  * on two tile qubits become one 4x4 unitary and one-qubit runs one 2x2
  * [default]; 0 = every gate applied as given), "timing" (1 = CUDA-event time
- * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb",
- * "jit", "plan_cache", "pass_variant", "global_policy". */
+ * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb"
+ * (exchange piece cap; the pieces are double-buffered between the engine
+ * stream and a transfer stream), "comm_timeout_ms", "jit", "plan_cache",
+ * "pass_variant", "global_policy". */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {

@@ -10,7 +10,7 @@ LIB_PATH = os.environ.get("QSIM_LIB") or os.path.join(HERE, "libqsim_b200.so")
 
 QSIM_MAX_CONTROLS = 8
 QSIM_MAX_PERM_TARGETS = 12
-TRANSPORT_LOCAL, TRANSPORT_VIRTUAL, TRANSPORT_NCCL = 0, 1, 2
+TRANSPORT_LOCAL, TRANSPORT_VIRTUAL, TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1, 2, 3
 
 STATUS = ["QSIM_OK", "QSIM_ERR_ARG", "QSIM_ERR_QUBIT_RANGE", "QSIM_ERR_DUP_QUBIT", "QSIM_ERR_NOT_UNITARY",
           "QSIM_ERR_NOT_PERMUTATION", "QSIM_ERR_OOM", "QSIM_ERR_CUDA", "QSIM_ERR_COMM", "QSIM_ERR_STATE",
@@ -52,7 +52,8 @@ class qsim_stats(ctypes.Structure):
 
 
 EXPORTS = [
-    "qsim_create", "qsim_create_ext", "qsim_create_rank", "qsim_scratch_bytes", "qsim_get_unique_id", "qsim_destroy",
+    "qsim_create", "qsim_create_ext", "qsim_create_rank", "qsim_scratch_bytes", "qsim_get_unique_id",
+    "qsim_get_loopback_id", "qsim_destroy",
     "qsim_init_basis", "qsim_apply_1q", "qsim_apply_controlled", "qsim_apply_perm", "qsim_apply_swap",
     "qsim_remap", "qsim_run_circuit", "qsim_probabilities", "qsim_expectations", "qsim_expectations_async",
     "qsim_measure",
@@ -81,6 +82,7 @@ def lib():
                               ctypes.c_size_t, ctypes.c_void_p, P(ctx)], st),
         "qsim_scratch_bytes": ([i, i], ctypes.c_size_t),
         "qsim_get_unique_id": ([ctypes.c_void_p], st),
+        "qsim_get_loopback_id": ([ctypes.c_void_p], st),
         "qsim_destroy": ([ctx], st),
         "qsim_init_basis": ([ctx, u64], st),
         "qsim_apply_1q": ([ctx, i, P(c128)], st),

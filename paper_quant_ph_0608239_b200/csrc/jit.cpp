@@ -50,6 +50,25 @@ int env_int(const char *k, int dflt)
     return v ? atoi(v) : dflt;
 }
 
+// Arithmetic form of general 2x2 (OPC_U2) and 4x4 (OPC_U4) blocks in a pass:
+// the 3M form (fewer FP64 instructions, three live copies of every input
+// amplitude) or the direct complex FMA form (two).  QSIM_JIT_3M (A/B switch,
+// read once): bit 0 = 3M for U2, bit 1 = 3M for U4; default auto.
+struct Forms {
+    bool u2 = true, u4 = true;
+};
+Forms forms_of(const Step &st)
+{
+    static const int env = env_int("QSIM_JIT_3M", -1);
+    Forms f;
+    if (env >= 0) {
+        f.u2 = env & 1;
+        f.u4 = (env >> 1) & 1;
+        return f;
+    }
+    return f;
+}
+
 // Parameter block: out-of-tile predicates (mout, vout) deduplicated by value;
 // matrix rows of 8 doubles: a U2 takes a row, a U4 its row and its 3 OPC_DATA
 // rows; phases share rows (a multiplier takes 2 doubles, an accumulated
@@ -58,6 +77,7 @@ int env_int(const char *k, int dflt)
 Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_idx, std::vector<int> &m_col)
 {
     Layout L;
+    const Forms fm = forms_of(st);
     out_idx.assign(st.ops.size(), -1);
     m_idx.assign(st.ops.size(), -1);
     m_col.assign(st.ops.size(), 0);
@@ -82,12 +102,12 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
             m_idx[o] = ph_row;
             m_col[o] = ph_col;
             ph_col += 2;
-        } else if (op.code == OPC_DATA) {
+        } else if (op.code == OPC_DATA && fm.u4) {
             continue;  // rows 1..3 of an OPC_U4: the U4's own 6 rows hold its 3M constants
-        } else if (op.code == OPC_U4) {
+        } else if (op.code == OPC_U4 && fm.u4) {
             m_idx[o] = L.n_m;  // A, -(A+B), B-A: 3 x 16 doubles
             L.n_m += 6;
-        } else if (op.code == OPC_U2) {
+        } else if (op.code == OPC_U2 && fm.u2) {
             m_idx[o] = L.n_m;  // A, -(A+B), B-A: 3 x 4 doubles
             L.n_m += 2;
         } else {
@@ -124,6 +144,7 @@ JitPass jit_generate(const Step &st)
 {
     std::vector<int> out_idx, m_idx, m_col;
     Layout L = layout_of(st, out_idx, m_idx, m_col);
+    const Forms fm = forms_of(st);
     std::ostringstream s;
     // FP64-pipe instructions per thread the generated code executes (DFMA,
     // DMUL, DADD and the F64 conversion of qexp), for the roofline
@@ -469,6 +490,49 @@ JitPass jit_generate(const Step &st)
         }
         if (op.code == OPC_PHASE_FLUSH) continue;  // lazy flush (above)
         if (op.code == OPC_DATA) continue;  // rows 1..3 of the preceding OPC_U4
+        if (op.code == OPC_U4 && !fm.u4) {
+            // direct form: each output one 8-long FMA chain for re and for im
+            const int k = op.k, k2 = (int)op.cfg;
+            flush(touching((1u << k) | (1u << k2)));
+            materialize((1u << k) | (1u << k2));
+            s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
+            const int il = env_int("QSIM_JIT_U4IL", u4_heavy ? 2 : 1);
+            for (int p0 = 0; p0 < kAmpsPerThread / 4; p0 += il) {
+                s << "  {\n";
+                std::vector<std::array<int, 4>> gi;
+                for (int p = p0; p < p0 + il && p < kAmpsPerThread / 4; p++) {
+                    int i0 = ((p >> k) << (k + 1)) | (p & ((1 << k) - 1));
+                    i0 = ((i0 >> k2) << (k2 + 1)) | (i0 & ((1 << k2) - 1));
+                    gi.push_back({i0, i0 | (1 << k), i0 | (1 << k2), i0 | (1 << k) | (1 << k2)});
+                }
+                for (size_t g = 0; g < gi.size(); g++)
+                    for (int c = 0; c < 4; c++) s << "   const double2 x" << g << "_" << c << " = " << A(gi[g][c]) << ";\n";
+                for (int c = 0; c < 4; c++)
+                    for (size_t g = 0; g < gi.size(); g++)
+                        for (int r = 0; r < 4; r++) {
+                            const std::string R = "P.m[" + std::to_string(m_idx[o] + r) + "]";
+                            const std::string re = "re" + std::to_string(g) + "_" + std::to_string(r),
+                                              im = "im" + std::to_string(g) + "_" + std::to_string(r),
+                                              x = "x" + std::to_string(g) + "_" + std::to_string(c);
+                            if (c == 0)
+                                s << "   double " << re << " = " << R << "[0] * " << x << ".x, " << im << " = " << R
+                                  << "[0] * " << x << ".y; " << re << " = fma(-" << R << "[1], " << x << ".y, " << re
+                                  << "); " << im << " = fma(" << R << "[1], " << x << ".x, " << im << ");\n";
+                            else
+                                s << "   " << re << " = fma(" << R << "[" << 2 * c << "], " << x << ".x, " << re << "); "
+                                  << re << " = fma(-" << R << "[" << 2 * c + 1 << "], " << x << ".y, " << re << "); "
+                                  << im << " = fma(" << R << "[" << 2 * c << "], " << x << ".y, " << im << "); " << im
+                                  << " = fma(" << R << "[" << 2 * c + 1 << "], " << x << ".x, " << im << ");\n";
+                        }
+                for (size_t g = 0; g < gi.size(); g++)
+                    for (int r = 0; r < 4; r++)
+                        s << "   " << A(gi[g][r]) << " = make_double2(re" << g << "_" << r << ", im" << g << "_" << r << ");\n";
+                s << "  }\n";
+            }
+            s << " }\n";
+            fpc += 16.0 * kAmpsPerThread;
+            continue;
+        }
         if (op.code == OPC_U4) {
             // 3M form of the complex 4x4: with U = A + iB and
             // x = p + iq, Re(Ux) = A(p+q) - (A+B)q, Im(Ux) = A(p+q) + (B-A)p.
@@ -480,9 +544,11 @@ JitPass jit_generate(const Step &st)
             flush(touching((1u << k) | (1u << k2)));
             materialize((1u << k) | (1u << k2));
             s << " { // op " << o << " U4 (" << k << "," << k2 << ")\n";
-            // groups whose chains are emitted interleaved: 2 on passes dominated by
-            // blocks, 1 otherwise (register pressure)
-            const int il = env_int("QSIM_JIT_U4IL", u4_heavy ? 2 : 1);
+            // groups whose rows are emitted interleaved.  The 3M form holds three
+            // copies of a group's inputs: on passes dominated by blocks one group
+            // at a time (config 2: 0.331 vs 0.352 ms/pass with 2), else two
+            // (chain circuits: 2 slightly ahead)
+            const int il = env_int("QSIM_JIT_U4IL", u4_heavy ? 1 : 2);
             auto C = [&](int table, int r, int c) {
                 const int idx = table * 16 + r * 4 + c;
                 return "P.m[" + std::to_string(m_idx[o] + (idx >> 3)) + "][" + std::to_string(idx & 7) + "]";
@@ -602,7 +668,7 @@ JitPass jit_generate(const Step &st)
                         std::swap(reg[i0], reg[i1]);
                     continue;
                 }
-                if (op.code == OPC_U2) {
+                if (op.code == OPC_U2 && fm.u2) {
                     // 3M form (as OPC_U4): s = p + q, k_r = sum_c A_rc s_c,
                     // Re = k_r - sum_c (A+B)_rc q_c, Im = k_r + sum_c (B-A)_rc p_c;
                     // 14 FP64 ops per pair instead of 16.  Parameter row pair:
@@ -625,10 +691,19 @@ JitPass jit_generate(const Step &st)
                     fpc += 14 * w;
                     continue;
                 }
-                // OPC_U2R
+                // OPC_U2R, or OPC_U2 in the direct form
                 std::ostringstream pp;
-                pp << "const double p1 = " << M << "[2] * " << y << ".x, p2 = " << M << "[2] * " << y << ".y, p3 = "
-                   << M << "[4] * " << x << ".x, p4 = " << M << "[4] * " << x << ".y; ";
+                if (op.code == OPC_U2R) {
+                    pp << "const double p1 = " << M << "[2] * " << y << ".x, p2 = " << M << "[2] * " << y << ".y, p3 = "
+                       << M << "[4] * " << x << ".x, p4 = " << M << "[4] * " << x << ".y; ";
+                } else {
+                    pp << "const double p1 = fma(-" << M << "[1], " << x << ".y, fma(" << M << "[2], " << y << ".x, -"
+                       << M << "[3] * " << y << ".y)); const double p2 = fma(" << M << "[1], " << x << ".x, fma(" << M
+                       << "[2], " << y << ".y, " << M << "[3] * " << y << ".x)); const double p3 = fma(" << M << "[4], "
+                       << x << ".x, fma(-" << M << "[5], " << x << ".y, -" << M << "[7] * " << y
+                       << ".y)); const double p4 = fma(" << M << "[4], " << x << ".y, fma(" << M << "[5], " << x
+                       << ".x, " << M << "[7] * " << y << ".x)); ";
+                }
                 s << "  { " << pp.str();
                 const char *dst[4] = {".x", ".y", ".x", ".y"};
                 const std::string xs[4] = {x, x, y, y};
@@ -646,7 +721,7 @@ JitPass jit_generate(const Step &st)
                           << "); ";
                 }
                 s << "}\n";
-                fpc += 8 * w;
+                fpc += (op.code == OPC_U2R ? 8 : 16) * w;
             }
         }
         if (pout && !sel) s << "  }\n";
@@ -702,6 +777,7 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
 {
     std::vector<int> out_idx, m_idx, m_col;
     Layout L = layout_of(st, out_idx, m_idx, m_col);
+    const Forms fm = forms_of(st);
     buf.assign(L.bytes, 0);
     uint8_t *b = buf.data();
     std::memcpy(b + 0, &state, 8);
@@ -727,7 +803,7 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
             uint8_t *row = b + L.off_m + 64 * m_idx[o];
             if (op.code == OPC_PHASE_ACC) std::memcpy(row + 8 * m_col[o], &op.cfg, 8);       // angle
             else if (op.code == OPC_PHASE) std::memcpy(row + 8 * m_col[o], op.m, 16);       // f
-            else if (op.code == OPC_U4 || op.code == OPC_U2) {
+            else if ((op.code == OPC_U4 && fm.u4) || (op.code == OPC_U2 && fm.u2)) {
                 // 3M constants of U = A + iB: A, -(A+B), B-A (row-major entries)
                 const int dim = op.code == OPC_U4 ? 4 : 2;
                 double c[48];
@@ -935,6 +1011,10 @@ std::string jit_key(const Step &st)
         ((uint64_t)(st.pass.fresh != 0) << 48) |
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
+    {
+        const Forms fm = forms_of(st);
+        put((uint64_t)fm.u2 | ((uint64_t)fm.u4 << 1));
+    }
     // the generated source indexes the deduplicated out-of-tile predicates
     // (P.out[out_idx[o]], and n_out sizes the parameter struct): the dedup
     // pattern is part of the structure, not only whether an op has one

@@ -1073,6 +1073,21 @@ void launch_swap_blocks(double2 *A, double2 *B, int M, int K, const int *lpos, u
     k_swap_blocks<<<grid_for(n_other, 256), 256, 0, s>>>(A, B, n_other, K, L, offA, offB);
 }
 
+// out[j] = sum over ranks r (in rank order) of all[r * count + j]
+__global__ void k_sum_ranks(const double *__restrict__ all, double *__restrict__ out, uint64_t count, int S)
+{
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += (uint64_t)gridDim.x * blockDim.x) {
+        double a = all[j];
+        for (int r = 1; r < S; r++) a += all[(uint64_t)r * count + j];
+        out[j] = a;
+    }
+}
+
+void launch_sum_ranks(const double *all, double *out, uint64_t count, int S, cudaStream_t s)
+{
+    k_sum_ranks<<<grid_for(count, 256), 256, 0, s>>>(all, out, count, S);
+}
+
 void launch_pack(const double2 *shard, double2 *buf, int M, int K, const int *lpos, uint64_t c, uint64_t first,
                  uint64_t count, int unpack, cudaStream_t s)
 {

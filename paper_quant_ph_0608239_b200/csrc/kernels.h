@@ -53,6 +53,7 @@ void launch_pair_gate(double2 *A, double2 *B, int M, uint64_t mloc, uint64_t vlo
                       cudaStream_t s);
 void launch_pair_combine(double2 *own, const double2 *other, uint64_t off, uint64_t count, uint64_t mloc,
                          uint64_t vloc, const double *c0, const double *c1, int self_first, cudaStream_t s);
+void launch_sum_ranks(const double *all, double *out, uint64_t count, int S, cudaStream_t s);
 int pass_regs_per_thread();
 
 }  // namespace qsb

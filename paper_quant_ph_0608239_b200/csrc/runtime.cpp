@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/qsim.h"
+#include "comm.h"
 #include "jit.h"
 #include "kernels.h"
 #include "plan.h"
@@ -58,7 +59,11 @@ struct qsim_ctx_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int n_sm = 148;  // SMs of the current device (persistent pass grid)
-    ncclComm_t comm = nullptr;
+    Comm *comm = nullptr;  // SPMD transports (NCCL, loopback)
+    double comm_timeout_ms = 600e3;
+    // exchange pipeline: transfers run on xstream, pack/unpack on stream
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t x_ready[2] = {nullptr, nullptr}, x_done[2] = {nullptr, nullptr}, x_used[2] = {nullptr, nullptr};
     Planner *planner = nullptr;
     bool initialized = false, init_pending = false;
     uint64_t init_index = 0;
@@ -114,14 +119,34 @@ struct qsim_ctx_s {
         }                                                                                           \
     } while (0)
 
-#define CKN(ctx, call)                                                                            \
+// a Comm call (comm.h): nonzero = transport error, message in _err
+#define CKC(ctx, call)                                                                            \
     do {                                                                                          \
-        ncclResult_t _r = (call);                                                                 \
-        if (_r != ncclSuccess) {                                                                  \
+        std::string _err;                                                                         \
+        if ((ctx)->comm->call) {                                                                  \
             (ctx)->poisoned = true;                                                               \
-            FAIL(ctx, QSIM_ERR_COMM, "%s: %s", #call, ncclGetErrorString(_r));                    \
+            FAIL(ctx, QSIM_ERR_COMM, "%s", _err.c_str());                                         \
         }                                                                                         \
     } while (0)
+
+static bool spmd(const qsim_ctx_s *c) { return c->comm != nullptr && c->P > 1; }
+
+// Wait for the context's stream.  SPMD: poll the transport's asynchronous
+// error state meanwhile and give up after comm_timeout_ms (an SPMD call
+// mismatch or a dead peer then returns QSIM_ERR_COMM instead of hanging).
+static qsim_status sync_stream(qsim_ctx c)
+{
+    if (c->comm) {
+        std::string err;
+        if (c->comm->wait(c->stream, c->comm_timeout_ms, err)) {
+            c->poisoned = true;
+            FAIL(c, QSIM_ERR_COMM, "%s", err.c_str());
+        }
+        return QSIM_OK;
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    return QSIM_OK;
+}
 
 #define LAUNCHED(ctx)                                                                         \
     do {                                                                                      \
@@ -289,7 +314,7 @@ struct RangeGuard {
 static qsim_status collect_timing(qsim_ctx c)
 {
     if (c->ranges.empty()) return QSIM_OK;
-    CK(c, cudaStreamSynchronize(c->stream));
+    { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     for (auto &r : c->ranges) {
         float ms = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
@@ -313,7 +338,7 @@ static qsim_status ensure_dev(qsim_ctx c, T *&p, size_t &cap, size_t need)
     if (need <= cap) return QSIM_OK;
     size_t nc = std::max(need, cap * 2);
     if (p) {
-        CK(c, cudaStreamSynchronize(c->stream));
+        { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
         CK(c, cudaFree(p));
         p = nullptr;
     }
@@ -352,6 +377,44 @@ static inline uint64_t with_sub(uint64_t r, const std::vector<int> &gpos, int M,
 }
 
 // ------------------------------------------------------------ exchange
+// Piece pipeline of the SPMD exchanges (P:759-779 split each send into
+// buffers; here the buffers are also pipelined).  Piece k is staged on the
+// engine stream (pack into slot k&1), transferred on xstream (one grouped
+// send/recv), and finished on the engine stream (unpack / combine).  With two
+// slots the transfer of piece k overlaps the finish of piece k-1 and the
+// stage of piece k+1; a slot is re-used only after its previous finish.
+template <class Stage, class Xfer, class Finish>
+static qsim_status pipeline(qsim_ctx c, uint64_t nb, Stage stage, Xfer xfer, Finish finish)
+{
+    if (!c->xstream) {
+        CK(c, cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CK(c, cudaEventCreateWithFlags(&c->x_ready[i], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->x_done[i], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->x_used[i], cudaEventDisableTiming));
+        }
+    }
+    qsim_status st;
+    auto finish_one = [&](uint64_t j) -> qsim_status {
+        const int sl = (int)(j & 1);
+        CK(c, cudaStreamWaitEvent(c->stream, c->x_done[sl], 0));
+        if ((st = finish(j, sl)) != QSIM_OK) return st;
+        CK(c, cudaEventRecord(c->x_used[sl], c->stream));
+        return QSIM_OK;
+    };
+    for (uint64_t k = 0; k < nb; k++) {
+        const int sl = (int)(k & 1);
+        if ((st = stage(k, sl)) != QSIM_OK) return st;
+        CK(c, cudaEventRecord(c->x_ready[sl], c->stream));
+        CK(c, cudaStreamWaitEvent(c->xstream, c->x_ready[sl], 0));
+        if (k >= 2) CK(c, cudaStreamWaitEvent(c->xstream, c->x_used[sl], 0));
+        if ((st = xfer(k, sl)) != QSIM_OK) return st;
+        CK(c, cudaEventRecord(c->x_done[sl], c->xstream));
+        if (k >= 1 && (st = finish_one(k - 1)) != QSIM_OK) return st;
+    }
+    return nb ? finish_one(nb - 1) : QSIM_OK;
+}
+
 static qsim_status exec_exchange(qsim_ctx c, const Step &s)
 {
     const int K = (int)s.lpos.size(), M = c->M;
@@ -374,8 +437,9 @@ static qsim_status exec_exchange(qsim_ctx c, const Step &s)
         c->stats.exchange_bytes += (nval - 1) * chunk * 16;
         return QSIM_OK;
     }
-    if (c->transport != QSIM_TRANSPORT_NCCL) FAIL(c, QSIM_ERR_STATE, "exchange without a multi-shard transport");
-    // NCCL: every rank trades chunk v with the peer whose global sub-bits are v
+    if (!spmd(c)) FAIL(c, QSIM_ERR_STATE, "exchange without a multi-shard transport");
+    // SPMD (NCCL / loopback): every rank trades chunk v with the peer whose
+    // global sub-bits are v, in pieces through the pipeline
     const uint64_t my = rank_sub((uint64_t)c->rank, s.gpos, M);
     bool contiguous = true;
     {
@@ -386,49 +450,56 @@ static qsim_status exec_exchange(qsim_ctx c, const Step &s)
     }
     const uint64_t npeer = nval - 1;
     const uint64_t scratch_amps = c->scratch_bytes / sizeof(double2);
+    const uint64_t per_piece = 2 * npeer * (contiguous ? 1 : 2);  // two slots of recv (+ send) buffers
     uint64_t piece = chunk;
     const uint64_t limit_amps = (uint64_t)c->chunk_mb * (1ULL << 20) / sizeof(double2);
-    while (piece > 1 && (piece * npeer * (contiguous ? 1 : 2) > scratch_amps || piece > limit_amps)) piece >>= 1;
-    if (piece * npeer * (contiguous ? 1 : 2) > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for exchange");
-    double2 *recvb = c->scratch;
-    double2 *sendb = c->scratch + piece * npeer;
-    for (uint64_t off = 0; off < chunk; off += piece) {
-        if (!contiguous) {
-            uint64_t idx = 0;
-            for (uint64_t v = 0; v < nval; v++) {
-                if (v == my) continue;
-                launch_pack(c->shards[0], sendb + idx * piece, M, K, s.lpos.data(), v, off, piece, 0, c->stream);
+    while (piece > 1 && (piece * per_piece > scratch_amps || piece > limit_amps)) piece >>= 1;
+    if (piece * per_piece > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for exchange");
+    const uint64_t slot_amps = piece * npeer * (contiguous ? 1 : 2);
+    auto recvb = [&](int slot) { return c->scratch + slot * slot_amps; };
+    auto sendb = [&](int slot) { return c->scratch + slot * slot_amps + piece * npeer; };
+    std::vector<uint64_t> vals;
+    for (uint64_t v = 0; v < nval; v++)
+        if (v != my) vals.push_back(v);
+    qsim_status st = pipeline(
+        c, chunk / piece,
+        [&](uint64_t k, int slot) -> qsim_status {  // stage: pack the outgoing blocks
+            if (contiguous) return QSIM_OK;
+            for (size_t i = 0; i < vals.size(); i++) {
+                launch_pack(c->shards[0], sendb(slot) + i * piece, M, K, s.lpos.data(), vals[i], k * piece, piece, 0,
+                            c->stream);
                 LAUNCHED(c);
-                idx++;
             }
-        }
-        CKN(c, ncclGroupStart());
-        uint64_t idx = 0;
-        for (uint64_t v = 0; v < nval; v++) {
-            if (v == my) continue;
-            const int peer = (int)with_sub((uint64_t)c->rank, s.gpos, M, v);
-            const double2 *src;
-            if (contiguous) {
-                uint64_t base = 0;
-                for (int i = 0; i < K; i++)
-                    if ((v >> i) & 1) base |= 1ULL << s.lpos[i];
-                src = c->shards[0] + base + off;
-            } else {
-                src = sendb + idx * piece;
+            return QSIM_OK;
+        },
+        [&](uint64_t k, int slot) -> qsim_status {  // transfer (xstream)
+            CKC(c, group_start(_err));
+            for (size_t i = 0; i < vals.size(); i++) {
+                const int peer = (int)with_sub((uint64_t)c->rank, s.gpos, M, vals[i]);
+                const double2 *src;
+                if (contiguous) {
+                    uint64_t base = 0;
+                    for (int b = 0; b < K; b++)
+                        if ((vals[i] >> b) & 1) base |= 1ULL << s.lpos[b];
+                    src = c->shards[0] + base + k * piece;
+                } else {
+                    src = sendb(slot) + i * piece;
+                }
+                CKC(c, send(src, piece * sizeof(double2), peer, c->xstream, _err));
+                CKC(c, recv(recvb(slot) + i * piece, piece * sizeof(double2), peer, c->xstream, _err));
             }
-            CKN(c, ncclSend(src, piece * 2, ncclDouble, peer, c->comm, c->stream));
-            CKN(c, ncclRecv(recvb + idx * piece, piece * 2, ncclDouble, peer, c->comm, c->stream));
-            idx++;
-        }
-        CKN(c, ncclGroupEnd());
-        idx = 0;
-        for (uint64_t v = 0; v < nval; v++) {
-            if (v == my) continue;
-            launch_pack(c->shards[0], recvb + idx * piece, M, K, s.lpos.data(), v, off, piece, 1, c->stream);
-            LAUNCHED(c);
-            idx++;
-        }
-    }
+            CKC(c, group_end(_err));
+            return QSIM_OK;
+        },
+        [&](uint64_t k, int slot) -> qsim_status {  // finish: unpack the incoming blocks in place
+            for (size_t i = 0; i < vals.size(); i++) {
+                launch_pack(c->shards[0], recvb(slot) + i * piece, M, K, s.lpos.data(), vals[i], k * piece, piece, 1,
+                            c->stream);
+                LAUNCHED(c);
+            }
+            return QSIM_OK;
+        });
+    if (st != QSIM_OK) return st;
     c->stats.exchange_bytes += npeer * chunk * 16;
     return QSIM_OK;
 }
@@ -453,7 +524,7 @@ static qsim_status exec_pairwise(qsim_ctx c, const Step &s)
         c->stats.exchange_bytes += (uint64_t)c->P * (16ULL << M);
         return QSIM_OK;
     }
-    if (c->transport != QSIM_TRANSPORT_NCCL) FAIL(c, QSIM_ERR_STATE, "pairwise step without a multi-shard transport");
+    if (!spmd(c)) FAIL(c, QSIM_ERR_STATE, "pairwise step without a multi-shard transport");
     const uint64_t r = (uint64_t)c->rank;
     if (((r << M) & mhi) != vhi) return QSIM_OK;  // the partner skips too (same control bits)
     const int peer = (int)(r ^ gbit);
@@ -465,16 +536,24 @@ static qsim_status exec_pairwise(qsim_ctx c, const Step &s)
     const uint64_t shard = 1ULL << M, scratch_amps = c->scratch_bytes / sizeof(double2);
     uint64_t piece = shard;
     const uint64_t limit_amps = (uint64_t)c->chunk_mb * (1ULL << 20) / sizeof(double2);
-    while (piece > 1 && (piece > scratch_amps || piece > limit_amps)) piece >>= 1;
-    if (piece > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for a pairwise exchange");
-    for (uint64_t off = 0; off < shard; off += piece) {
-        CKN(c, ncclGroupStart());
-        CKN(c, ncclSend(c->shards[0] + off, piece * 2, ncclDouble, peer, c->comm, c->stream));
-        CKN(c, ncclRecv(c->scratch, piece * 2, ncclDouble, peer, c->comm, c->stream));
-        CKN(c, ncclGroupEnd());
-        launch_pair_combine(c->shards[0] + off, c->scratch, off, piece, mloc, vloc, c0, c1, !hi, c->stream);
-        LAUNCHED(c);
-    }
+    while (piece > 1 && (2 * piece > scratch_amps || piece > limit_amps)) piece >>= 1;
+    if (2 * piece > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for a pairwise exchange");
+    qsim_status st = pipeline(
+        c, shard / piece, [&](uint64_t, int) -> qsim_status { return QSIM_OK; },
+        [&](uint64_t k, int slot) -> qsim_status {
+            CKC(c, group_start(_err));
+            CKC(c, send(c->shards[0] + k * piece, piece * sizeof(double2), peer, c->xstream, _err));
+            CKC(c, recv(c->scratch + slot * piece, piece * sizeof(double2), peer, c->xstream, _err));
+            CKC(c, group_end(_err));
+            return QSIM_OK;
+        },
+        [&](uint64_t k, int slot) -> qsim_status {
+            launch_pair_combine(c->shards[0] + k * piece, c->scratch + slot * piece, k * piece, piece, mloc, vloc, c0,
+                                c1, !hi, c->stream);
+            LAUNCHED(c);
+            return QSIM_OK;
+        });
+    if (st != QSIM_OK) return st;
     c->stats.exchange_bytes += 16ULL << M;
     return QSIM_OK;
 }
@@ -890,6 +969,13 @@ size_t qsim_scratch_bytes(int n_qubits, int n_ranks)
     return std::min<size_t>(shard, (size_t)4 << 30);
 }
 
+qsim_status qsim_get_loopback_id(void *out128)
+{
+    if (!out128) return QSIM_ERR_ARG;
+    new_loopback_id(out128);
+    return QSIM_OK;
+}
+
 qsim_status qsim_get_unique_id(void *out128)
 {
     if (!out128) return QSIM_ERR_ARG;
@@ -932,15 +1018,16 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
     const int G = ilog2(P);
     if (n - G < 1) return QSIM_ERR_ARG;
     if (cfg->transport == QSIM_TRANSPORT_LOCAL && P != 1) return QSIM_ERR_ARG;
-    if (cfg->transport < 0 || cfg->transport > 2) return QSIM_ERR_ARG;
-    if (cfg->transport == QSIM_TRANSPORT_NCCL && (cfg->rank < 0 || cfg->rank >= P)) return QSIM_ERR_ARG;
+    if (cfg->transport < 0 || cfg->transport > 3) return QSIM_ERR_ARG;
+    const bool spmd_tp = cfg->transport == QSIM_TRANSPORT_NCCL || cfg->transport == QSIM_TRANSPORT_LOOPBACK;
+    if (spmd_tp && (cfg->rank < 0 || cfg->rank >= P)) return QSIM_ERR_ARG;
     cudaGetLastError();  // do not inherit a stale error of another context
     qsim_ctx c = new qsim_ctx_s();
     c->n = n;
     c->P = P;
     c->G = G;
     c->M = n - G;
-    c->rank = cfg->transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
+    c->rank = spmd_tp ? cfg->rank : 0;
     c->transport = cfg->transport;
     c->planner = new Planner(n, G);
     auto bail = [&](qsim_status s) {
@@ -971,7 +1058,7 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(QSIM_ERR_CUDA);
         c->own_stream = true;
     }
-    if (cfg->transport == QSIM_TRANSPORT_NCCL) {
+    if (spmd_tp) {
         c->scratch = (double2 *)cfg->scratch;
         c->scratch_bytes = cfg->scratch_bytes;
         if (!c->scratch) {
@@ -982,9 +1069,14 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
             }
             c->own_scratch = true;
         }
-        ncclUniqueId id;
-        std::memcpy(&id, cfg->nccl_id, sizeof(id));
-        if (ncclCommInitRank(&c->comm, P, id, cfg->rank) != ncclSuccess) return bail(QSIM_ERR_COMM);
+        if (const char *e = getenv("QSIM_COMM_TIMEOUT_S")) c->comm_timeout_ms = 1e3 * atof(e);
+        std::string err;
+        c->comm = cfg->transport == QSIM_TRANSPORT_NCCL ? make_nccl_comm(cfg->nccl_id, P, cfg->rank, c->comm_timeout_ms, err)
+                                                        : make_loopback_comm(cfg->nccl_id, P, cfg->rank, c->comm_timeout_ms, err);
+        if (!c->comm) {
+            fprintf(stderr, "qsim_create_ext: %s\n", err.c_str());
+            return bail(QSIM_ERR_COMM);
+        }
     }
     {
         int dev = 0;
@@ -1013,8 +1105,13 @@ qsim_status qsim_create(int n_qubits, int n_gpus, qsim_ctx *out)
 qsim_status qsim_destroy(qsim_ctx c)
 {
     if (!c) return QSIM_OK;
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->stream && !c->poisoned) cudaStreamSynchronize(c->stream);
+    if (c->xstream && !c->poisoned) cudaStreamSynchronize(c->xstream);
+    delete c->comm;
+    for (int i = 0; i < 2; i++)
+        for (cudaEvent_t e : {c->x_ready[i], c->x_done[i], c->x_used[i]})
+            if (e) cudaEventDestroy(e);
+    if (c->xstream) cudaStreamDestroy(c->xstream);
     if (c->own_shards)
         for (double2 *p : c->shards) cudaFree(p);
     if (c->own_scratch) cudaFree(c->scratch);
@@ -1170,7 +1267,7 @@ qsim_status qsim_sync(qsim_ctx c)
     GUARD(c);
     qsim_status s = flush(c);
     if (s != QSIM_OK) return s;
-    CK(c, cudaStreamSynchronize(c->stream));
+    { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     return collect_timing(c);
 }
 
@@ -1187,14 +1284,14 @@ qsim_status qsim_get_layout(qsim_ctx c, int *out)
 // cross-shard sum of per-shard host vectors in fixed rank order
 static qsim_status sum_over_ranks(qsim_ctx c, std::vector<std::vector<double>> &per, double *out, size_t len)
 {
-    if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1) {
+    if (spmd(c)) {
         qsim_status s;
         if ((s = ensure_dev(c, c->d_red, c->d_red_cap, len * (c->P + 1))) != QSIM_OK) return s;
         CK(c, cudaMemcpyAsync(c->d_red, per[0].data(), len * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CKN(c, ncclAllGather(c->d_red, c->d_red + len, len, ncclDouble, c->comm, c->stream));
+        CKC(c, all_gather(c->d_red, c->d_red + len, len, c->stream, _err));
         std::vector<double> all(len * c->P);
         CK(c, cudaMemcpyAsync(all.data(), c->d_red + len, len * c->P * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
+        { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
         for (size_t j = 0; j < len; j++) {
             double a = 0.0;
             for (int r = 0; r < c->P; r++) a += all[r * len + j];
@@ -1250,7 +1347,7 @@ static qsim_status probabilities_impl(qsim_ctx c, const int *qubits, int k, doub
         LAUNCHED(c);
         CK(c, cudaMemcpyAsync(per[i].data(), c->d_red + partial_len, B * sizeof(double), cudaMemcpyDeviceToHost,
                               c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
+        { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     }
     return sum_over_ranks(c, per, out, B);
 }
@@ -1270,7 +1367,7 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
     if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
     qsim_status s = flush(c);
     if (s != QSIM_OK) return s;
-    const int M = c->M, cb = std::min(12, M), n = c->n, S = c->transport == QSIM_TRANSPORT_NCCL ? c->P : n_local(c);
+    const int M = c->M, cb = std::min(12, M), n = c->n, S = spmd(c) ? c->P : n_local(c);
     const uint64_t nch = 1ULL << (M - cb);
     const size_t plen = nch * (cb + 1), vlen = (size_t)M + 1;
     // partial sums | this process's shard vectors | all ranks' vectors (NCCL) | logical result
@@ -1283,8 +1380,8 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
         LAUNCHED(c);
     }
     const double *phys = own;
-    if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1) {
-        CKN(c, ncclAllGather(own, all, vlen, ncclDouble, c->comm, c->stream));
+    if (spmd(c)) {
+        CKC(c, all_gather(own, all, vlen, c->stream, _err));
         phys = all;
     }
     ExpectMap m{};
@@ -1295,7 +1392,7 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
     launch_expect_logical(phys, m, res, c->stream);
     LAUNCHED(c);
     CK(c, cudaMemcpyAsync(out, res, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (sync) CK(c, cudaStreamSynchronize(c->stream));
+    if (sync) { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     return QSIM_OK;
 }
 
@@ -1327,7 +1424,7 @@ qsim_status qsim_measure(qsim_ctx c, const int *qubits, int k, uint64_t seed, ui
     launch_sample(dp, k, seed, n_shots, dc, dout, c->stream);
     LAUNCHED(c);
     if (n_shots) CK(c, cudaMemcpyAsync(out, dout, n_shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
+    { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     return QSIM_OK;
 }
 
@@ -1339,8 +1436,12 @@ qsim_status qsim_get_amplitudes(qsim_ctx c, uint64_t first, uint64_t count, qsim
     if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
     qsim_status s = flush(c);
     if (s != QSIM_OK) return s;
-    const uint64_t piece = 1ULL << 22;
-    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, 2 * piece)) != QSIM_OK) return s;
+    // SPMD: every rank gathers the amplitudes it owns (zeros elsewhere), the
+    // pieces are all-gathered and summed in rank order (exactly one rank holds
+    // each index, so the sum is a selection)
+    const int S = spmd(c) ? c->P : 1;
+    const uint64_t piece = std::max<uint64_t>(1, (1ULL << 22) / S);
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, 2 * piece * (S > 1 ? S + 1 : 1))) != QSIM_OK) return s;
     const int virt = c->transport == QSIM_TRANSPORT_VIRTUAL;
     for (uint64_t off = 0; off < count; off += piece) {
         const uint64_t cnt = std::min(piece, count - off);
@@ -1348,10 +1449,14 @@ qsim_status qsim_get_amplitudes(qsim_ctx c, uint64_t first, uint64_t count, qsim
         launch_gather(dout, first + off, cnt, c->d_shard_ptrs, virt, c->rank, c->M, c->n, c->planner->phys_of.data(),
                       c->stream);
         LAUNCHED(c);
-        if (c->transport == QSIM_TRANSPORT_NCCL && c->P > 1)
-            CKN(c, ncclAllReduce(dout, dout, cnt * 2, ncclDouble, ncclSum, c->comm, c->stream));
+        if (S > 1) {
+            double *all = c->d_red + 2 * piece;
+            CKC(c, all_gather((const double *)dout, all, 2 * cnt, c->stream, _err));
+            launch_sum_ranks(all, (double *)dout, 2 * cnt, S, c->stream);
+            LAUNCHED(c);
+        }
         CK(c, cudaMemcpyAsync(host_out + off, dout, cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
+        { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
     }
     return QSIM_OK;
 }
@@ -1368,6 +1473,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else if (k == "comm_timeout_ms") c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
     else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
     else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }

@@ -78,6 +78,46 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
+def get_loopback_id() -> bytes:
+    """Id of a new loopback group (QSim(..., transport="loopback", nccl_id=id))."""
+    buf = (ctypes.c_uint8 * 128)()
+    s = N.lib().qsim_get_loopback_id(buf)
+    if s != 0:
+        raise QsimError(s, "qsim_get_loopback_id")
+    return bytes(buf)
+
+
+def run_loopback(n: int, n_ranks: int, body, **kw) -> list:
+    """Run the SPMD program body(sim, rank) -> result on n_ranks loopback
+    ranks: one QSim per rank, each driven by its own host thread (the ctypes
+    calls release the GIL), all on the current device.  Returns the results
+    in rank order; re-raises the first exception."""
+    import threading
+    cid = get_loopback_id()
+    out, errs = [None] * n_ranks, [None] * n_ranks
+
+    def worker(r):
+        sim = None
+        try:
+            sim = QSim(n, n_ranks=n_ranks, transport="loopback", rank=r, nccl_id=cid, **kw)
+            out[r] = body(sim, r)
+        except BaseException as e:  # noqa: BLE001 (reported below)
+            errs[r] = e
+        finally:
+            if sim is not None:
+                sim.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(n_ranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
 GLOBAL_POLICY = {"remap": 0, "pairwise": 1, "auto": 2}
 
 
@@ -122,7 +162,9 @@ class QSim:
     """One context of the engine.
 
     transport: "local" (1 shard on this GPU), "virtual" (n_ranks shards on
-    this GPU, exchanged by device copies), "nccl" (one process per GPU).
+    this GPU, exchanged by device copies), "nccl" (one process per GPU),
+    "loopback" (one rank of an SPMD group whose ranks are threads of this
+    process on this GPU: the NCCL transport's code path, see run_loopback).
     """
 
     def __init__(self, n: int, n_ranks: int = 1, transport: str = "local", rank: int = 0,
@@ -133,7 +175,8 @@ class QSim:
             raise RuntimeError("QSim needs a CUDA device (no CPU fallback)")
         self.lib = N.lib()
         self.n, self.n_ranks = n, n_ranks
-        tp = {"local": N.TRANSPORT_LOCAL, "virtual": N.TRANSPORT_VIRTUAL, "nccl": N.TRANSPORT_NCCL}[transport]
+        tp = {"local": N.TRANSPORT_LOCAL, "virtual": N.TRANSPORT_VIRTUAL, "nccl": N.TRANSPORT_NCCL,
+              "loopback": N.TRANSPORT_LOOPBACK}[transport]
         G = (n_ranks - 1).bit_length()
         self.M = n - G
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -145,12 +188,12 @@ class QSim:
         self._shards = [torch.empty(2 << self.M, dtype=torch.float64, device=dev) for _ in range(nsh)]
         for i, t in enumerate(self._shards):
             cfg.shards[i] = t.data_ptr()
-        if tp == N.TRANSPORT_NCCL:
+        if tp in (N.TRANSPORT_NCCL, N.TRANSPORT_LOOPBACK):
             sb = self.lib.qsim_scratch_bytes(n, n_ranks) if scratch_bytes is None else scratch_bytes
             self._scratch = torch.empty(max(16, sb), dtype=torch.uint8, device=dev)
             cfg.scratch, cfg.scratch_bytes = self._scratch.data_ptr(), sb
             if nccl_id is None:
-                raise ValueError("nccl transport needs nccl_id (see QSim.distributed)")
+                raise ValueError("nccl/loopback transport needs nccl_id (QSim.distributed, get_loopback_id)")
             for j in range(128):
                 cfg.nccl_id[j] = nccl_id[j]
         self._stream = torch.cuda.Stream(device=dev)
