@@ -8,8 +8,15 @@ gates) + qsim_expectations (<Q_i> of every qubit, read back to
 the host): every hot-path row of SURVEY.md §8(a) that this circuit uses.
 metric = N_O * 2^n / t  (N_O = user gates per step).
 
-N > 1 (torchrun, one rank per GPU, NCCL): weak scaling, n = 24 + log2(N)
-qubits of the same circuit family sharded over the N GPUs.
+Default --steps 200 (a ~1 s timed region).  At N = 1 the line also carries
+detail.per_config: BASELINE configs 3 (Shor 28 q) and 4 (QFT 32 q, 64 GiB)
+and the config-5 family at 33 q (128 GiB), each device-timed with its own
+kernel rooflines and clock record.
+
+N > 1 (one rank per GPU, NCCL; `--gpus N` alone spawns the ranks with
+torch.distributed.run on 127.0.0.1): weak scaling of the config-5 family,
+n = 33 + log2(N) qubits (128 GiB per GPU; N = 8 is config 5 at 36 q), or
+`--workload config2` for the config-2 family at 24 + log2(N).
 
 --impl reference runs the CPU oracle (oracle/) on a bounded sample of the
 same workload on the host cores (there is no reference implementation).
@@ -35,7 +42,6 @@ sys.path.insert(0, ROOT)
 METRIC = "amplitude-gate updates/s"
 UNIT = "AGU/s"
 DEPTH = 40
-TIMING_EVERY = 4  # roofline events on every 4th step of the timed region
 CPU_LAYERS, CPU_REPS = DEPTH, 2  # cpu_baseline sample: two whole steps of the workload (~12 s on 16 cores)
 BASE_QUBITS = 24
 
@@ -176,7 +182,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    layers = 10  # a quarter of the circuit per step (~1.3 s on 16 cores): the run stays within minutes
+    # a bounded sample of the workload per step: the first `layers` of the 40
+    # layers (~0.13 s per layer on 16 host cores), sized so that the whole
+    # warmup + steps run stays within ~2 minutes
+    layers = max(1, min(10, int(100 / (0.13 * max(1, args.steps + args.warmup)))))
     for _ in range(args.warmup):
         cpu_sample(layers)
     vals, tot = [], 0.0
@@ -197,13 +206,121 @@ def run_reference(args):
     return 0
 
 
+def workload_for(world: int, name: str):
+    """(workload name, n, init, gates) of a bench run.  N = 1: config 2
+    (BASELINE.json configs[1], the metric's headline config).  N > 1: the
+    config-5 circuit family weak-scaled, n = 33 + log2 N (128 GiB per GPU;
+    N = 8 is config 5 itself at 36 q), unless --workload config2 is given
+    (the config-2 family at 24 + log2 N)."""
+    from workloads import circuits as C
+    G = (world - 1).bit_length()
+    if name == "auto":
+        name = "config2" if world == 1 else "config5"
+    if name == "config2":
+        n = BASE_QUBITS + G
+        return ("config2_random_brickwork" if world == 1 else "config2_family_weak"), n, 0, \
+            C.random_brickwork(n, DEPTH, seed=2)
+    if name == "config5":
+        n = 33 + G
+        return ("config5_family_weak" if n != 36 else "config5_random36"), n, 0, \
+            C.random_chain(n, 10, seed=5, sweep=True)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def measured_peaks():
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-measured
+    copy), FP64 from the library's DFMA probe on this GPU (qsim_probe_peaks)."""
+    from paper_quant_ph_0608239_b200 import probe_peaks
+    hbm, hbm_src, sm_max = peaks()
+    pk = probe_peaks(fp64=True, copy=False)
+    return {"hbm_gbs": hbm, "hbm_src": hbm_src, "sm_max": sm_max, "fp64_tflops": pk["fp64_tflops"],
+            "fp64_src": "measured: DFMA probe (qsim_probe_peaks: 8 independent FMA chains/thread, "
+                        "2 x 256-thread CTAs/SM), best of 5",
+            "fp64_derived": 2.0 * FP64_FMA_PER_CLK_PER_SM * N_SM * sm_max * 1e6 / 1e12}
+
+
+def kernel_roofline(st, pk, amps_per_launch_bytes):
+    """Achieved FP64 and HBM rates of the timed pass / permutation launches."""
+    out = {}
+    if st["pass_ms"] > 0:
+        f = 2.0 * st["pass_fp64_slots"] / (st["pass_ms"] / 1e3) / 1e12
+        b = st["pass_amp_bytes"] / (st["pass_ms"] / 1e3) / 1e9
+        out["pass"] = {"ms": st["pass_ms"], "launches": int(st["passes"]),
+                       "fp64_tflops": f, "fp64_frac": f / pk["fp64_tflops"],
+                       "hbm_gbs": b, "hbm_frac": b / pk["hbm_gbs"]}
+    if st["perm_ms"] > 0:
+        nb = st["perm_launches"] * amps_per_launch_bytes
+        out["perm"] = {"ms": st["perm_ms"], "launches": int(st["perm_launches"]),
+                       "hbm_gbs": nb / (st["perm_ms"] / 1e3) / 1e9,
+                       "hbm_frac": nb / (st["perm_ms"] / 1e3) / 1e9 / pk["hbm_gbs"]}
+    if st["exchange_ms"] > 0:
+        out["exchange"] = {"ms": st["exchange_ms"], "count": int(st["exchanges"]),
+                           "bytes_sent": int(st["exchange_bytes"]),
+                           "gbs_per_direction": st["exchange_bytes"] / (st["exchange_ms"] / 1e3) / 1e9,
+                           "nvlink_frac": st["exchange_bytes"] / (st["exchange_ms"] / 1e3) / 900e9}
+    return out
+
+
+def per_config(pk, local):
+    """Device-timed BASELINE configs 3 and 4 and the config-5 family at 33 q
+    (the N = 1 point of the weak-scaling workload) on this GPU: steps timed
+    with events and no per-kernel events, then one step with per-launch
+    events for the kernel breakdown."""
+    import torch
+
+    from paper_quant_ph_0608239_b200 import QSim, pack_gates
+    from workloads import circuits as C
+    w3, w4 = C.config3_shor(), C.config4_qft()
+    runs = [("config3_shor_N899", w3.n, w3.init, w3.gates, 10),
+            ("config4_qft32", 32, w4.init, w4.gates, 3),
+            ("config5_family_33q", 33, 0, C.random_chain(33, 10, seed=5, sweep=True), 2)]
+    out = []
+    for name, n, init, gates, steps in runs:
+        free, _ = torch.cuda.mem_get_info()
+        if free < (16 << n) + (4 << 30):
+            out.append({"workload": name, "skipped": "not enough free HBM"})
+            continue
+        sim = QSim(n)
+        packed = pack_gates(gates)
+
+        def step():
+            sim.init_basis(init)
+            sim.run_circuit(gates, packed=packed)
+
+        step()
+        sim.sync()
+        clocks = Clocks(local)
+        torch.cuda.synchronize()
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sim.stream)
+        for _ in range(steps):
+            step()
+        e1.record(sim.stream)
+        torch.cuda.synchronize()
+        ck = clocks.stop()
+        ms = e0.elapsed_time(e1) / steps
+        sim.set_option("timing", 1)
+        sim.reset_stats()
+        step()
+        sim.sync()
+        st = sim.stats()
+        sim.close()
+        del sim
+        torch.cuda.empty_cache()
+        out.append({"workload": name, "n_qubits": n, "gates_per_step": len(gates), "steps": steps,
+                    "ms_per_step": ms, "value": len(gates) * float(1 << n) / (ms / 1e3), "unit": UNIT,
+                    "passes_per_step": int(st["passes"]), "perm_launches_per_step": int(st["perm_launches"]),
+                    "kernels": kernel_roofline(st, pk, 32 << n), "clocks": ck})
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_quant_ph_0608239_b200 import QSim, pack_gates
     from paper_quant_ph_0608239_b200 import _native as N
-    from workloads import circuits as C
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -214,12 +331,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G = (world - 1).bit_length()
-    n = BASE_QUBITS + G
-    gates = C.random_brickwork(n, DEPTH, seed=2)
+    wname, n, init, gates = workload_for(world, args.workload)
     n_o = len(gates)
     packed = pack_gates(gates)
+    pk = measured_peaks()
     sim = QSim.distributed(n) if world > 1 else QSim(n)
-    sim.set_option("timing", 1)  # CUDA events around pass launches (roofline)
     stream = sim.stream
 
     # <Q_i> of every step goes to pinned host memory with an async copy, so the
@@ -228,12 +344,12 @@ def run_ours(args):
     ex_buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
 
     def step():
-        sim.init_basis(0)
+        sim.init_basis(init)
         sim.run_circuit(gates, packed=packed)
         sim.expectations_async(ex_buf)
 
     def step_sync():
-        sim.init_basis(0)
+        sim.init_basis(init)
         sim.run_circuit(gates, packed=packed)
         return sim.expectations()
 
@@ -242,7 +358,14 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         step()
     sim.sync()
     ex = ex_buf.numpy().copy()
@@ -250,38 +373,42 @@ def run_ours(args):
     assert np.array_equal(ex, step_sync())
     assert abs(sim.norm() - 1) < 1e-10 and all(0 <= x <= 1 for x in ex)
 
-    # ---- device-timed region (events on the engine's stream)
+    # ---- device-timed region: K steps, events on the engine's stream, no
+    # per-kernel events (the library default)
+    sim.set_option("timing", 0)
     clocks = Clocks(local)
     barrier()
     sim.reset_stats()
     clocks.start()
-    # per-kernel events (roofline) on every TIMING_EVERY-th step of the region:
-    # an event pair around each pass costs ~1.6% of a step when on every step
-    n_timed = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for k in range(args.steps):
-        on = k % TIMING_EVERY == 0
-        n_timed += on
-        sim.set_option("timing", int(on))
+    for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     ck = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    st = sim.stats()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    st_value = sim.stats()
     value = args.steps * n_o * float(1 << n) / (ms / 1e3)
+
+    # ---- kernel roofline: the same steps again with CUDA events around every
+    # launch (on the engine's stream, where the kernels run), after the value
+    # region so the events cannot perturb `value`
+    rf_steps = max(1, min(args.steps, 50 if n <= 26 else 2))
+    sim.set_option("timing", 1)
+    barrier()
+    sim.reset_stats()
+    for _ in range(rf_steps):
+        step()
+    sim.sync()
+    st = sim.stats()
+    sim.set_option("timing", 0)
 
     # ---- end-to-end through the public C-ABI with host buffers: the host
     # gate array (qsim_gate[]) is validated, planned (plan cache off) and
     # uploaded every step and <Q_i> comes back to host memory; wall clock,
     # max over ranks.
-    sim.set_option("timing", 0)  # the library default: no per-kernel events
     sim.set_option("plan_cache", 0)
     step()
     barrier()
@@ -289,40 +416,32 @@ def run_ours(args):
     for _ in range(args.steps):
         step()
     barrier()
-    wall = time.perf_counter() - t0
+    e2e = args.steps * n_o * float(1 << n) / max_over_ranks(time.perf_counter() - t0)
     # the same with a synchronous readout every step (host and device alternate)
+    e2e_steps = max(1, min(args.steps, 20))
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         step_sync()
     barrier()
-    tw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-    e2e_sync = args.steps * n_o * float(1 << n) / float(tw.item())
+    e2e_sync = e2e_steps * n_o * float(1 << n) / max_over_ranks(time.perf_counter() - t0)
     sim.set_option("plan_cache", 1)
-    tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-    wall = float(tw.item())
-    e2e = args.steps * n_o * float(1 << n) / wall
     # the same with the library's default plan cache (a repeated circuit is
     # validated and uploaded every step but planned once)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         step()
     barrier()
-    tw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-    e2e_cached = args.steps * n_o * float(1 << n) / float(tw.item())
+    e2e_cached = e2e_steps * n_o * float(1 << n) / max_over_ranks(time.perf_counter() - t0)
     import ctypes
     h2d = n_o * ctypes.sizeof(N.qsim_gate)
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
 
-    hbm_peak, peak_src, sm_max = peaks()
+    hbm_peak, fp64_peak = pk["hbm_gbs"], pk["fp64_tflops"]
     pass_ms = st["pass_ms"]
-    fp64_peak = 2.0 * FP64_FMA_PER_CLK_PER_SM * N_SM * sm_max * 1e6 / 1e12  # TFLOP/s
     fp64_ach = (2.0 * st["pass_fp64_slots"] / (pass_ms / 1e3) / 1e12) if pass_ms > 0 else None
     hbm_ach = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
     t_min_ms, _ = pass_roofline(n, world, gates, fp64_peak, hbm_peak)
@@ -330,61 +449,83 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    step_ms = ms / args.steps
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": warm, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2_random_brickwork" if world == 1 else "config2_family_weak",
-                       "n_qubits": n, "depth": DEPTH, "gates_per_step": n_o, "shard_qubits": n - G,
+            "config": {"workload": wname, "n_qubits": n, "gates_per_step": n_o, "shard_qubits": n - G,
                        "parallelism": f"sharded{world}" if world > 1 else "single",
                        "l2": "state %d MiB per GPU > 126 MB L2 (no flush needed)" % ((16 << (n - G)) >> 20)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n,
                     "plan_cache": "off: every step validates, plans and uploads the gate list",
                     "readout": "<Q_i> copied to pinned host memory every step (async); host syncs at the end",
-                    "value_sync_readout": e2e_sync,
-                    "value_plan_cached": e2e_cached},
-            "gpu_launches": int(st["kernel_launches"]),
+                    "value_sync_readout": e2e_sync, "value_plan_cached": e2e_cached,
+                    "sync_and_cached_steps": e2e_steps},
+            "gpu_launches": int(st_value["kernel_launches"]),
             "roofline": {"bound": "alu", "achieved": fp64_ach, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (fp64_ach / fp64_peak) if fp64_ach else None, "traffic": traffic,
-                         "kernel": "qsim_pass (NVRTC pass-specialised k_pass)",
-                         "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x %.0f MHz" % sm_max,
-                         "launches": int(st["passes"] * n_timed / args.steps), "kernel_ms": pass_ms,
-                         "timed_steps": f"{n_timed} of {args.steps} (every {TIMING_EVERY}th)",
-                         "kernel_share_of_step": pass_ms / (ms * n_timed / args.steps) if ms > 0 else None,
+                         "traffic_source": "static: ncu --set full capture of a config-2 pass, profiles/pass_traffic.json",
+                         "kernel": "qsim_pass (NVRTC pass-specialised tile pass)",
+                         "peak_source": pk["fp64_src"], "peak_derived": pk["fp64_derived"],
+                         "frac_of_derived": (fp64_ach / pk["fp64_derived"]) if fp64_ach else None,
+                         "achieved_from": "executed FP64-pipe instructions of the generated code (per launch) "
+                                          "x 2 / per-launch CUDA-event time",
+                         "launches": int(st["passes"]), "kernel_ms": pass_ms, "timed_steps": rf_steps,
+                         "kernel_share_of_step": pass_ms / (step_ms * rf_steps) if step_ms > 0 else None,
                          # per-launch bound max(FP64, HBM) summed over the passes of a step
                          "per_pass_bound": {"t_min_ms_per_step": t_min_ms,
-                                            "frac": (t_min_ms * n_timed / pass_ms) if pass_ms > 0 else None},
+                                            "frac": (t_min_ms * rf_steps / pass_ms) if pass_ms > 0 else None},
                          "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
-                                 "frac": (hbm_ach / hbm_peak) if hbm_ach else None, "peak_source": peak_src,
+                                 "frac": (hbm_ach / hbm_peak) if hbm_ach else None, "peak_source": pk["hbm_src"],
                                  "bytes_per_launch": 32 << (n - G)}},
             "clocks": ck,
-            "detail": {"passes_per_step": st["passes"] / args.steps, "plan_ms_per_step": st["plan_ms"] / args.steps,
-                       "jit_passes_per_step": st["jit_launches"] / args.steps,
-                       "plan_cache_hits": int(st["plan_cache_hits"]),
-                       "exchanges_per_step": st["exchanges"] / args.steps,
-                       "reduce_ms_per_step": st["reduce_ms"] / args.steps},
+            "detail": {"passes_per_step": st_value["passes"] / args.steps,
+                       "plan_ms_per_step": st_value["plan_ms"] / args.steps,
+                       "jit_passes_per_step": st_value["jit_launches"] / args.steps,
+                       "plan_cache_hits": int(st_value["plan_cache_hits"]),
+                       "exchanges_per_step": st_value["exchanges"] / args.steps,
+                       "kernels": kernel_roofline(st, pk, 32 << (n - G))},
         }
+        if world == 1 and not args.no_per_config:
+            line["detail"]["per_config"] = per_config(pk, local)
         if world == 1 and not args.no_cpu_baseline:
             v, tcpu, ng, cores = cpu_sample(CPU_LAYERS, CPU_REPS)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": f"{CPU_REPS} steps of the first {CPU_LAYERS} of {DEPTH} layers ({ng} gates) of the same circuit, "
                                               f"{tcpu:.1f} s"}
         print(json.dumps(line), flush=True)
-    sim.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def spawn(args):
+    """--gpus N > 1 without torchrun: launch N ranks of this script with
+    torch.distributed.run on 127.0.0.1 (one process per GPU)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true", help="skip detail.per_config (configs 3, 4, 5-family)")
+    ap.add_argument("--workload", default="auto", choices=["auto", "config2", "config5"])
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

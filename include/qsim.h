@@ -199,7 +199,17 @@ qsim_status qsim_expectations_async(qsim_ctx ctx, double *out);
 
 /* n_shots basis states of the listed qubits drawn with probability
  * |<x|Phi>|^2 by inverse CDF with the counter-based
- * SplitMix64 rule (reading R14).  Non-collapsing.  Host out. */
+ * SplitMix64 rule (reading R14): u_s = draw_s x total, outcome =
+ * min{beta : C(beta) > u_s}, C the prefix sum over beta in increasing order
+ * (beta bit b <-> qubits[b]).  Non-collapsing.  Host out[n_shots].
+ * k <= 24: one level (the 2^k marginal, its CDF and a binary search per
+ * shot on the device).  24 < k <= min(n, 40), up to the whole register:
+ * two levels with the same outcome rule, C(beta) = C_hi(beta_hi - 1) +
+ * C_lo(beta_lo): the marginal of the top kh = max(20, k - 16) listed qubits
+ * picks the high bits and the residual draw, then the conditional marginal of
+ * the low k - kh listed qubits inside the drawn high bins (device kernels;
+ * sharded states sum every shard's part in rank order).  QSIM_ERR_ARG for
+ * k > 40. */
 qsim_status qsim_measure(qsim_ctx ctx, const int *qubits, int k, uint64_t seed, uint64_t n_shots,
                          uint64_t *out);
 
@@ -250,6 +260,14 @@ typedef struct {
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);
 qsim_status qsim_reset_stats(qsim_ctx ctx);
+
+/* Roofline denominators measured on the current CUDA device (no context
+ * needed; takes ~0.1 s): *fp64_tflops = FP64 FMA-pipe throughput of a DFMA
+ * probe (8 independent chains per thread, 2 x 256-thread CTAs per SM, the
+ * pass kernel's residency), in TFLOP/s (2 flop per FMA); *copy_gbs =
+ * streaming copy of 2 GiB (read + write bytes) in GB/s.  Either pointer may
+ * be NULL (that probe is skipped).  QSIM_ERR_CUDA if no device. */
+qsim_status qsim_probe_peaks(double *fp64_tflops, double *copy_gbs);
 
 const char *qsim_status_str(qsim_status s);
 const char *qsim_last_error(qsim_ctx ctx);

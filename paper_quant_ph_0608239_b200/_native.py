@@ -59,6 +59,7 @@ EXPORTS = [
     "qsim_measure",
     "qsim_get_amplitudes", "qsim_sync", "qsim_get_layout", "qsim_set_option", "qsim_get_stats",
     "qsim_reset_stats", "qsim_status_str", "qsim_last_error", "qsim_plan_json", "qsim_exchange_peers",
+    "qsim_probe_peaks",
 ]
 
 _lib = None
@@ -105,6 +106,7 @@ def lib():
         "qsim_last_error": ([ctx], ctypes.c_char_p),
         "qsim_plan_json": ([i, i, P(qsim_gate), ctypes.c_size_t, i, ctypes.c_char_p, ctypes.c_size_t], st),
         "qsim_exchange_peers": ([i, i, i, P(i), i, P(i), P(i)], st),
+        "qsim_probe_peaks": ([P(d), P(d)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

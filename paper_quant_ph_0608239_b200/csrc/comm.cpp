@@ -52,7 +52,6 @@ int poll_stream(cudaStream_t s, double timeout_ms, std::string &err, F poll)
 class NcclComm : public Comm {
 public:
     ncclComm_t comm = nullptr;
-    double timeout_ms = 600e3;
     bool aborted = false;
 
     // non-blocking communicator: an NCCL call may return ncclInProgress;
@@ -148,7 +147,6 @@ class LoopbackComm : public Comm {
 public:
     std::shared_ptr<Hub> hub;
     std::string id;
-    double timeout_ms = 600e3;
     struct Op {
         void *buf;
         size_t bytes;

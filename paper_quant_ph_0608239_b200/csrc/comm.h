@@ -43,6 +43,7 @@ public:
     virtual int wait(cudaStream_t s, double timeout_ms, std::string &err) = 0;
     virtual void abort() = 0;
     int rank = 0, size = 1;
+    double timeout_ms = 600e3;  // blocking host waits of the transport (qsim option comm_timeout_ms)
 };
 
 // NCCL communicator from a 128-byte ncclUniqueId; nullptr + err on failure

@@ -906,6 +906,133 @@ void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, doub
     if (n_shots) k_sample<<<grid_for(n_shots, 256), 256, 0, s>>>(cdf, B, seed, n_shots, out);
 }
 
+// --------------------------------------------- two-level sampling (k > 24)
+// Conditional marginals of the low c listed qubits inside nb bins of the
+// high listed qubits (bins[j] = value of the high listed qubits): out[j 2^c +
+// b] = sum over the unlisted qubits (fixed increasing order) of |a|^2 at the
+// amplitude whose listed-low bits are b, listed-high bits bins[j]; only the
+// amplitudes this shard holds (physical bits >= M equal `rank`) contribute.
+struct BinDesc {
+    int32_t c, kh, nu, M;
+    uint64_t rank;
+    int32_t pos_lo[24], pos_hi[24], pos_un[64];
+};
+
+__global__ void k_bin_marginal(const double2 *__restrict__ st, BinDesc d, const uint64_t *__restrict__ bins,
+                               uint64_t nb, double *__restrict__ out)
+{
+    const uint64_t per = 1ULL << d.c, total = nb * per;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = t >> d.c, b = t & (per - 1), h = bins[j];
+        uint64_t base = 0;
+        for (int i = 0; i < d.c; i++) base |= ((b >> i) & 1) << d.pos_lo[i];
+        for (int i = 0; i < d.kh; i++) base |= ((h >> i) & 1) << d.pos_hi[i];
+        double acc = 0.0;
+        const uint64_t nun = 1ULL << d.nu;
+        for (uint64_t u = 0; u < nun; u++) {
+            uint64_t x = base;
+            for (int i = 0; i < d.nu; i++) x |= ((u >> i) & 1) << d.pos_un[i];
+            if ((x >> d.M) != d.rank) continue;
+            const double2 a = st[x & ((1ULL << d.M) - 1)];
+            acc = fma(a.x, a.x, acc);
+            acc = fma(a.y, a.y, acc);
+        }
+        out[t] = acc;
+    }
+}
+
+void launch_bin_marginal(const double2 *st, int M, uint64_t rank, int c, const int *pos_lo, int kh,
+                         const int *pos_hi, int nu, const int *pos_un, const uint64_t *bins, uint64_t nb, double *out,
+                         cudaStream_t s)
+{
+    BinDesc d{};
+    d.c = c;
+    d.kh = kh;
+    d.nu = nu;
+    d.M = M;
+    d.rank = rank;
+    for (int i = 0; i < c; i++) d.pos_lo[i] = pos_lo[i];
+    for (int i = 0; i < kh; i++) d.pos_hi[i] = pos_hi[i];
+    for (int i = 0; i < nu; i++) d.pos_un[i] = pos_un[i];
+    k_bin_marginal<<<grid_for(nb << c, 256), 256, 0, s>>>(st, d, bins, nb, out);
+}
+
+// level 1: per shot, u = draw * total; the high bin (min beta_hi with
+// C[beta_hi] > u, else the last) and the residual u - C[beta_hi - 1]
+__global__ void k_sample_hi(const double *__restrict__ C, uint64_t B, uint64_t seed, uint64_t n,
+                            uint64_t *__restrict__ bhi, double *__restrict__ res)
+{
+    const double tot = C[B - 1];
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n; s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = sm64_dev(seed + (s + 1) * 0x9E3779B97F4A7C15ULL);
+        const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0) * tot;
+        uint64_t lo = 0, hi = B - 1;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (C[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        bhi[s] = lo;
+        res[s] = u - (lo ? C[lo - 1] : 0.0);
+    }
+}
+
+// level 2: one CTA per bin row, the row's inclusive prefix sum (k_cdf order)
+__global__ void __launch_bounds__(1024) k_cdf_rows(double *__restrict__ rows, uint64_t per)
+{
+    __shared__ double tot[1024];
+    double *C = rows + blockIdx.x * per;
+    const uint64_t seg = (per + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * seg, hi = lo + seg < per ? lo + seg : per;
+    double acc = 0.0;
+    for (uint64_t i = lo; i < hi; i++) { acc += C[i]; C[i] = acc; }
+    tot[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < (int)blockDim.x; t++) { const double x = tot[t]; tot[t] = run; run += x; }
+    }
+    __syncthreads();
+    const double off = tot[threadIdx.x];
+    for (uint64_t i = lo; i < hi; i++) C[i] += off;
+}
+
+// per shot of this batch: min beta_lo with C_row[beta_lo] > residual (the last
+// bin of nonzero weight if rounding leaves the residual at the row's end);
+// outcome = beta_lo | beta_hi << c
+__global__ void k_sample_lo(const double *__restrict__ rows, uint64_t per, int c, const uint32_t *__restrict__ shot_row,
+                            const uint64_t *__restrict__ shot_idx, uint64_t n, const uint64_t *__restrict__ bhi,
+                            const double *__restrict__ res, uint64_t *__restrict__ out)
+{
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = shot_idx[t];
+        const double *C = rows + (uint64_t)shot_row[t] * per;
+        const double u = res[s];
+        uint64_t lo = 0, hi = per - 1;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (C[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        while (lo > 0 && C[lo] == (lo ? C[lo - 1] : 0.0)) lo--;  // zero-weight tail (rounding)
+        out[s] = lo | (bhi[s] << c);
+    }
+}
+
+void launch_sample_hi(const double *p, int kh, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *bhi,
+                      double *res, cudaStream_t s)
+{
+    const uint64_t B = 1ULL << kh;
+    k_cdf<<<1, 1024, 0, s>>>(p, B, cdf);
+    if (n_shots) k_sample_hi<<<grid_for(n_shots, 256), 256, 0, s>>>(cdf, B, seed, n_shots, bhi, res);
+}
+
+void launch_sample_lo(double *rows, uint64_t nrows, int c, const uint32_t *shot_row, const uint64_t *shot_idx,
+                      uint64_t n, const uint64_t *bhi, const double *res, uint64_t *out, cudaStream_t s)
+{
+    const uint64_t per = 1ULL << c;
+    k_cdf_rows<<<(unsigned)nrows, 1024, 0, s>>>(rows, per);
+    if (n) k_sample_lo<<<grid_for(n, 256), 256, 0, s>>>(rows, per, c, shot_row, shot_idx, n, bhi, res, out);
+}
+
 // ------------------------------------------------------------- readout
 struct Phys64 {
     int32_t p[64];
@@ -1095,6 +1222,90 @@ void launch_pack(const double2 *shard, double2 *buf, int M, int K, const int *lp
     LPos L = make_lpos(K, lpos, c, &off);
     (void)M;
     k_pack<<<grid_for(count, 256), 256, 0, s>>>(const_cast<double2 *>(shard), buf, first, count, K, L, off, unpack);
+}
+
+// ------------------------------------------------ roofline denominators
+// FP64 FMA-pipe throughput probe: 8 independent DFMA chains per thread, two
+// 256-thread CTAs per SM per wave (the pass kernel's residency), many waves.
+__global__ void __launch_bounds__(256) k_probe_dfma(double *out, int iters, double a, double b)
+{
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+           x7 = x0 + 7;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (r == 12345.678) out[blockIdx.x] = r;  // keeps the chains live, never true
+}
+
+// streaming copy (read + write), 256-bit accesses, grid-stride
+__global__ void k_probe_copy(const double4 *__restrict__ in, double4 *__restrict__ out, size_t n)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+int probe_peaks(double *fp64_flops, double *copy_bytes_per_s, int reps)
+{
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return -1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double *out = nullptr;
+    int rc = 0;
+    if (cudaMalloc(&out, sizeof(double) * sms * 64) != cudaSuccess) rc = -1;
+    if (!rc && fp64_flops) {
+        const int iters = 2048, blocks = sms * 2 * 8;
+        k_probe_dfma<<<blocks, 256, 0, s>>>(out, 16, 1.0000001, 1e-9);
+        float best = 1e30f;
+        for (int r = 0; r < reps; r++) {
+            cudaEventRecord(e0, s);
+            k_probe_dfma<<<blocks, 256, 0, s>>>(out, iters, 1.0000001, 1e-9);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+        }
+        *fp64_flops = 2.0 * (double)blocks * 256 * iters * 16 * 8 / (best * 1e-3);
+    }
+    if (!rc && copy_bytes_per_s) {
+        const size_t bytes = (size_t)2 << 30;
+        double4 *a = nullptr, *b = nullptr;
+        if (cudaMalloc(&a, bytes) != cudaSuccess || cudaMalloc(&b, bytes) != cudaSuccess) {
+            rc = -1;
+        } else {
+            cudaMemsetAsync(a, 0, bytes, s);
+            const size_t n = bytes / sizeof(double4);
+            float best = 1e30f;
+            for (int r = 0; r < reps + 1; r++) {
+                cudaEventRecord(e0, s);
+                k_probe_copy<<<sms * 8, 256, 0, s>>>(a, b, n);
+                cudaEventRecord(e1, s);
+                cudaEventSynchronize(e1);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (r) best = ms < best ? ms : best;
+            }
+            *copy_bytes_per_s = 2.0 * bytes / (best * 1e-3);
+        }
+        cudaFree(a);
+        cudaFree(b);
+    }
+    cudaFree(out);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    if (cudaGetLastError() != cudaSuccess) rc = -1;
+    return rc;
 }
 
 }  // namespace qsb

@@ -54,6 +54,21 @@ void launch_pair_gate(double2 *A, double2 *B, int M, uint64_t mloc, uint64_t vlo
 void launch_pair_combine(double2 *own, const double2 *other, uint64_t off, uint64_t count, uint64_t mloc,
                          uint64_t vloc, const double *c0, const double *c1, int self_first, cudaStream_t s);
 void launch_sum_ranks(const double *all, double *out, uint64_t count, int S, cudaStream_t s);
+// conditional marginals of the c low listed qubits inside bins of the kh high
+// listed qubits (two-level sampling of k > 24 qubits); this shard's part
+void launch_bin_marginal(const double2 *st, int M, uint64_t rank, int c, const int *pos_lo, int kh,
+                         const int *pos_hi, int nu, const int *pos_un, const uint64_t *bins, uint64_t nb, double *out,
+                         cudaStream_t s);
+// level 1 of the two-level sampler: CDF of the high-qubit marginal (2^kh),
+// per shot the high bin and the residual draw
+void launch_sample_hi(const double *p, int kh, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *bhi,
+                      double *res, cudaStream_t s);
+// level 2: prefix sums of nrows bin rows (2^c each, in place), then per shot
+// (shot_idx[t], its row shot_row[t]) the low bits; out[s] = lo | bhi[s] << c
+void launch_sample_lo(double *rows, uint64_t nrows, int c, const uint32_t *shot_row, const uint64_t *shot_idx,
+                      uint64_t n, const uint64_t *bhi, const double *res, uint64_t *out, cudaStream_t s);
 int pass_regs_per_thread();
+// measured FP64 FMA-pipe flop/s (DFMA probe) and streaming-copy bytes/s (read + write) of the current device
+int probe_peaks(double *fp64_flops, double *copy_bytes_per_s, int reps);
 
 }  // namespace qsb

@@ -1408,10 +1408,106 @@ qsim_status qsim_expectations_async(qsim_ctx c, double *out)
     return expectations_impl(c, out, false);
 }
 
+// Two-level sampler for k > 24 listed qubits (up to the whole
+// register): the same draw u_s and the same outcome min{beta : C(beta) > u_s}
+// as the one-level rule (reading R14), with C(beta) = C_hi(beta_hi - 1) +
+// C_lo(beta_lo).  Level 1: the marginal of the top kh listed qubits (the
+// qsim_probabilities path), its CDF and, per shot, the high bin and the
+// residual draw, on the device.  Level 2: for the distinct high bins, the
+// conditional marginal of the c low listed qubits (k_bin_marginal, every
+// shard's part summed in rank order), its CDF and the low bits by binary
+// search, on the device.  Memory: 2^kh + batches of <= 2^24 bin entries.
+static qsim_status measure_two_level(qsim_ctx c, const int *qubits, int k, uint64_t seed, uint64_t n_shots,
+                                     uint64_t *out)
+{
+    const int kh = std::max(20, k - 16), cl = k - kh;
+    uint64_t seen = 0;
+    for (int j = 0; j < k; j++) {
+        if (qubits[j] < 0 || qubits[j] >= c->n) FAIL(c, QSIM_ERR_QUBIT_RANGE, "qubit %d", qubits[j]);
+        if ((seen >> qubits[j]) & 1) FAIL(c, QSIM_ERR_DUP_QUBIT, "qubit %d repeated", qubits[j]);
+        seen |= 1ULL << qubits[j];
+    }
+    std::vector<double> phi((size_t)1 << kh);
+    qsim_status s = probabilities_impl(c, qubits + cl, kh, phi.data());
+    if (s != QSIM_OK) return s;
+    if (!n_shots) return QSIM_OK;
+    const size_t BH = phi.size(), per = (size_t)1 << cl;
+    const size_t batch_rows = std::max<size_t>(1, ((size_t)1 << 24) / per);
+    // device: p_hi | CDF | res (n) | rows (batch_rows x per) | bhi, shot_idx, out (n each) | bins | shot_row (u32)
+    const size_t need = 2 * BH + n_shots + batch_rows * per + 3 * n_shots + batch_rows + n_shots / 2 + 8;
+    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
+    double *dp = c->d_red, *dc = dp + BH, *dres = dc + BH, *drows = dres + n_shots;
+    uint64_t *dbhi = (uint64_t *)(drows + batch_rows * per), *didx = dbhi + n_shots, *dout = didx + n_shots,
+             *dbins = dout + n_shots;
+    uint32_t *drow = (uint32_t *)(dbins + batch_rows);
+    RangeGuard rg(c, 4, 0);
+    CK(c, cudaMemcpyAsync(dp, phi.data(), BH * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_sample_hi(dp, kh, seed, n_shots, dc, dbhi, dres, c->stream);
+    LAUNCHED(c);
+    std::vector<uint64_t> bhi(n_shots);
+    CK(c, cudaMemcpyAsync(bhi.data(), dbhi, n_shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
+    // shots grouped by high bin (host bookkeeping: which rows to build)
+    std::vector<uint64_t> order(n_shots);
+    for (uint64_t i = 0; i < n_shots; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return bhi[a] < bhi[b]; });
+    int pos_lo[24], pos_hi[24], pos_un[64], nu = 0;
+    for (int j = 0; j < cl; j++) pos_lo[j] = c->planner->phys_of[qubits[j]];
+    for (int j = 0; j < kh; j++) pos_hi[j] = c->planner->phys_of[qubits[cl + j]];
+    for (int q = 0; q < c->n; q++)
+        if (!((seen >> q) & 1)) pos_un[nu++] = c->planner->phys_of[q];
+    // rows of one batch: per shard its part, summed in rank order (on the
+    // host for SPMD ranks, as the marginals are)
+    std::vector<std::vector<double>> per_rank(n_local(c));
+    std::vector<double> rows;
+    for (uint64_t i0 = 0; i0 < n_shots;) {
+        std::vector<uint64_t> bins;
+        std::vector<uint32_t> shot_row;
+        std::vector<uint64_t> shot_idx;
+        uint64_t i = i0;
+        while (i < n_shots) {
+            const uint64_t b = bhi[order[i]];
+            if (bins.empty() || bins.back() != b) {
+                if (bins.size() == batch_rows) break;
+                bins.push_back(b);
+            }
+            shot_row.push_back((uint32_t)(bins.size() - 1));
+            shot_idx.push_back(order[i]);
+            i++;
+        }
+        const size_t nb = bins.size(), len = nb * per;
+        CK(c, cudaMemcpyAsync(dbins, bins.data(), nb * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        rows.assign(len, 0.0);
+        for (int r = 0; r < n_local(c); r++) {
+            per_rank[r].assign(len, 0.0);
+            launch_bin_marginal(c->shards[r], c->M, (uint64_t)local_ranks(c, r), cl, pos_lo, kh, pos_hi, nu, pos_un,
+                                dbins, nb, drows, c->stream);
+            LAUNCHED(c);
+            CK(c, cudaMemcpyAsync(per_rank[r].data(), drows, len * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
+        }
+        if ((s = sum_over_ranks(c, per_rank, rows.data(), len)) != QSIM_OK) return s;
+        CK(c, cudaMemcpyAsync(drows, rows.data(), len * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaMemcpyAsync(drow, shot_row.data(), shot_row.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaMemcpyAsync(didx, shot_idx.data(), shot_idx.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        launch_sample_lo(drows, nb, cl, drow, didx, shot_idx.size(), dbhi, dres, dout, c->stream);
+        LAUNCHED(c);
+        { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
+        i0 = i;
+    }
+    CK(c, cudaMemcpyAsync(out, dout, n_shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
+    return QSIM_OK;
+}
+
 qsim_status qsim_measure(qsim_ctx c, const int *qubits, int k, uint64_t seed, uint64_t n_shots, uint64_t *out)
 {
     GUARD(c);
     if (n_shots && !out) return QSIM_ERR_ARG;
+    if (k > 24) {
+        if (k > 40 || k > c->n || !qubits) FAIL(c, QSIM_ERR_ARG, "measure: k=%d (at most min(n, 40) listed qubits)", k);
+        return measure_two_level(c, qubits, k, seed, n_shots, out);
+    }
     const size_t B = (size_t)1 << (k < 0 ? 0 : k);
     std::vector<double> p(B);
     qsim_status s = probabilities_impl(c, qubits, k, p.data());
@@ -1473,7 +1569,10 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
-    else if (k == "comm_timeout_ms") c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
+    else if (k == "comm_timeout_ms") {
+        c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
+        if (c->comm) c->comm->timeout_ms = c->comm_timeout_ms;
+    }
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
     else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
     else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }
@@ -1504,6 +1603,16 @@ qsim_status qsim_reset_stats(qsim_ctx c)
     qsim_status s = collect_timing(c);
     if (s != QSIM_OK) return s;
     std::memset(&c->stats, 0, sizeof(c->stats));
+    return QSIM_OK;
+}
+
+qsim_status qsim_probe_peaks(double *fp64_tflops, double *copy_gbs)
+{
+    if (!fp64_tflops && !copy_gbs) return QSIM_ERR_ARG;
+    double f = 0, b = 0;
+    if (qsb::probe_peaks(fp64_tflops ? &f : nullptr, copy_gbs ? &b : nullptr, 5) != 0) return QSIM_ERR_CUDA;
+    if (fp64_tflops) *fp64_tflops = f / 1e12;
+    if (copy_gbs) *copy_gbs = b / 1e9;
     return QSIM_OK;
 }
 

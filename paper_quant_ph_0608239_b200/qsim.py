@@ -78,6 +78,16 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
+def probe_peaks(fp64: bool = True, copy: bool = True) -> dict:
+    """Measured roofline denominators of the current CUDA device
+    (qsim_probe_peaks): FP64 FMA-pipe TFLOP/s and streaming-copy GB/s."""
+    f, b = ctypes.c_double(0), ctypes.c_double(0)
+    s = N.lib().qsim_probe_peaks(ctypes.byref(f) if fp64 else None, ctypes.byref(b) if copy else None)
+    if s != 0:
+        raise QsimError(s, "qsim_probe_peaks")
+    return {"fp64_tflops": f.value if fp64 else None, "copy_gbs": b.value if copy else None}
+
+
 def get_loopback_id() -> bytes:
     """Id of a new loopback group (QSim(..., transport="loopback", nccl_id=id))."""
     buf = (ctypes.c_uint8 * 128)()

@@ -126,13 +126,21 @@ class ShorResult:
     expectations: np.ndarray  # <Q_i>, i < X (Eq. Shor7)
 
 
-def run(G: int, y: int, X: int, F: int, shots: int = 16, seed: int = 1, sim=None) -> ShorResult:
+def run(G: int, y: int, X: int, F: int, shots: int = 16, seed: int = 1, sim=None,
+        full_register: bool = True) -> ShorResult:
+    """full_register: draw basis states of the WHOLE (X + F)-qubit register
+    (the two-level sampler when X + F > 24) and keep their
+    x-register bits; else sample the x-register marginal directly."""
     from .qsim import QSim, pack_gates
     sim = sim or QSim(X + F)
     gates = circuit(G, y, X, F)
     sim.init_basis(1 << X)
     sim.run_circuit(gates, packed=pack_gates(gates))
     ex = sim.expectations()[:X]
-    samples = sim.measure(list(range(X)), seed=seed, shots=shots)
+    if full_register:
+        full = sim.measure(list(range(X + F)), seed=seed, shots=shots)
+        samples = full & np.uint64((1 << X) - 1)
+    else:
+        samples = sim.measure(list(range(X)), seed=seed, shots=shots)
     r = order_from_samples(samples, X, G, y)
     return ShorResult(samples, r, factors_from_order(G, y, r) if r else None, ex)

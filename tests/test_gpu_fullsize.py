@@ -1,0 +1,133 @@
+"""Full-size parity at BASELINE.json's configs (-m gpu), amplitude by amplitude.
+
+North-star bar: max |delta amplitude| <= 1e-11, |1 - ||psi||^2| <= 1e-12.
+- config 3 (Shor, 28 q, N=899): the whole 2^28-amplitude state against the
+  oracle run of the same 216 gates (4 GiB on each side), plus the control
+  marginal against the corrected closed form (DESIGN R1/R8).
+- config 4 (QFT, 32 q, 64 GiB on one GPU): all 2^32 amplitudes against the
+  closed form e^{2 pi i x0 k / 2^32} / 2^16 with the phase reduced in integers
+  (P:1034-1036 QFT definition; DESIGN R5), in 1 GiB chunks, computed with
+  plain torch CPU ops.
+- config 5 circuit family (H on all, Haar layers + CNOT chain, per-position
+  sweep) at 28 q on 8 virtual shards (3 nonlocal qubits, K-pair exchanges,
+  P:759-779) and at 26 q on 8 loopback ranks (the NCCL-branch exchange code):
+  the whole state against the oracle.
+"""
+import numpy as np
+import pytest
+
+from tests import pins
+from workloads import circuits as C
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+NORM_TOL = 1e-12
+CHUNK = 1 << 26
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_quant_ph_0608239_b200 as pkg
+    return pkg
+
+
+def _need_gpu_bytes(nbytes):
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < nbytes:
+        pytest.skip(f"needs {nbytes >> 30} GiB free on the GPU")
+
+
+def _chunked_max_diff(sim, n, ref_view):
+    err = 0.0
+    for first in range(0, 1 << n, CHUNK):
+        g = sim.get_amplitudes(first, min(CHUNK, (1 << n) - first))
+        err = max(err, float(np.max(np.abs(g - ref_view[first:first + g.size]))))
+    return err
+
+
+def test_config3_full_state(P, oracle_mod):
+    """BASELINE config 3 at full size: every amplitude vs the oracle."""
+    w = C.config3_shor()
+    sim = P.QSim(w.n)
+    sim.init_basis(w.init)
+    sim.run_circuit(w.gates)
+    st = sim.stats()
+    o = oracle_mod.Oracle(w.n)
+    o.init_basis(w.init)
+    o.run(w.gates)
+    err = _chunked_max_diff(sim, w.n, o.psi.view(np.complex128))
+    assert err <= TOL, err
+    assert abs(1 - sim.norm()) <= NORM_TOL
+    assert st["perm_launches"] >= 1  # the permutation path ran
+    ctl = list(range(18))
+    assert np.max(np.abs(sim.probabilities(ctl) - pins.shor_pk(w.meta["r"], 18))) <= 1e-10
+    sim.close()
+
+
+def test_config4_qft32_all_amplitudes(P):
+    """BASELINE config 4 on one GPU: all 2^32 amplitudes vs the closed form."""
+    import torch
+    _need_gpu_bytes(70 << 30)
+    w = C.config4_qft()
+    n, x0 = 32, w.meta["x0"]
+    sim = P.QSim(n)
+    sim.init_basis(w.init)
+    sim.run_circuit(w.gates)
+    nrm = sim.norm()
+    err = 0.0
+    mask = (1 << n) - 1
+    two_pi = 2.0 * np.pi / float(1 << n)
+    for first in range(0, 1 << n, CHUNK):
+        got = torch.from_numpy(sim.get_amplitudes(first, CHUNK))
+        k = torch.arange(first, first + CHUNK, dtype=torch.int64)
+        ph = ((k * x0) & mask).to(torch.float64) * two_pi  # (x0 k) mod 2^n exactly: both < 2^32, product < 2^63
+        ref = torch.complex(torch.cos(ph), torch.sin(ph)) / float(1 << (n // 2))
+        err = max(err, float((got - ref).abs().max()))
+    assert err <= TOL, err
+    assert abs(1 - nrm) <= NORM_TOL
+    sim.close()
+
+
+def test_config5_family_28q_8_virtual_shards(P, oracle_mod):
+    """The config-5 family at 28 q on 8 virtual shards (M = 25): whole state."""
+    n = 28
+    gates = C.random_chain(n, 10, seed=5, sweep=True)
+    sim = P.QSim(n, n_ranks=8, transport="virtual")
+    sim.init_basis(0)
+    sim.run_circuit(gates)
+    st = sim.stats()
+    o = oracle_mod.Oracle(n)
+    o.init_basis(0)
+    o.run(gates)
+    err = _chunked_max_diff(sim, n, o.psi.view(np.complex128))
+    assert err <= TOL, err
+    assert abs(1 - sim.norm()) <= NORM_TOL
+    assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-12
+    assert st["exchanges"] >= 1
+    sim.close()
+
+
+def test_config5_family_26q_8_loopback_ranks(P, oracle_mod):
+    """The same family at 26 q on 8 SPMD ranks of the loopback transport (the
+    NCCL-branch exchange engine, default scratch): whole state on every rank."""
+    n = 26
+    gates = C.random_chain(n, 10, seed=5, sweep=True)
+    o = oracle_mod.Oracle(n)
+    o.init_basis(0)
+    o.run(gates)
+    ref = o.psi.view(np.complex128)
+
+    def body(sim, r):
+        sim.init_basis(0)
+        sim.run_circuit(gates)
+        err = _chunked_max_diff(sim, n, ref)
+        return err, sim.norm(), sim.stats()["exchanges"]
+
+    for err, nrm, ex in P.run_loopback(n, 8, body):
+        assert err <= TOL, err
+        assert abs(1 - nrm) <= NORM_TOL
+        assert ex >= 1
