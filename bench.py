@@ -282,10 +282,12 @@ def per_config(pk, local):
             continue
         sim = QSim(n)
         packed = pack_gates(gates)
+        exb = torch.empty(n, dtype=torch.float64, pin_memory=True)
 
-        def step():
+        def step():  # as the headline step: init + circuit + <Q_i> (the readout flushes the queue)
             sim.init_basis(init)
             sim.run_circuit(gates, packed=packed)
+            sim.expectations_async(exb)
 
         step()
         sim.sync()
@@ -466,7 +468,7 @@ def run_ours(args):
             "gpu_launches": int(st_value["kernel_launches"]),
             "roofline": {"bound": "alu", "achieved": fp64_ach, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (fp64_ach / fp64_peak) if fp64_ach else None, "traffic": traffic,
-                         "traffic_source": "static: ncu --set full capture of a config-2 pass, profiles/pass_traffic.json",
+                         "traffic_source": "static: ncu --set full capture of a config-2 pass this round (profiles/pass_traffic.json, profiles/r2_pass_c2.txt)",
                          "kernel": "qsim_pass (NVRTC pass-specialised tile pass)",
                          "peak_source": pk["fp64_src"], "peak_derived": pk["fp64_derived"],
                          "frac_of_derived": (fp64_ach / pk["fp64_derived"]) if fp64_ach else None,

@@ -55,6 +55,7 @@ def test_config3_full_state(P, oracle_mod):
     sim = P.QSim(w.n)
     sim.init_basis(w.init)
     sim.run_circuit(w.gates)
+    sim.sync()
     st = sim.stats()
     o = oracle_mod.Oracle(w.n)
     o.init_basis(w.init)
@@ -99,6 +100,7 @@ def test_config5_family_28q_8_virtual_shards(P, oracle_mod):
     sim = P.QSim(n, n_ranks=8, transport="virtual")
     sim.init_basis(0)
     sim.run_circuit(gates)
+    sim.sync()
     st = sim.stats()
     o = oracle_mod.Oracle(n)
     o.init_basis(0)
