@@ -138,9 +138,11 @@ constexpr int kMaxPermRun = 32;
 // shared memory of one k_perm_run CTA: two staged tiles (16 B per element),
 // one control mask per extra-bit pattern, R tables of 2^t uint16
 constexpr size_t kPermRunSmemMax = 226 * 1024;  // 227 KB per block less room for the kernel's static smem
-QSB_HD size_t perm_run_smem_bytes(int tile_bits, int t, int R)
+QSB_HD size_t perm_run_smem_bytes(int tile_bits, int t, int R, bool compose = false)
 {
-    return ((size_t)32 << tile_bits) + ((size_t)4 << (tile_bits - t)) + (size_t)R * ((size_t)2 << t);
+    // 2 tile buffers | in-tile control masks | R inverse tables [+ the slow-head
+    // table + 2 composed tables] (uint16)
+    return ((size_t)32 << tile_bits) + ((size_t)4 << (tile_bits - t)) + (size_t)(R + (compose ? 3 : 0)) * ((size_t)2 << t);
 }
 struct PermRunDesc {
     uint64_t rank_bits;
@@ -155,6 +157,14 @@ struct PermRunDesc {
     int32_t tile_sorted[kPermTileBits];
     uint32_t m_tile[kMaxPermRun], v_tile[kMaxPermRun];  // controls on tile-local bits
     uint64_t m_out[kMaxPermRun], v_out[kMaxPermRun];    // controls outside the tile (incl. rank bits)
+    // Composition (k_perm_run): pre_mask = the perms at the head of the gather
+    // chain (highest j first) with no in-tile control: for a tile their active
+    // subset is CTA-uniform, so they are composed into one table per tile.
+    // slow_mask (a head of pre_mask) = those whose controls change at most
+    // every 2^b tiles of a CTA's contiguous instance range: composed once per
+    // change into the slow table the per-tile composition starts from.
+    // (pre_mask != 0: instances in one contiguous range per CTA; else grid-stride)
+    uint32_t pre_mask, slow_mask;
 };
 
 }  // namespace qsb

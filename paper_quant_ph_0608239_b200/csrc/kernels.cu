@@ -507,6 +507,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 constexpr int kPermRunThreads = 512;
+// Composition (PermRunDesc pre_mask / slow_mask): the gather chain of an
+// element is P_jk^-1 o ... with j descending.  Its head, the perms without
+// in-tile controls, has the same active subset for every element of a tile
+// (CTA-uniform), so per tile it is composed once into a 2^t-entry table
+// (2^t lookups per head perm instead of 2^tile_bits); the slowest part of
+// that head, whose controls only change every few tiles of the CTA's
+// contiguous instance range, is itself composed once per change.  An element
+// then does one lookup for the head plus its in-tile-controlled perms.
 __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_constant__ PermRunDesc d, double2 *__restrict__ st,
                                                   const uint32_t *__restrict__ tabs)
 {
@@ -515,6 +523,8 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
     double2 *bufs = reinterpret_cast<double2 *>(smraw);                                        // 2 x E
     uint32_t *xmask = reinterpret_cast<uint32_t *>(smraw + 2 * (size_t)E * sizeof(double2));  // NX entries
     uint16_t *tab = reinterpret_cast<uint16_t *>(xmask + NX);                                // R * TT entries
+    uint16_t *slow_tab = tab + (size_t)d.R * TT;                                             // TT
+    uint16_t *comp = slow_tab + TT;                                                           // 2 x TT
     for (uint32_t i = threadIdx.x; i < (uint32_t)d.R * TT; i += blockDim.x) tab[i] = (uint16_t)__ldg(tabs + d.tab_offset + i);
     // in-tile control predicates of every extra-bit pattern x (tile-local e = x << t | w)
     for (uint32_t x = threadIdx.x; x < NX; x += blockDim.x) {
@@ -524,9 +534,14 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
         xmask[x] = m;
     }
     __syncthreads();
-    // this CTA's next tile (from `inst` on) that some perm touches; CTA-uniform
+    // this CTA's contiguous instance range; the next tile (from `inst` on)
+    // that some perm touches; CTA-uniform
+    const bool compose = d.pre_mask != 0;
+    const uint64_t per = compose ? (d.n_inst + gridDim.x - 1) / gridDim.x : d.n_inst;
+    const uint64_t i_first = compose ? (uint64_t)blockIdx.x * per : blockIdx.x, step = compose ? 1 : gridDim.x;
+    const uint64_t i_end = compose ? min(d.n_inst, i_first + per) : d.n_inst;
     auto next_tile = [&](uint64_t inst, uint64_t &base, uint32_t &A) {
-        for (; inst < d.n_inst; inst += gridDim.x) {
+        for (; inst < i_end; inst += step) {
             base = inst;
             for (int j = 0; j < d.tile_bits; j++) base = insert_zero(base, d.tile_sorted[j]);
             A = 0;  // perms whose out-of-tile controls this tile satisfies
@@ -534,29 +549,51 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
                 if (((d.rank_bits | base) & d.m_out[j]) == d.v_out[j]) A |= 1u << j;
             if (A) break;
         }
-        return inst;
+        return inst < i_end ? inst : d.n_inst;
     };
     auto stage = [&](double2 *buf, uint64_t base, uint32_t A) {
         for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
             if (A & xmask[e >> d.t])
                 cp_async16(buf + e, st + base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits)));
     };
+    // chain of the perms in `m` (descending j) applied to v
+    auto chain = [&](uint32_t m, uint32_t v) {
+        while (m) {
+            const int j = 31 - __clz(m);
+            v = tab[j * TT + v];
+            m &= ~(1u << j);
+        }
+        return v;
+    };
+    uint32_t slow_cur = 0xffffffffu;  // subset the slow table holds (uniform)
+    auto build = [&](uint32_t A, uint16_t *dst) {  // caller: the slow table may be rebuilt (no reader)
+        const uint32_t S = A & d.slow_mask, F = A & d.pre_mask & ~d.slow_mask;
+        if (S != slow_cur) {
+            for (uint32_t w = threadIdx.x; w < TT; w += blockDim.x) slow_tab[w] = (uint16_t)chain(S, w);
+            slow_cur = S;
+            __syncthreads();
+        }
+        for (uint32_t w = threadIdx.x; w < TT; w += blockDim.x) dst[w] = (uint16_t)chain(F, slow_tab[w]);
+    };
     // tile k+1's (instance, base, active set) is found by one thread while the
     // CTA gathers tile k-1, and read by all from a two-slot ring
     __shared__ unsigned long long s_inst[2], s_base[2];
     __shared__ uint32_t s_A[2];
     if (threadIdx.x == 0) {
-        uint64_t b0, b1;
-        uint32_t a0, a1;
-        const uint64_t i0 = next_tile(blockIdx.x, b0, a0);
-        const uint64_t i1 = next_tile(i0 + gridDim.x, b1, a1);
+        uint64_t b0 = 0, b1 = 0;
+        uint32_t a0 = 0, a1 = 0;
+        const uint64_t i0 = next_tile(i_first, b0, a0);
+        const uint64_t i1 = i0 < d.n_inst ? next_tile(i0 + step, b1, a1) : d.n_inst;
         s_inst[0] = i0; s_base[0] = b0; s_A[0] = a0;
         s_inst[1] = i1; s_base[1] = b1; s_A[1] = a1;
     }
     __syncthreads();
     uint64_t inst = s_inst[0], base = s_base[0];
     uint32_t A = s_A[0];
-    if (inst < d.n_inst) stage(bufs, base, A);
+    if (inst < d.n_inst) {
+        stage(bufs, base, A);
+        if (compose) build(A, comp);
+    }
     cp_async_commit();
     for (int b = 0; inst < d.n_inst; b ^= 1) {
         const uint64_t ninst = s_inst[b ^ 1], nbase = s_base[b ^ 1];
@@ -564,24 +601,32 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
         if (ninst < d.n_inst) stage(bufs + (size_t)(b ^ 1) * E, nbase, nA);
         cp_async_commit();  // (possibly empty) group of the next tile
         cp_async_wait1();   // this thread's copies of the current tile landed
-        __syncthreads();
+        __syncthreads();    // ... and everyone's; comp[b] complete
         if (threadIdx.x == 0) {  // slot b (this tile's) is free: every thread read it last iteration
-            uint64_t b2;
-            uint32_t a2;
-            const uint64_t i2 = next_tile(ninst + gridDim.x, b2, a2);
+            uint64_t b2 = 0;
+            uint32_t a2 = 0;
+            const uint64_t i2 = ninst < d.n_inst ? next_tile(ninst + step, b2, a2) : d.n_inst;
             s_inst[b] = i2; s_base[b] = b2; s_A[b] = a2;
         }
         const double2 *sm = bufs + (size_t)b * E;
+        const uint16_t *cb = comp + (size_t)b * TT;
+        const uint32_t head = compose ? (A & d.pre_mask) : 0u;  // composed part of every element's chain
+        const uint32_t rest = compose ? ~d.pre_mask : ~0u;
         if (d.contiguous && d.t >= 2) {
             // 4 consecutive elements share the non-target bits: 4 independent
             // lookup chains per thread
             double2 *dst = st + base;
             for (uint32_t e = 4 * threadIdx.x; e < E; e += 4 * blockDim.x) {
-                uint32_t act = A & xmask[e >> d.t];
-                if (!act) continue;
+                const uint32_t all = A & xmask[e >> d.t];
+                if (!all) continue;
+                uint32_t act = all & rest;
                 uint32_t w[4];
 #pragma unroll
                 for (int i = 0; i < 4; i++) w[i] = (e + i) & T;
+                if (head) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) w[i] = cb[w[i]];
+                }
                 while (act) {
                     const int j = 31 - __clz(act);  // latest active perm first (inverse order)
                     const uint16_t *tj = tab + j * TT;
@@ -595,17 +640,16 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
             }
         } else {
             for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
-                uint32_t act = A & xmask[e >> d.t];
-                if (!act) continue;
+                const uint32_t all = A & xmask[e >> d.t];
+                if (!all) continue;
                 uint32_t w = e & T;
-                while (act) {
-                    const int j = 31 - __clz(act);
-                    w = tab[j * TT + w];
-                    act &= ~(1u << j);
-                }
+                if (head) w = cb[w];
+                w = chain(all & rest, w);
                 st[base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits))] = sm[(e & ~T) | w];
             }
         }
+        // the next tile's composed table (comp[b ^ 1] was last read two tiles ago)
+        if (compose && ninst < d.n_inst) build(nA, comp + (size_t)(b ^ 1) * TT);
         __syncthreads();  // the buffer is refilled two tiles on; slot b is visible
         inst = ninst;
         base = nbase;
@@ -613,7 +657,7 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
     }
 }
 
-size_t perm_run_smem(const PermRunDesc &d) { return perm_run_smem_bytes(d.tile_bits, d.t, d.R); }
+size_t perm_run_smem(const PermRunDesc &d) { return perm_run_smem_bytes(d.tile_bits, d.t, d.R, d.pre_mask != 0); }
 
 void launch_perm_run(const PermRunDesc &d, double2 *st, const uint32_t *perm_tab, int n_sm, cudaStream_t s)
 {

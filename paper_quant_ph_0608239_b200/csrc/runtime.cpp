@@ -644,6 +644,26 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
             if (tl >= 0) { d.m_tile[j] |= 1u << tl; d.v_tile[j] |= 1u << tl; }
             else { d.m_out[j] |= 1ULL << b; d.v_out[j] |= 1ULL << b; }
         }
+    // composition head (PermRunDesc): the perms at the top of the gather
+    // chain (highest j) without in-tile controls; of those, the ones whose
+    // controls sit on instance bits >= 4 (or on rank bits) form the
+    // slow head.  QSIM_PERMRUN_COMPOSE=0 disables (A/B), QSIM_PERMRUN_SLOWBIT sets the bit.
+    static const int compose = [] { const char *e = getenv("QSIM_PERMRUN_COMPOSE"); return e ? atoi(e) : 1; }();
+    static const int slow_bit = [] { const char *e = getenv("QSIM_PERMRUN_SLOWBIT"); return e ? atoi(e) : 4; }();
+    if (compose && perm_run_smem_bytes(tb, t, R, true) <= kPermRunSmemMax) {
+        for (int j = R - 1; j >= 0 && d.m_tile[j] == 0; j--) d.pre_mask |= 1u << j;
+        for (int j = R - 1; j >= 0 && ((d.pre_mask >> j) & 1); j--) {
+            bool slow = true;
+            for (int b = 0; b < M && slow; b++) {
+                if (!((d.m_out[j] >> b) & 1)) continue;
+                int below = 0;  // tile positions below b: the instance bit of b is b - below
+                for (int i = 0; i < tb; i++) below += d.tile_pos[i] < b;
+                slow = b - below >= slow_bit;
+            }
+            if (!slow) break;
+            d.slow_mask |= 1u << j;
+        }
+    }
     if (perm_run_smem(d) > kPermRunSmemMax) FAIL(c, QSIM_ERR_ARG, "permutation run too large for shared memory");
     RangeGuard rg(c, 2, 0);
     for (int i = 0; i < n_local(c); i++) {
