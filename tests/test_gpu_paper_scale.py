@@ -78,3 +78,45 @@ def test_shor_table3_L33(P, G, y, r):
     sim.close()
     del sim
     torch.cuda.empty_cache()
+
+
+def test_paper_adder_3_11QBA_33q(P):
+    """The paper's 3-11QBA adder (Table IV; Fig. 2) at its
+    size, 33 qubits (128 GiB): N_O = 286 as printed, and the sum register holds
+    292 + 585 + 1170 = 2047 with probability 1 (reading R15)."""
+    import torch
+    torch.cuda.empty_cache()
+    w = C.paper_adder("3-11QBA")
+    assert w.n == 33 and len(w.gates) == w.meta["n_o_paper"] == 286
+    sim = P.QSim(33)
+    sim.init_basis(0)
+    sim.run_circuit(w.gates)
+    p = sim.probabilities(w.meta["sum_register"])
+    assert w.meta["expect_sum"] == 2047 and p[2047] >= 1 - 1e-12
+    assert abs(1 - sim.norm()) <= 1e-12
+    # the other registers keep their loaded values (up to the phase of the doubled gates)
+    assert sim.probabilities(list(range(11)))[292] >= 1 - 1e-12
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+
+
+def test_h_on_all_33q(P):
+    """H on all 33 qubits (the paper's scaling test, Tables IV-IX
+    "H" rows): every <Q_i> = 1/2, norm 1, and sampled amplitudes equal
+    2^(-33/2) (closed form)."""
+    import torch
+    torch.cuda.empty_cache()
+    w = C.h_on_all(33)
+    sim = P.QSim(33)
+    sim.init_basis(0)
+    sim.run_circuit(w.gates)
+    assert np.max(np.abs(sim.expectations() - 0.5)) <= 1e-12
+    assert abs(1 - sim.norm()) <= 1e-12
+    rng = np.random.default_rng(33)
+    for first in rng.integers(0, (1 << 33) - 4096, size=8):
+        a = sim.get_amplitudes(int(first), 4096)
+        assert np.max(np.abs(a - 2.0 ** -16.5)) <= 1e-15
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
