@@ -230,7 +230,9 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb"
  * (exchange piece cap; the pieces are double-buffered between the engine
  * stream and a transfer stream), "comm_timeout_ms", "jit", "plan_cache",
- * "pass_variant", "global_policy". */
+ * "pass_variant", "global_policy", "overlap" (1 = a pass followed by an
+ * exchange of the top local bits runs block by block with each block's
+ * transfer overlapping the next block's compute [default]; 0 = in sequence). */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {
@@ -256,6 +258,9 @@ typedef struct {
     double pass_fp64_slots;    /* algorithmic FP64 FMA-pipe instructions of the timed passes (timing=1) */
     uint64_t plan_cache_hits;  /* flushes that reused a cached plan */
     uint64_t streamed_steps;   /* plan steps launched while the planner was still running */
+    uint64_t overlapped;       /* pass + exchange pairs run overlapped (option "overlap"; counted in
+                                  passes and exchanges too) */
+    double overlap_ms;         /* event time of the overlapped pairs (timing=1; not in pass_ms/exchange_ms) */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);

@@ -45,7 +45,9 @@ class qsim_stats(ctypes.Structure):
                                                             ("jit_compile_ms", ctypes.c_double),
                                                             ("pass_fp64_slots", ctypes.c_double),
                                                             ("plan_cache_hits", ctypes.c_uint64),
-                                                            ("streamed_steps", ctypes.c_uint64)]
+                                                            ("streamed_steps", ctypes.c_uint64),
+                                                            ("overlapped", ctypes.c_uint64),
+                                                            ("overlap_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -93,6 +93,9 @@ struct qsim_ctx_s {
     int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
+    int overlap = 1;  // a pass followed by a top-bit exchange runs chunk by chunk under the exchange
+    cudaEvent_t ov_evs[64] = {};
+    int ov_next = 0;
     // stats
     qsim_stats stats{};
     std::vector<TimedRange> ranges;
@@ -323,6 +326,7 @@ static qsim_status collect_timing(qsim_ctx c)
         case 1: c->stats.generic_ms += ms; break;
         case 2: c->stats.perm_ms += ms; break;
         case 3: c->stats.exchange_ms += ms; break;
+        case 5: c->stats.overlap_ms += ms; break;
         default: c->stats.reduce_ms += ms; break;
         }
         c->event_pool.push_back(r.a);
@@ -716,6 +720,196 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     return QSIM_OK;
 }
 
+// One JIT pass launch over tile instances [inst0, inst0 + count) of local
+// shard i on `stream` (the companion per-thread phase-table kernel first
+// when with_tab).
+static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t inst0, uint64_t count, cudaStream_t stream,
+                                    bool with_tab, const int *fix_pos = nullptr, int K = 0, uint64_t fixbits = 0)
+{
+    PlanCache &pc = c->pc;
+    const Step &s = pc.steps[si];
+    CUfunction fn = jit_cache().find(pc.jkeys[si]);
+    int nts = 0;
+    CUfunction tabfn = jit_cache().find_tab(pc.jkeys[si], nts);
+    if (!fn) FAIL(c, QSIM_ERR_STATE, "jit pass kernel missing");
+    qsim_status st;
+    if (tabfn && (st = ensure_dev(c, c->d_ttab, c->d_ttab_cap, (size_t)nts * kPassThreads)) != QSIM_OK) return st;
+    const uint64_t rb = (uint64_t)local_ranks(c, i) << c->M;
+    auto &pp = pc.params[si];
+    if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
+    if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
+    if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
+    if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
+    jit_set_inst0(pp[i], inst0);  // the launch copies the parameter block
+    if (!jit_set_block(pp[i], s, fix_pos, K, fixbits)) FAIL(c, QSIM_ERR_STATE, "jit pass: too many fixed bits");
+    size_t sz = pp[i].size();
+    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
+    if (tabfn && with_tab) {  // the per-thread phase slots (the same for every shard and range)
+        CUresult ct = drv().launchKernel(tabfn, 1, 1, 1, kPassThreads, 1, 1, 0, (CUstream)stream, nullptr, extra);
+        if (ct != CUDA_SUCCESS) {
+            c->poisoned = true;
+            FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass table) failed: %d", (int)ct);
+        }
+        LAUNCHED(c);
+    }
+    unsigned grid, block, smem;
+    jit_launch_dims(s, c->n_sm, grid, block, smem);
+    grid = (unsigned)count;
+    CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)stream, nullptr, extra);
+    if (cr != CUDA_SUCCESS) {
+        c->poisoned = true;
+        FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
+    }
+    LAUNCHED(c);
+    return QSIM_OK;
+}
+
+static cudaEvent_t ov_event(qsim_ctx c)
+{
+    cudaEvent_t &e = c->ov_evs[c->ov_next];
+    c->ov_next = (c->ov_next + 1) % 64;
+    if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+}
+
+// Whether the pass at si and the exchange after it can run overlapped: the
+// exchange's local bits are not tile bits of the pass (so the pass's tiles
+// split into the exchange's 2^K blocks by those instance bits), K <= 3, JIT
+// tier, more than one shard.
+static bool overlap_ok(qsim_ctx c, size_t si)
+{
+    PlanCache &pc = c->pc;
+    if (!c->overlap || !c->jit || si + 1 >= pc.steps.size() || c->P < 2) return false;
+    if (c->transport != QSIM_TRANSPORT_VIRTUAL && !spmd(c)) return false;
+    const Step &p = pc.steps[si], &x = pc.steps[si + 1];
+    if (p.type != ST_PASS || x.type != ST_EXCHANGE || !jit_cache().find(pc.jkeys[si])) return false;
+    const int K = (int)x.lpos.size(), M = c->M;
+    if (K < 1 || K > 3 || M - kTileBits < K) return false;
+    for (int t = 0; t < kTileBits; t++)
+        for (int l : x.lpos)
+            if (p.pass.tp[t] == l || p.pass.tp_out[t] == l) return false;
+    return true;
+}
+
+// The pass at si and the K-pair exchange at si + 1, overlapped:
+// the pass runs block by block (the 2^K blocks of the exchange, as instance
+// ranges), each outgoing block's transfer starting on the transfer stream as
+// soon as its block is computed while the engine stream computes the next;
+// the block that stays is computed last, under the last transfers.  Rounds
+// follow the XOR schedule (round j: the peer whose sub-value is mine ^ j), so
+// every round pairs the ranks and no transfer waits on a cycle.
+static qsim_status exec_pass_exchange(qsim_ctx c, size_t si)
+{
+    PlanCache &pc = c->pc;
+    const Step &p = pc.steps[si], &x = pc.steps[si + 1];
+    const int K = (int)x.lpos.size(), M = c->M;
+    const uint64_t nval = 1ULL << K, chunk = 1ULL << (M - K);
+    const uint64_t n_inst = p.pass.n_inst, per = n_inst >> K;
+    // block v: the tiles whose local bits lpos[b] equal bit b of v
+    auto fix_of = [&](uint64_t v) {
+        uint64_t f = 0;
+        for (int b = 0; b < K; b++)
+            if ((v >> b) & 1) f |= 1ULL << x.lpos[b];
+        return f;
+    };
+    auto block = [&](int i, uint64_t v, bool tab) {
+        return launch_jit_range(c, si, i, 0, per, c->stream, tab, x.lpos.data(), K, fix_of(v));
+    };
+    qsim_status st;
+    if (!c->xstream) {  // created by pipeline() otherwise
+        CK(c, cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CK(c, cudaEventCreateWithFlags(&c->x_ready[i], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->x_done[i], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->x_used[i], cudaEventDisableTiming));
+        }
+    }
+    RangeGuard rg(c, 5, (uint64_t)n_local(c) * (32ULL << M));
+    c->stats.passes += n_local(c);
+    c->stats.jit_launches += n_local(c);
+    c->stats.exchanges++;
+    c->stats.overlapped++;  // (its time is overlap_ms, not pass_ms / exchange_ms)
+    bool tab_done = false;
+    // the transfer stream starts after everything before this step
+    cudaEvent_t e0 = ov_event(c);
+    CK(c, cudaEventRecord(e0, c->stream));
+    CK(c, cudaStreamWaitEvent(c->xstream, e0, 0));
+    if (c->transport == QSIM_TRANSPORT_VIRTUAL) {
+        // pairs of blocks (shard r, block v) <-> (shard peer, block my_r), by round
+        std::vector<char> done_blk((size_t)c->P * nval, 0);
+        for (uint64_t j = 1; j < nval; j++)
+            for (uint64_t r = 0; r < (uint64_t)c->P; r++) {
+                const uint64_t my = rank_sub(r, x.gpos, M), v = my ^ j, peer = with_sub(r, x.gpos, M, v);
+                if (peer < r) continue;
+                for (auto rb : {std::make_pair(r, v), std::make_pair(peer, my)}) {
+                    if (done_blk[rb.first * nval + rb.second]) continue;
+                    if ((st = block((int)rb.first, rb.second, !tab_done)) != QSIM_OK) return st;
+                    tab_done = true;
+                    done_blk[rb.first * nval + rb.second] = 1;
+                }
+                cudaEvent_t e = ov_event(c);
+                CK(c, cudaEventRecord(e, c->stream));
+                CK(c, cudaStreamWaitEvent(c->xstream, e, 0));
+                launch_swap_blocks(c->shards[r], c->shards[peer], M, K, x.lpos.data(), v, my, c->xstream);
+                LAUNCHED(c);
+            }
+        for (uint64_t r = 0; r < (uint64_t)c->P; r++) {
+            const uint64_t my = rank_sub(r, x.gpos, M);
+            if ((st = block((int)r, my, !tab_done)) != QSIM_OK) return st;
+            tab_done = true;
+        }
+        c->stats.exchange_bytes += (nval - 1) * chunk * 16;
+    } else {
+        const uint64_t my = rank_sub((uint64_t)c->rank, x.gpos, M);
+        bool contiguous = true;  // the blocks are contiguous when lpos are the top K bits
+        {
+            std::vector<int> l = x.lpos;
+            std::sort(l.begin(), l.end());
+            for (int i = 0; i < K; i++)
+                if (l[i] != M - K + i) contiguous = false;
+        }
+        const uint64_t scratch_amps = c->scratch_bytes / sizeof(double2), nbuf = contiguous ? 1 : 2;
+        const uint64_t limit_amps = (uint64_t)c->chunk_mb * (1ULL << 20) / sizeof(double2);
+        uint64_t piece = chunk;
+        while (piece > 1 && (nbuf * piece > scratch_amps || piece > limit_amps)) piece >>= 1;
+        if (nbuf * piece > scratch_amps) FAIL(c, QSIM_ERR_OOM, "scratch too small for exchange");
+        double2 *rbuf = c->scratch, *sbuf = c->scratch + piece;
+        for (uint64_t j = 1; j < nval; j++) {
+            const uint64_t v = my ^ j;
+            const int peer = (int)with_sub((uint64_t)c->rank, x.gpos, M, v);
+            if ((st = block(0, v, !tab_done)) != QSIM_OK) return st;
+            tab_done = true;
+            cudaEvent_t e = ov_event(c);
+            CK(c, cudaEventRecord(e, c->stream));
+            CK(c, cudaStreamWaitEvent(c->xstream, e, 0));
+            const uint64_t base = fix_of(v);
+            // block v goes to the peer, the peer's block `my` lands here, in
+            // pieces through the scratch, all on the transfer stream (a piece's
+            // send completes before its unpack overwrites it)
+            for (uint64_t k = 0; k < chunk / piece; k++) {
+                const double2 *src = c->shards[0] + base + k * piece;
+                if (!contiguous) {
+                    launch_pack(c->shards[0], sbuf, M, K, x.lpos.data(), v, k * piece, piece, 0, c->xstream);
+                    LAUNCHED(c);
+                    src = sbuf;
+                }
+                CKC(c, group_start(_err));
+                CKC(c, send(src, piece * sizeof(double2), peer, c->xstream, _err));
+                CKC(c, recv(rbuf, piece * sizeof(double2), peer, c->xstream, _err));
+                CKC(c, group_end(_err));
+                launch_pack(c->shards[0], rbuf, M, K, x.lpos.data(), v, k * piece, piece, 1, c->xstream);
+                LAUNCHED(c);
+            }
+        }
+        if ((st = block(0, my, !tab_done)) != QSIM_OK) return st;
+        c->stats.exchange_bytes += (nval - 1) * chunk * 16;
+    }
+    cudaEvent_t e1 = ov_event(c);
+    CK(c, cudaEventRecord(e1, c->xstream));
+    CK(c, cudaStreamWaitEvent(c->stream, e1, 0));
+    return QSIM_OK;
+}
+
 // Launch step si of the plan (its uploads done, its JIT kernel compiled).
 static qsim_status exec_step(qsim_ctx c, size_t si)
 {
@@ -727,45 +921,18 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
     case ST_PASS: {
         RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
         CUfunction fn = c->jit ? jit_cache().find(pc.jkeys[si]) : nullptr;
-        int nts = 0;
-        CUfunction tabfn = fn ? jit_cache().find_tab(pc.jkeys[si], nts) : nullptr;
-        if (tabfn && (st = ensure_dev(c, c->d_ttab, c->d_ttab_cap, (size_t)nts * kPassThreads)) != QSIM_OK) return st;
         for (int i = 0; i < n_local(c); i++) {
             const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
             if (fn) {
-                auto &pp = pc.params[si];
-                if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
-                if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
-                if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
-                if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
-                size_t sz = pp[i].size();
-                void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
-                                 CU_LAUNCH_PARAM_END};
-                if (tabfn && i == 0) {  // the per-thread phase slots (the same for every shard), once per step
-                    CUresult ct = drv().launchKernel(tabfn, 1, 1, 1, kPassThreads, 1, 1, 0, (CUstream)c->stream,
-                                                     nullptr, extra);
-                    if (ct != CUDA_SUCCESS) {
-                        c->poisoned = true;
-                        FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass table) failed: %d", (int)ct);
-                    }
-                    LAUNCHED(c);
-                }
-                unsigned grid, block, smem;
-                jit_launch_dims(s, c->n_sm, grid, block, smem);
-                CUresult cr = drv().launchKernel(fn, grid, 1, 1, block, 1, 1, smem, (CUstream)c->stream, nullptr,
-                                                 extra);
-                if (cr != CUDA_SUCCESS) {
-                    c->poisoned = true;
-                    FAIL(c, QSIM_ERR_CUDA, "cuLaunchKernel(jit pass) failed: %d", (int)cr);
-                }
+                if ((st = launch_jit_range(c, si, i, 0, s.pass.n_inst, c->stream, i == 0)) != QSIM_OK) return st;
                 c->stats.jit_launches++;
             } else {
                 PassDesc d = s.pass;
                 d.rank_bits = rb;
                 launch_pass(d, s.ops.data(), c->shards[i], c->pass_variant, c->stream,
                             s.ops.size() > (size_t)kMaxPassOps ? c->d_ops + s.t : nullptr);
+                LAUNCHED(c);
             }
-            LAUNCHED(c);
             c->stats.passes++;
             if (c->timing) {  // executed FP64-pipe instructions, pairs with pass_ms
                 const double fpt = fn ? jit_cache().fp64_per_thread(pc.jkeys[si]) : -1.0;
@@ -873,12 +1040,24 @@ static qsim_status flush(qsim_ctx c)
         }
         return QSIM_OK;
     };
-    auto launch_one = [&](size_t i) -> qsim_status {
+    // launch step i (and, for an overlapped pass + exchange, step i + 1 too:
+    // *used = steps consumed)
+    auto launch_one = [&](size_t i, size_t *used) -> qsim_status {
+        *used = 1;
         if (init_left && steps[i].type != ST_RELABEL) {
             if (steps[i].type == ST_PASS && steps[i].pass.fresh) init_left = false;
             else if (qsim_status e = launch_init_all()) return e;
         }
+        if (overlap_ok(c, i)) {
+            *used = 2;
+            return exec_pass_exchange(c, i);
+        }
         return exec_step(c, i);
+    };
+    // a pass whose successor is not planned yet waits for it when the state is
+    // sharded (it may be an exchange to overlap with)
+    auto wait_successor = [&](const std::vector<Step> &out, size_t i) {
+        return c->overlap && c->jit && c->P > 1 && out[i].type == ST_PASS && i + 1 == out.size();
     };
     size_t next = 0;  // first step not launched yet
     if (hit) {
@@ -909,13 +1088,16 @@ static qsim_status flush(qsim_ctx c)
         opt.sink = [&](std::vector<Step> &out) {
             if (!streaming || err != QSIM_OK) return;
             const auto tl = std::chrono::steady_clock::now();
-            for (; next < out.size(); next++) {
+            while (next < out.size()) {
                 mark_fresh(next);
                 std::string key;
                 if (!launchable_now(c, out[next], key)) { streaming = false; break; }
+                if (wait_successor(out, next)) break;  // streaming continues at the next emit
                 if (pc.jkeys.size() < out.size()) { pc.jkeys.resize(out.size()); pc.params.resize(out.size()); }
                 pc.jkeys[next] = key;
-                if ((err = launch_one(next)) != QSIM_OK) break;
+                size_t used = 1;
+                if ((err = launch_one(next, &used)) != QSIM_OK) break;
+                next += used;
             }
             launch_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
         };
@@ -953,8 +1135,8 @@ static qsim_status flush(qsim_ctx c)
         for (size_t i = next; i < steps.size(); i++)
             if (steps[i].type == ST_PASS) pc.jkeys[i] = jit_key(steps[i]);
     }
-    for (size_t i = next; i < steps.size(); i++)
-        if ((st = launch_one(i)) != QSIM_OK) return st;
+    for (size_t i = next, used = 1; i < steps.size(); i += used)
+        if ((st = launch_one(i, &used)) != QSIM_OK) return st;
     return init_left ? launch_init_all() : QSIM_OK;
 }
 
@@ -1589,6 +1771,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else if (k == "overlap") c->overlap = value != 0;
     else if (k == "comm_timeout_ms") {
         c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
         if (c->comm) c->comm->timeout_ms = c->comm_timeout_ms;

@@ -139,3 +139,28 @@ def test_loopback_timeout_on_spmd_mismatch(P):
 
     res = P.run_loopback(n, 2, body)
     assert res == ["QSIM_ERR_COMM", "ok"]
+
+
+@pytest.mark.parametrize("n,ranks", [(22, 2), (22, 4), (18, 8)])
+def test_overlapped_pass_exchange(P, oracle_mod, n, ranks):
+    """A pass followed by an exchange whose local bits are not tile bits of
+    the pass runs block by block with each block's transfer overlapping the
+    next block's compute (option "overlap"): identical amplitudes with the
+    overlap on and off, on the loopback (NCCL-branch) and virtual transports,
+    and equal to the oracle (config-5 family circuits where it applies)."""
+    gates = C.random_chain(n, 6, seed=15, sweep=True)
+    ref = oracle_run(oracle_mod, n, 0, gates).amplitudes()
+    out = {}
+    for ov in (1, 0):
+        res = spmd_run(P, n, ranks, 0, gates, {"overlap": ov}, scratch_bytes=1 << 16)
+        out[ov] = res
+        for amp, st, _ in res:
+            assert np.max(np.abs(amp - ref)) <= TOL
+            assert (st["overlapped"] >= 1) == bool(ov)
+    assert np.array_equal(out[0][0][0], out[1][0][0])
+    sim = P.QSim(n, n_ranks=ranks, transport="virtual")
+    sim.init_basis(0)
+    sim.run_circuit(gates)
+    got = sim.get_amplitudes()
+    assert sim.stats()["overlapped"] >= 1
+    assert np.array_equal(got, out[1][0][0])
