@@ -230,9 +230,11 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb"
  * (exchange piece cap; the pieces are double-buffered between the engine
  * stream and a transfer stream), "comm_timeout_ms", "jit", "plan_cache",
- * "pass_variant", "global_policy", "overlap" (1 = a pass followed by an
- * exchange of the top local bits runs block by block with each block's
- * transfer overlapping the next block's compute [default]; 0 = in sequence). */
+ * "pass_variant", "global_policy", "overlap" (a pass followed by an
+ * exchange whose local bits are not tile bits of the pass runs block by block,
+ * each block's transfer overlapping the next block's compute: 1 = on the
+ * NCCL / loopback transports [default]; 2 = also on virtual shards, where the
+ * transfer is device copy work on the same HBM; 0 = in sequence). */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {

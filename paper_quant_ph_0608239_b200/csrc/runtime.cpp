@@ -93,7 +93,7 @@ struct qsim_ctx_s {
     int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
-    int overlap = 1;  // a pass followed by a top-bit exchange runs chunk by chunk under the exchange
+    int overlap = 1;  // pass + exchange overlap: 1 = SPMD transports, 2 = also virtual shards, 0 = off
     cudaEvent_t ov_evs[64] = {};
     int ov_next = 0;
     // stats
@@ -780,7 +780,9 @@ static bool overlap_ok(qsim_ctx c, size_t si)
 {
     PlanCache &pc = c->pc;
     if (!c->overlap || !c->jit || si + 1 >= pc.steps.size() || c->P < 2) return false;
-    if (c->transport != QSIM_TRANSPORT_VIRTUAL && !spmd(c)) return false;
+    // virtual shards share one GPU's HBM: their "transfer" is copy work the
+    // pass competes with, so the overlap there only on request (overlap = 2)
+    if (c->transport == QSIM_TRANSPORT_VIRTUAL ? c->overlap < 2 : !spmd(c)) return false;
     const Step &p = pc.steps[si], &x = pc.steps[si + 1];
     if (p.type != ST_PASS || x.type != ST_EXCHANGE || !jit_cache().find(pc.jkeys[si])) return false;
     const int K = (int)x.lpos.size(), M = c->M;
@@ -1771,7 +1773,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
-    else if (k == "overlap") c->overlap = value != 0;
+    else if (k == "overlap") c->overlap = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 2);
     else if (k == "comm_timeout_ms") {
         c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
         if (c->comm) c->comm->timeout_ms = c->comm_timeout_ms;

@@ -159,6 +159,7 @@ def test_overlapped_pass_exchange(P, oracle_mod, n, ranks):
             assert (st["overlapped"] >= 1) == bool(ov)
     assert np.array_equal(out[0][0][0], out[1][0][0])
     sim = P.QSim(n, n_ranks=ranks, transport="virtual")
+    sim.set_option("overlap", 2)  # virtual shards overlap only on request
     sim.init_basis(0)
     sim.run_circuit(gates)
     got = sim.get_amplitudes()
