@@ -36,8 +36,11 @@ int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 // parameter block layout (the JP struct of the generated source)
 constexpr int kMaxFix = 4;  // instance bits a launch may fix (jit_set_block)
 constexpr size_t kOffInit = 32, kOffTtab = 40, kOffFix = 48, kOffTpm = 56, kOffTs = kOffTpm + 8 * kTileBits;
-constexpr size_t kOffTpo = (kOffTs + 4 * (kTileBits + kMaxFix) + 7) / 8 * 8;  // natural u64 alignment
+// 16-B aligned (the matrix rows that follow are read as 128-bit constants)
+constexpr size_t kOffTpo = (kOffTs + 4 * (kTileBits + kMaxFix) + 15) / 16 * 16;
+constexpr int kTsPad = (int)(kOffTpo - kOffTs) / 4 - (kTileBits + kMaxFix);  // ints of padding after ts
 
+static_assert((kOffTpo + 8 * kTileBits) % 16 == 0, "matrix rows must be 16-B aligned");
 struct Layout {
     int n_out = 0, n_m = 0;
     size_t off_out = kOffTpo + 8 * kTileBits, off_m = 0, bytes = 0;
@@ -154,16 +157,22 @@ JitPass jit_generate(const Step &st)
     const int kQexpOps = 13;
     const int minb = env_int("QSIM_JIT_MINB", kPassMinBlocks);  // CTAs per SM (register cap)
     s << "// minb=" << minb << "\n";
-    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long inst0; "
+    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long unused; "
          "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long fixbits; "
-         "unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits + kMaxFix
-      << "]; unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
+         "unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits + kMaxFix << "]; "
+      << (kTsPad ? "int ts_pad[" + std::to_string(kTsPad) + "]; " : std::string())
+      << "unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
-    // instance -> physical base: zeros inserted at the tile positions and at
-    // the positions a launch fixes (ts sorted ascending, 64 = unused)
+    // instance -> physical base: zeros inserted at the tile positions (ts
+    // sorted ascending).  The block variant (Step::jit_block) also inserts
+    // them at the positions a launch fixes and ORs in their values (unused
+    // entries are 62: a no-op insertion for any b < 2^62).  Only that
+    // variant pays for the longer chain: the 16-entry form in every pass
+    // raised the kernels' uniform-register traffic several-fold.
+    const int n_ins = st.jit_block ? kTileBits + kMaxFix : kTileBits;
     s << "__device__ __forceinline__ unsigned long long qdep(unsigned long long b, const int *ts)\n{\n"
-         "#pragma unroll\n for (int j = 0; j < " << kTileBits + kMaxFix << "; j++) { const int t = ts[j]; "
-         "if (t < 64) b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
+         "#pragma unroll\n for (int j = 0; j < " << n_ins << "; j++) { const int t = ts[j]; "
+         "b = ((b >> t) << (t + 1)) | (b & ((1ULL << t) - 1)); }\n return b;\n}\n";
     // e^{2 pi i t / 2^64}: table of the top 8 bits x Taylor series of the rest (|x| < 2pi/256)
     // e^{2 pi i t / 2^64}: the nearest table angle k/256 times e^{i x}, |x| <=
     // pi/256, by Taylor to x^6 (cos) and x^5 (sin): truncation < 1e-17
@@ -182,8 +191,8 @@ JitPass jit_generate(const Step &st)
       << ") qsim_pass(const __grid_constant__ JP P)\n{\n";
     s << " extern __shared__ double2 sm[];\n";
     s << " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    s << " { const unsigned long long inst = P.inst0 + blockIdx.x;  // instance range [inst0, inst0 + grid)\n";
-    s << " const unsigned long long base = qdep(inst, TSP) | P.fixbits;\n";
+    s << " { const unsigned long long inst = blockIdx.x;\n";
+    s << " const unsigned long long base = qdep(inst, TSP)" << (st.jit_block ? " | P.fixbits" : "") << ";\n";
     s << " const unsigned long long gcta = P.rank_bits | base;\n";
     s << " double2 a0";
     for (int i = 1; i < kAmpsPerThread; i++) s << ", a" << i;
@@ -787,13 +796,13 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     uint8_t *b = buf.data();
     std::memcpy(b + 0, &state, 8);
     std::memcpy(b + 8, &rank_bits, 8);
-    const uint64_t inst0 = 0;  // first instance (jit_set_inst0)
-    std::memcpy(b + 16, &inst0, 8);
+    const uint64_t unused = 0;
+    std::memcpy(b + 16, &unused, 8);
     const void *tab = jit_phase_table();
     std::memcpy(b + 24, &tab, 8);
     std::memcpy(b + kOffInit, &st.pass.init_phys, 8);
     for (int t = kTileBits; t < kTileBits + kMaxFix; t++) {
-        const int32_t none = 64;
+        const int32_t none = 62;  // no-op insertion (see qdep)
         std::memcpy(b + kOffTs + 4 * t, &none, 4);
     }
     for (int t = 0; t < kTileBits; t++) {
@@ -831,18 +840,13 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     }
 }
 
-void jit_set_inst0(std::vector<uint8_t> &buf, uint64_t inst0)
-{
-    if (buf.size() >= 24) std::memcpy(buf.data() + 16, &inst0, 8);
-}
-
 bool jit_set_block(std::vector<uint8_t> &buf, const Step &st, const int *pos, int K, uint64_t fixbits)
 {
     if (K > kMaxFix || buf.size() < kOffTpo) return false;
     std::vector<int32_t> ts(st.pass.tile_sorted, st.pass.tile_sorted + kTileBits);
     ts.insert(ts.end(), pos, pos + K);
     std::sort(ts.begin(), ts.end());
-    ts.resize(kTileBits + kMaxFix, 64);
+    ts.resize(kTileBits + kMaxFix, 62);
     std::memcpy(buf.data() + kOffTs, ts.data(), 4 * ts.size());
     std::memcpy(buf.data() + kOffFix, &fixbits, 8);
     return true;
@@ -1035,7 +1039,7 @@ std::string jit_key(const Step &st)
     std::string k;
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
     put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) |
-        ((uint64_t)(st.pass.fresh != 0) << 48) |
+        ((uint64_t)(st.pass.fresh != 0) << 48) | ((uint64_t)(st.jit_block != 0) << 49) |
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
     {

@@ -48,11 +48,10 @@ JitPass jit_generate(const Step &st);
 void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vector<uint8_t> &buf);
 // update the basis-state index a fresh pass (PassDesc::fresh) synthesises
 void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys);
-// first tile instance of a launch (a launch of g CTAs covers instances [inst0, inst0 + g))
-void jit_set_inst0(std::vector<uint8_t> &buf, uint64_t inst0);
-// restrict a launch to the tiles whose physical bits pos[0..K) are fixed to
-// those of fixbits (the instance index then enumerates the other non-tile
-// bits; 2^(M - 12 - K) instances); K = 0 undoes it.  false if K is too large.
+// Block variant (Step::jit_block): restrict a launch to the tiles whose
+// physical bits pos[0..K) equal those of fixbits (the instance index then
+// enumerates the other non-tile bits; 2^(M - 12 - K) instances); K = 0
+// undoes it.  false if K is too large.
 bool jit_set_block(std::vector<uint8_t> &buf, const Step &st, const int *pos, int K, uint64_t fixbits);
 // device table (n_tslots x kPassThreads uint64) qsim_pass_tab writes and the pass reads
 void jit_set_ttab(std::vector<uint8_t> &buf, void *ttab);

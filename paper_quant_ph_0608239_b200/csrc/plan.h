@@ -76,6 +76,10 @@ struct Step {
     std::vector<int> lpos, gpos;
     // ST_RELABEL: swap physical roles of logical qubits a,b (no data)
     int ra = -1, rb = -1;
+    // ST_PASS, JIT tier: 1 = the block variant of the kernel (its launches
+    // cover the tiles whose fixed local bits equal the launch's fixbits,
+    // jit_set_block; the overlapped pass + exchange)
+    int jit_block = 0;
 };
 
 struct PlanOptions {

@@ -720,15 +720,17 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     return QSIM_OK;
 }
 
-// One JIT pass launch over tile instances [inst0, inst0 + count) of local
-// shard i on `stream` (the companion per-thread phase-table kernel first
-// when with_tab).
-static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t inst0, uint64_t count, cudaStream_t stream,
-                                    bool with_tab, const int *fix_pos = nullptr, int K = 0, uint64_t fixbits = 0)
+// One JIT pass launch of `count` tile instances of local shard i on
+// `stream` (the companion per-thread phase-table kernel first when
+// with_tab).  fn: the kernel (nullptr: the pass's own); K > 0: the block
+// variant's launch over the tiles whose local bits fix_pos equal fixbits'.
+static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t count, cudaStream_t stream, bool with_tab,
+                                    CUfunction fn = nullptr, const int *fix_pos = nullptr, int K = 0,
+                                    uint64_t fixbits = 0)
 {
     PlanCache &pc = c->pc;
     const Step &s = pc.steps[si];
-    CUfunction fn = jit_cache().find(pc.jkeys[si]);
+    if (!fn) fn = jit_cache().find(pc.jkeys[si]);
     int nts = 0;
     CUfunction tabfn = jit_cache().find_tab(pc.jkeys[si], nts);
     if (!fn) FAIL(c, QSIM_ERR_STATE, "jit pass kernel missing");
@@ -740,7 +742,7 @@ static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t inst0
     if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
     if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
     if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
-    jit_set_inst0(pp[i], inst0);  // the launch copies the parameter block
+    // (the launch copies the parameter block)
     if (!jit_set_block(pp[i], s, fix_pos, K, fixbits)) FAIL(c, QSIM_ERR_STATE, "jit pass: too many fixed bits");
     size_t sz = pp[i].size();
     void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, pp[i].data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
@@ -814,8 +816,19 @@ static qsim_status exec_pass_exchange(qsim_ctx c, size_t si)
             if ((v >> b) & 1) f |= 1ULL << x.lpos[b];
         return f;
     };
+    // the block variant of the pass kernel (compiled here on first use; cached
+    // in memory and on disk like every pass kernel)
+    Step bv = p;
+    bv.jit_block = 1;
+    const std::string bkey = jit_key(bv);
+    CUfunction bfn = jit_cache().find(bkey);
+    if (!bfn) {
+        std::string jerr;
+        if (!jit_cache().compile({&bv}, jerr)) FAIL(c, QSIM_ERR_CUDA, "jit block variant: %s", jerr.substr(0, 300).c_str());
+        bfn = jit_cache().find(bkey);
+    }
     auto block = [&](int i, uint64_t v, bool tab) {
-        return launch_jit_range(c, si, i, 0, per, c->stream, tab, x.lpos.data(), K, fix_of(v));
+        return launch_jit_range(c, si, i, per, c->stream, tab, bfn, x.lpos.data(), K, fix_of(v));
     };
     qsim_status st;
     if (!c->xstream) {  // created by pipeline() otherwise
@@ -926,7 +939,7 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
         for (int i = 0; i < n_local(c); i++) {
             const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
             if (fn) {
-                if ((st = launch_jit_range(c, si, i, 0, s.pass.n_inst, c->stream, i == 0)) != QSIM_OK) return st;
+                if ((st = launch_jit_range(c, si, i, s.pass.n_inst, c->stream, i == 0)) != QSIM_OK) return st;
                 c->stats.jit_launches++;
             } else {
                 PassDesc d = s.pass;
