@@ -230,7 +230,9 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb"
  * (exchange piece cap; the pieces are double-buffered between the engine
  * stream and a transfer stream), "comm_timeout_ms", "jit", "plan_cache",
- * "pass_variant", "global_policy", "overlap" (a pass followed by an
+ * "pass_variant", "global_policy", "peak_link_gbs" (link GB/s per direction
+ * for the sharded planner's device-time model; its FP64 and HBM rates are
+ * measured once per process on the device, qsim_probe_peaks), "overlap" (a pass followed by an
  * exchange whose local bits are not tile bits of the pass runs block by block,
  * each block's transfer overlapping the next block's compute: 1 = on the
  * NCCL / loopback transports [default]; 2 = also on virtual shards, where the
@@ -272,7 +274,7 @@ qsim_status qsim_reset_stats(qsim_ctx ctx);
  * needed; takes ~0.1 s): *fp64_tflops = FP64 FMA-pipe throughput of a DFMA
  * probe (8 independent chains per thread, 2 x 256-thread CTAs per SM, the
  * pass kernel's residency), in TFLOP/s (2 flop per FMA); *copy_gbs =
- * streaming copy of 2 GiB (read + write bytes) in GB/s.  Either pointer may
+ * streaming copy of 1 GiB (read + write bytes) in GB/s.  Either pointer may
  * be NULL (that probe is skipped).  QSIM_ERR_CUDA if no device. */
 qsim_status qsim_probe_peaks(double *fp64_tflops, double *copy_gbs);
 

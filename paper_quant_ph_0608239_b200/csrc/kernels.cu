@@ -1322,7 +1322,7 @@ int probe_peaks(double *fp64_flops, double *copy_bytes_per_s, int reps)
         *fp64_flops = 2.0 * (double)blocks * 256 * iters * 16 * 8 / (best * 1e-3);
     }
     if (!rc && copy_bytes_per_s) {
-        const size_t bytes = (size_t)2 << 30;
+        const size_t bytes = (size_t)1 << 30;
         double4 *a = nullptr, *b = nullptr;
         if (cudaMalloc(&a, bytes) != cudaSuccess || cudaMalloc(&b, bytes) != cudaSuccess) {
             rc = -1;

@@ -1086,12 +1086,12 @@ void Planner::remap(const std::vector<int> &local_q, const std::vector<int> &glo
 
 // Modelled device time of a planned step list (seconds): a pass costs
 // max(FP64 FMA-slot work / FP64 peak, 32 B/amp / HBM peak), a K-pair exchange
-// its (2^K-1)/2^K shard share over NVLink plus the HBM pack/unpack, other
-// steps one HBM round trip.  Peaks: derived FP64, measured
-// HBM copy and NVLink peer-copy bandwidths (B200_PROFILING.md).
-double plan_cost(const std::vector<Step> &steps, int M)
+// its (2^K-1)/2^K shard share over the link plus the HBM pack/unpack, other
+// steps one HBM round trip.  Peaks from PlanOptions: the runtime measures
+// FP64 and HBM on its device (qsim_probe_peaks); the link rate is an option.
+double plan_cost(const std::vector<Step> &steps, int M, const PlanOptions &opt)
 {
-    const double amps = std::ldexp(1.0, M), fp64 = 37.2e12, hbm = 6.5e12, nvl = 0.77e12;
+    const double amps = std::ldexp(1.0, M), fp64 = opt.peak_fp64, hbm = opt.peak_hbm, nvl = opt.peak_link;
     double t = 0;
     for (const Step &s : steps) {
         switch (s.type) {
@@ -1168,7 +1168,7 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
         *this = start;
         std::vector<Step> cand;
         plan_list(lists[i], o2, cand);
-        const double cost = plan_cost(cand, M);
+        const double cost = plan_cost(cand, M, opt);
         if (i == 0 || cost < best_cost) {
             best_cost = cost;
             best.swap(cand);

@@ -89,6 +89,11 @@ struct PlanOptions {
     int remap_lookahead = 6;   // candidates searched for those three (<= 3: the first three needed)
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
+    // device-time model inputs (plan_cost): FP64 FMA-pipe flop/s, HBM bytes/s,
+    // link bytes/s per direction.  The runtime fills FP64 and HBM from the
+    // measured probe of its device (qsim_probe_peaks) and the link from the
+    // option "peak_link_gbs"; the defaults are the nominal fallbacks.
+    double peak_fp64 = 37.2e12, peak_hbm = 6.5e12, peak_link = 0.77e12;
     // called with the step list each time the planner has appended finished
     // steps (earlier steps never change again): the runtime launches them
     // while planning continues
@@ -128,7 +133,7 @@ private:
 };
 
 // modelled device seconds of a step list on 2^M-amplitude shards (planner choices)
-double plan_cost(const std::vector<Step> &steps, int M);
+double plan_cost(const std::vector<Step> &steps, int M, const PlanOptions &opt = PlanOptions());
 
 std::string plan_to_json(const Planner &final_state, const std::vector<Step> &steps);
 

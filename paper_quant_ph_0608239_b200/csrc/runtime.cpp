@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -93,6 +94,7 @@ struct qsim_ctx_s {
     int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
+    double peak_link_gbs = 0;  // planner link rate per direction (option peak_link_gbs; 0 = nominal)
     int overlap = 1;  // pass + exchange overlap: 1 = SPMD transports, 2 = also virtual shards, 0 = off
     cudaEvent_t ov_evs[64] = {};
     int ov_next = 0;
@@ -1001,6 +1003,20 @@ static bool launchable_now(qsim_ctx c, const Step &s, std::string &key)
     return jit_cache().find(key) != nullptr;
 }
 
+// FP64 and HBM peaks of this process's device, measured once (DFMA probe and
+// streaming copy, ~0.1 s) for the planner's device-time model; 0 if the probe fails
+static void measured_peaks(double &fp64, double &hbm)
+{
+    static double f = -1, b = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (f < 0) {
+        if (probe_peaks(&f, &b, 2) != 0) f = b = 0;
+    }
+    fp64 = f;
+    hbm = b;
+}
+
 static qsim_status flush(qsim_ctx c)
 {
     if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
@@ -1100,6 +1116,13 @@ static qsim_status flush(qsim_ctx c)
         opt.remap_lookahead = c->remap_lookahead;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
+        if (c->P > 1) {  // the sharded planner weighs alternatives by modelled device time
+            double f = 0, b = 0;
+            measured_peaks(f, b);
+            if (f > 0) opt.peak_fp64 = f;
+            if (b > 0) opt.peak_hbm = b;
+            if (c->peak_link_gbs > 0) opt.peak_link = c->peak_link_gbs * 1e9;
+        }
         opt.sink = [&](std::vector<Step> &out) {
             if (!streaming || err != QSIM_OK) return;
             const auto tl = std::chrono::steady_clock::now();
@@ -1786,6 +1809,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else if (k == "peak_link_gbs") c->peak_link_gbs = (double)std::max<int64_t>(value, 0);
     else if (k == "overlap") c->overlap = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 2);
     else if (k == "comm_timeout_ms") {
         c->comm_timeout_ms = value < 1 ? 1.0 : (double)value;
