@@ -290,7 +290,10 @@ const char *qsim_last_error(qsim_ctx ctx);
  * remap; bit 10 = generate the pass kernels' sources and check that equal
  * kernel-cache keys mean equal sources (no compile; across every plan checked
  * in this process; reported under "jit"); bits 12-16 = remap look-ahead + 1
- * (0 = default 6).  Returns
+ * (0 = default 6); bits 17-19 = candidate gate list + 1 to plan alone
+ * (0 = all, costed; each candidate's modelled time is reported under
+ * "candidates"); bit 20 = cost the plan for a transport that overlaps a pass
+ * with the exchange after it (the runtime's "overlap" on NCCL/loopback).  Returns
  * QSIM_ERR_ARG if buf is too small. */
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
                            int flags, char *buf, size_t buf_bytes);

@@ -1092,8 +1092,11 @@ void Planner::remap(const std::vector<int> &local_q, const std::vector<int> &glo
 double plan_cost(const std::vector<Step> &steps, int M, const PlanOptions &opt)
 {
     const double amps = std::ldexp(1.0, M), fp64 = opt.peak_fp64, hbm = opt.peak_hbm, nvl = opt.peak_link;
-    double t = 0;
+    double t = 0, t_prev_pass = 0;
+    const Step *prev = nullptr;
     for (const Step &s : steps) {
+        const Step *before = prev;
+        prev = &s;
         switch (s.type) {
         case ST_PASS: {
             double f = 0;
@@ -1104,12 +1107,20 @@ double plan_cost(const std::vector<Step> &steps, int M, const PlanOptions &opt)
                                : (op.code == OPC_U2R || op.code == OPC_PHASE || op.code == OPC_PHASE_ACC) ? 4 : 0;
                 f += c * std::ldexp(1.0, -pb);
             }
-            t += std::max(2 * f * amps / fp64, 32 * amps / hbm);
+            t_prev_pass = std::max(2 * f * amps / fp64, 32 * amps / hbm);
+            t += t_prev_pass;
             break;
         }
         case ST_EXCHANGE: {
-            const double share = 1.0 - std::ldexp(1.0, -(int)s.lpos.size());
-            t += share * 16 * amps / nvl + 2 * share * 16 * amps / hbm;
+            const int K = (int)s.lpos.size();
+            const double share = 1.0 - std::ldexp(1.0, -K);
+            const double tx = share * 16 * amps / nvl + 2 * share * 16 * amps / hbm;
+            bool ov = opt.overlap && before && before->type == ST_PASS && K >= 1 && K <= 3;
+            for (int i = 0; ov && i < kTileBits; i++)
+                for (int l : s.lpos)
+                    if (before->pass.tp[i] == l || before->pass.tp_out[i] == l) ov = false;
+            // overlapped: the pair costs max(pass, exchange) + one block of the pass
+            t += ov ? std::max(0.0, tx - t_prev_pass) + t_prev_pass * std::ldexp(1.0, -K) : tx;
             break;
         }
         case ST_PAIRWISE: t += 16 * amps / nvl + 48 * amps / hbm; break;
@@ -1154,6 +1165,10 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
     // nonlocal qubit (more exchanges): the unblocked list (build_pass still
     // fuses inside each pass) is a candidate too.
     if (G > 0) lists.push_back(user_gates);
+    if (opt.force_list >= 0 && opt.force_list < (int)lists.size()) {
+        std::vector<GateRec> keep = lists[opt.force_list];
+        lists.assign(1, keep);
+    }
     if (lists.size() == 1) {
         plan_list(lists[0], opt, out);  // streams its steps (opt.sink)
         return;
@@ -1169,6 +1184,12 @@ void Planner::plan(const std::vector<GateRec> &user_gates, const PlanOptions &op
         std::vector<Step> cand;
         plan_list(lists[i], o2, cand);
         const double cost = plan_cost(cand, M, opt);
+        if (opt.cand_report) {
+            int np = 0, nx = 0;
+            for (const Step &st : cand) { np += st.type == ST_PASS; nx += st.type == ST_EXCHANGE || st.type == ST_PAIRWISE; }
+            opt.cand_report->push_back("{\"list\":" + std::to_string(i) + ",\"model_s\":" + std::to_string(cost) +
+                                       ",\"passes\":" + std::to_string(np) + ",\"exchanges\":" + std::to_string(nx) + "}");
+        }
         if (i == 0 || cost < best_cost) {
             best_cost = cost;
             best.swap(cand);

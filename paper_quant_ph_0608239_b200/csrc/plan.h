@@ -89,11 +89,24 @@ struct PlanOptions {
     int remap_lookahead = 6;   // candidates searched for those three (<= 3: the first three needed)
     int max_scan = 1 << 30;   // look-ahead window (gates) per pass
     int global_policy = GP_AUTO;
-    // device-time model inputs (plan_cost): FP64 FMA-pipe flop/s, HBM bytes/s,
-    // link bytes/s per direction.  The runtime fills FP64 and HBM from the
-    // measured probe of its device (qsim_probe_peaks) and the link from the
-    // option "peak_link_gbs"; the defaults are the nominal fallbacks.
-    double peak_fp64 = 37.2e12, peak_hbm = 6.5e12, peak_link = 0.77e12;
+    // device-time model inputs (plan_cost): the FP64-pipe flop/s and HBM
+    // bytes/s the fused passes ACHIEVE, link bytes/s per direction.  The
+    // runtime fills FP64 and HBM from the probe of its device
+    // (qsim_probe_peaks) times the fractions the passes reach (kPassFp64Eff,
+    // kPassHbmEff, measured round 2: 0.66-0.68 of the DFMA peak on
+    // block-heavy passes, 0.73-0.86 of HBM on streaming ones) and the link
+    // from the option "peak_link_gbs"; the defaults are those fractions of
+    // the B200 peaks (34.2 TFLOP/s DFMA probe, 6.55 TB/s copy).
+    static constexpr double kPassFp64Eff = 0.68, kPassHbmEff = 0.8;
+    double peak_fp64 = kPassFp64Eff * 34.2e12, peak_hbm = kPassHbmEff * 6.55e12, peak_link = 0.77e12;
+    // introspection (qsim_plan_json): plan only candidate list i (>= 0), and
+    // report each candidate's modelled time and step counts
+    int force_list = -1;
+    // the runtime overlaps a pass with the exchange after it (runtime option
+    // overlap on this transport): plan_cost models such a pair as
+    // max(pass, exchange) + one block of the pass
+    bool overlap = false;
+    std::vector<std::string> *cand_report = nullptr;
     // called with the step list each time the planner has appended finished
     // steps (earlier steps never change again): the runtime launches them
     // while planning continues

@@ -1116,11 +1116,13 @@ static qsim_status flush(qsim_ctx c)
         opt.remap_lookahead = c->remap_lookahead;
         opt.max_scan = c->max_scan;
         opt.global_policy = c->global_policy;
+        opt.overlap = c->jit && c->P > 1 &&
+                      (c->transport == QSIM_TRANSPORT_VIRTUAL ? c->overlap >= 2 : spmd(c) && c->overlap >= 1);
         if (c->P > 1) {  // the sharded planner weighs alternatives by modelled device time
             double f = 0, b = 0;
             measured_peaks(f, b);
-            if (f > 0) opt.peak_fp64 = f;
-            if (b > 0) opt.peak_hbm = b;
+            if (f > 0) opt.peak_fp64 = PlanOptions::kPassFp64Eff * f;
+            if (b > 0) opt.peak_hbm = PlanOptions::kPassHbmEff * b;
             if (c->peak_link_gbs > 0) opt.peak_link = c->peak_link_gbs * 1e9;
         }
         opt.sink = [&](std::vector<Step> &out) {
@@ -1896,6 +1898,10 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
     opt.low_remap = !(fusion & 0x200);
     if ((fusion >> 12) & 31) opt.remap_lookahead = ((fusion >> 12) & 31) - 1;
     opt.global_policy = (fusion >> 4) & 3 ? ((fusion >> 4) & 3) - 1 : GP_AUTO;
+    if ((fusion >> 17) & 7) opt.force_list = ((fusion >> 17) & 7) - 1;
+    opt.overlap = (fusion >> 20) & 1;
+    std::vector<std::string> cands;
+    opt.cand_report = &cands;
     const auto tp0 = std::chrono::steady_clock::now();
     P.plan(recs, opt, steps);
     const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
@@ -1916,7 +1922,10 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
         jit_info = ",\"jit\":{\"ok\":" + std::string(ok ? "true" : "false") + ",\"kernels\":" + std::to_string(nk) +
                    ",\"compile_ms\":" + std::to_string(ms) + ",\"fp64_per_amp\":[" + fps + "],\"error\":\"" + e + "\"}";
     }
-    std::string js = init + plan_to_json(P, steps) + jit_info + ",\"plan_ms\":" + std::to_string(plan_ms) + "}";
+    std::string cj;
+    for (size_t i = 0; i < cands.size(); i++) cj += (i ? "," : "") + cands[i];
+    std::string js = init + plan_to_json(P, steps) + jit_info + ",\"plan_ms\":" + std::to_string(plan_ms) +
+                     ",\"candidates\":[" + cj + "]}";
     if (js.size() + 1 > buf_bytes) return QSIM_ERR_ARG;
     std::memcpy(buf, js.c_str(), js.size() + 1);
     return QSIM_OK;
