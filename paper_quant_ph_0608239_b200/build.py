@@ -12,8 +12,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libqsim_b200.so")
+# QSB_BUILD_TAG=<t>: an experiment build (e.g. QSB_TILE_BITS=13) into
+# _build_<t>/ and libqsim_b200_<t>.so, loaded with QSIM_LIB=<that path>
+_TAG = os.environ.get("QSB_BUILD_TAG", "")
+BUILD = os.path.join(HERE, "_build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(HERE, "libqsim_b200" + ("_" + _TAG if _TAG else "") + ".so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -40,10 +40,11 @@ constexpr size_t kOffInit = 32, kOffTtab = 40, kOffFix = 48, kOffTpm = 56, kOffT
 constexpr size_t kOffTpo = (kOffTs + 4 * (kTileBits + kMaxFix) + 15) / 16 * 16;
 constexpr int kTsPad = (int)(kOffTpo - kOffTs) / 4 - (kTileBits + kMaxFix);  // ints of padding after ts
 
-static_assert((kOffTpo + 8 * kTileBits) % 16 == 0, "matrix rows must be 16-B aligned");
+constexpr size_t kOffOut = (kOffTpo + 8 * kTileBits + 15) / 16 * 16;  // the matrix rows after out[] stay 16-B aligned
+constexpr int kTpoPad = (int)(kOffOut - kOffTpo) / 8 - kTileBits;     // u64s of padding after tpo
 struct Layout {
     int n_out = 0, n_m = 0;
-    size_t off_out = kOffTpo + 8 * kTileBits, off_m = 0, bytes = 0;
+    size_t off_out = kOffOut, off_m = 0, bytes = 0;
 };
 
 // generator variant (env, for A/B experiments): minimum CTAs per SM.  A
@@ -161,7 +162,9 @@ JitPass jit_generate(const Step &st)
          "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long fixbits; "
          "unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits + kMaxFix << "]; "
       << (kTsPad ? "int ts_pad[" + std::to_string(kTsPad) + "]; " : std::string())
-      << "unsigned long long tpo[" << kTileBits << "]; unsigned long long out["
+      << "unsigned long long tpo[" << kTileBits << "]; "
+      << (kTpoPad ? "unsigned long long tpo_pad[" + std::to_string(kTpoPad) + "]; " : std::string())
+      << "unsigned long long out["
       << std::max(1, L.n_out) << "][2]; double m[" << std::max(1, L.n_m) << "][8]; };\n";
     // instance -> physical base: zeros inserted at the tile positions (ts
     // sorted ascending).  The block variant (Step::jit_block) also inserts
@@ -222,7 +225,7 @@ JitPass jit_generate(const Step &st)
         for (int j = 0; j < kWarpBits; j++) s << "(((warp >> " << j << ") & 1) << " << nib(c, kWarpNib + j) << ") | ";
         s << "0;\n";
         s << "  const int zz" << tag << " = zt" << tag << " ^ (((zt" << tag << " >> 3) ^ (zt" << tag << " >> 6) ^ (zt"
-          << tag << " >> 9)) & 7);\n";
+          << tag << " >> 9)" << (kTileBits > 12 ? std::string(" ^ (zt") + tag + " >> 12)" : std::string()) << ") & 7);\n";
     };
     auto zreg = [&](uint64_t c, int i) {
         int z = 0;

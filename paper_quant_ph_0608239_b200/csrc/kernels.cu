@@ -190,7 +190,7 @@ __device__ __forceinline__ void u4_op(double2 (&a)[kAmpsPerThread], const KOp *r
 // residue t mod 3, so a warp access whose 5 lane bits cover all three
 // residues touches every bank group exactly 4 times (4 wavefronts per
 // 512 B: conflict-free).  swz is GF(2)-linear: swz(a ^ b) = swz(a) ^ swz(b).
-__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7); }
 
 // thread's lane/warp part of the smem index and the 4 register-bit parts
 __device__ __forceinline__ void smem_coords(uint64_t c, int lane, int warp, int &zt, int (&zr)[kRegBits])
