@@ -230,7 +230,9 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * every launch), "max_scan" (planner look-ahead window), "exchange_chunk_mb"
  * (exchange piece cap; the pieces are double-buffered between the engine
  * stream and a transfer stream), "comm_timeout_ms", "jit", "plan_cache",
- * "pass_variant", "global_policy", "peak_link_gbs" (link GB/s per direction
+ * "pass_variant", "global_policy", "sample_batch" (two-level sampler: cap on
+ * the high bins whose conditional marginals are built per batch; 0 = sized by
+ * memory, <= 2^24 entries), "peak_link_gbs" (link GB/s per direction
  * for the sharded planner's device-time model; its FP64 and HBM rates are
  * measured once per process on the device, qsim_probe_peaks), "overlap" (a pass followed by an
  * exchange whose local bits are not tile bits of the pass runs block by block,

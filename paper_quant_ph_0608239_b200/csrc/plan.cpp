@@ -17,6 +17,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -1036,6 +1037,21 @@ void Planner::emit_exchange(const std::vector<GateRec> &gates, const std::vector
         return a > b;  // prefer the top bits: contiguous exchange blocks
     });
     int K = std::min<int>((int)need.size(), (int)cand.size());
+    // Among the 2K furthest-used candidates, prefer victims that are not tile
+    // bits of the pass just emitted: that pass can then run block by block
+    // under this exchange (runtime overlap), at the price of evicting a qubit
+    // used slightly sooner.
+    static const int prefer_off_tile = [] { const char *e = getenv("QSIM_PLAN_VICTIM_TILE"); return e ? atoi(e) : 1; }();
+    if (prefer_off_tile && !out.empty() && out.back().type == ST_PASS && K > 0) {
+        const Step &prev = out.back();
+        auto in_tile = [&](int p) {
+            for (int t = 0; t < kTileBits; t++)
+                if (prev.pass.tp[t] == p || prev.pass.tp_out[t] == p) return true;
+            return false;
+        };
+        const size_t pool = std::min(cand.size(), (size_t)2 * K);
+        std::stable_partition(cand.begin(), cand.begin() + pool, [&](int p) { return !in_tile(p); });
+    }
     Step s;
     s.type = ST_EXCHANGE;
     for (int i = 0; i < K; i++) {

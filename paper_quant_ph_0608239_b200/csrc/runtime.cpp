@@ -94,6 +94,7 @@ struct qsim_ctx_s {
     int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
     int64_t chunk_mb = 1024;
+    int64_t sample_batch = 0;  // two-level sampler: high bins per batch cap (option sample_batch; 0 = by memory)
     double peak_link_gbs = 0;  // planner link rate per direction (option peak_link_gbs; 0 = nominal)
     int overlap = 1;  // pass + exchange overlap: 1 = SPMD transports, 2 = also virtual shards, 0 = off
     cudaEvent_t ov_evs[64] = {};
@@ -1674,7 +1675,8 @@ static qsim_status measure_two_level(qsim_ctx c, const int *qubits, int k, uint6
     if (s != QSIM_OK) return s;
     if (!n_shots) return QSIM_OK;
     const size_t BH = phi.size(), per = (size_t)1 << cl;
-    const size_t batch_rows = std::max<size_t>(1, ((size_t)1 << 24) / per);
+    size_t batch_rows = std::max<size_t>(1, ((size_t)1 << 24) / per);
+    if (c->sample_batch > 0) batch_rows = std::min(batch_rows, (size_t)c->sample_batch);
     // device: p_hi | CDF | res (n) | rows (batch_rows x per) | bhi, shot_idx, out (n each) | bins | shot_row (u32)
     const size_t need = 2 * BH + n_shots + batch_rows * per + 3 * n_shots + batch_rows + n_shots / 2 + 8;
     if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
@@ -1811,6 +1813,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
     else if (k == "timing") c->timing = value != 0;
     else if (k == "max_scan") { c->max_scan = value < 1 ? 1 : (int)std::min<int64_t>(value, 1 << 30); c->pc.valid = false; }
     else if (k == "exchange_chunk_mb") c->chunk_mb = value < 1 ? 1 : value;
+    else if (k == "sample_batch") c->sample_batch = std::max<int64_t>(value, 0);
     else if (k == "peak_link_gbs") c->peak_link_gbs = (double)std::max<int64_t>(value, 0);
     else if (k == "overlap") c->overlap = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 2);
     else if (k == "comm_timeout_ms") {

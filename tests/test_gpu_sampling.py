@@ -67,6 +67,25 @@ def test_measure_permuted_listed_subset(P, oracle_mod):
     sim.close()
 
 
+def test_measure_two_level_batches(P, oracle_mod):
+    """The second level built in many small batches of high bins (option
+    sample_batch) gives the same outcomes as one batch."""
+    n = 26
+    gates = C.random_brickwork(n, 2, seed=31)
+    sim = P.QSim(n, n_ranks=2, transport="virtual")
+    sim.init_basis(0)
+    sim.run_circuit(gates)
+    qs = list(range(n))
+    one = sim.measure(qs, seed=5, shots=64)
+    sim.set_option("sample_batch", 3)
+    many = sim.measure(qs, seed=5, shots=64)
+    assert np.array_equal(one, many)
+    o = _oracle(oracle_mod, n, 0, gates)
+    ref, tie = o.measure(qs, 5, 64)
+    _check(many, ref, tie, 56)
+    sim.close()
+
+
 def test_measure_whole_register_loopback(P, oracle_mod):
     """k = n = 25 on 4 SPMD loopback ranks (the NCCL-branch reductions)."""
     n = 25
