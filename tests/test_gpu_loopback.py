@@ -56,8 +56,11 @@ def test_loopback_kitchen_sink(P, oracle_mod, ranks, policy):
         assert st["exchanges"] >= 1
     assert all(np.array_equal(res[0][0], x[0]) for x in res)
     # the virtual transport (one context, device copies between its shards)
-    # plans the same steps and does the same arithmetic: identical bits
+    # plans the same steps and does the same arithmetic: identical bits (with
+    # the pass/exchange overlap on, as on the SPMD transports, the planner's
+    # cost model and so its plan are the same)
     sim = P.QSim(n, n_ranks=ranks, transport="virtual")
+    sim.set_option("overlap", 2)
     sim.set_option("global_policy", policy)
     sim.init_basis(3)
     sim.run_circuit(gates)
