@@ -161,6 +161,22 @@ def pass_roofline(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float)
     return 1e3 * t, slots
 
 
+def sigma_gate_flop_per_amp(gates) -> float:
+    """SURVEY §8(d) algorithmic FP64 flops per amplitude of the unfused gate
+    list: a general (complex) 2x2 costs 14 per touched amplitude, an exact
+    X-type target (CNOT, Toffoli) or a SWAP 0, controls halve the touched set."""
+    from workloads.gates import G_1Q, G_CTRL
+    f = 0.0
+    for g in gates:
+        if g.kind not in (G_1Q, G_CTRL):
+            continue
+        u = [complex(z) for z in g.u]
+        if abs(u[0]) == 0 and abs(u[3]) == 0 and u[1] == 1 and u[2] == 1:
+            continue  # exact X target: a swap
+        f += 14.0 / (1 << len(getattr(g, "controls", ()) or ()))
+    return f
+
+
 def cpu_sample(layers: int, reps: int = 1):
     """The oracle on the first `layers` layers of the same 24-qubit circuit,
     `reps` times (state re-initialised), with <Q_i> each time."""
@@ -393,6 +409,7 @@ def run_ours(args):
     ms = max_over_ranks(e0.elapsed_time(e1))
     st_value = sim.stats()
     value = args.steps * n_o * float(1 << n) / (ms / 1e3)
+    step_ms_dev = ms / args.steps
 
     # ---- kernel roofline: the same steps again with CUDA events around every
     # launch (on the engine's stream, where the kernels run), after the value
@@ -411,16 +428,19 @@ def run_ours(args):
     # gate array (qsim_gate[]) is validated, planned (plan cache off) and
     # uploaded every step and <Q_i> comes back to host memory; wall clock,
     # max over ranks.
+    # (K steps like the value region, at most ~10 s of them on the large
+    # multi-GPU workloads; the variants below at most 20 steps / ~4 s)
+    e2e_main = max(1, min(args.steps, int(10e3 / max(step_ms_dev, 1e-3))))
     sim.set_option("plan_cache", 0)
     step()
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_main):
         step()
     barrier()
-    e2e = args.steps * n_o * float(1 << n) / max_over_ranks(time.perf_counter() - t0)
+    e2e = e2e_main * n_o * float(1 << n) / max_over_ranks(time.perf_counter() - t0)
     # the same with a synchronous readout every step (host and device alternate)
-    e2e_steps = max(1, min(args.steps, 20))
+    e2e_steps = max(1, min(args.steps, 20, int(4e3 / max(step_ms_dev, 1e-3))))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -464,7 +484,7 @@ def run_ours(args):
                     "plan_cache": "off: every step validates, plans and uploads the gate list",
                     "readout": "<Q_i> copied to pinned host memory every step (async); host syncs at the end",
                     "value_sync_readout": e2e_sync, "value_plan_cached": e2e_cached,
-                    "sync_and_cached_steps": e2e_steps},
+                    "steps": e2e_main, "sync_and_cached_steps": e2e_steps},
             "gpu_launches": int(st_value["kernel_launches"]),
             "roofline": {"bound": "alu", "achieved": fp64_ach, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": (fp64_ach / fp64_peak) if fp64_ach else None, "traffic": traffic,
@@ -474,6 +494,13 @@ def run_ours(args):
                          "frac_of_derived": (fp64_ach / pk["fp64_derived"]) if fp64_ach else None,
                          "achieved_from": "executed FP64-pipe instructions of the generated code (per launch) "
                                           "x 2 / per-launch CUDA-event time",
+                         "executed_fp64_instr_per_amp_step": (st["pass_fp64_slots"] / rf_steps / float(1 << (n - G)))
+                         if rf_steps else None,
+                         "note": "executed count: 3M complex form, 13 FP64 instructions per amplitude per fused 4x4 "
+                                 "block (the round-1 count was the direct form's 16)",
+                         "sigma_gate_tflops": sigma_gate_flop_per_amp(gates) * float(1 << n) / (step_ms / 1e3) / 1e12,
+                         "sigma_gate_note": "SURVEY 8(d) unfused per-gate flops (14 per general U2 amp, 0 for CNOT) "
+                                            "over the whole step: fusion makes this exceed the FP64 peak",
                          "launches": int(st["passes"]), "kernel_ms": pass_ms, "timed_steps": rf_steps,
                          "kernel_share_of_step": pass_ms / (step_ms * rf_steps) if step_ms > 0 else None,
                          # per-launch bound max(FP64, HBM) summed over the passes of a step
