@@ -27,19 +27,20 @@ def summary(rep):
 
 for src, dst in (("bench.json", "bench.json"), ("launches.csv", "bench_launches.csv"),
                  ("configs.jsonl", "configs.jsonl"), ("paper.jsonl", "paper_benchmarks.jsonl"),
-                 ("bench_reference.json", "bench_reference.json")):
+                 ("sweep30.jsonl", "position_sweep_30q.jsonl"), ("bench_reference.json", "bench_reference.json")):
     if os.path.exists(os.path.join(G, src)) and os.path.getsize(os.path.join(G, src)):
         shutil.copy(os.path.join(G, src), os.path.join(P, f"{r}_{dst}"))
-for rep, dst in (("prof_pass.ncu-rep", "pass_jit_ncu.txt"), ("prof_qft.ncu-rep", "pass_qft_ncu.txt")):
+for rep, dst in (("prof_pass.ncu-rep", "pass_c2.txt"), ("prof_qft.ncu-rep", "pass_qft.txt"),
+                 ("prof_perm.ncu-rep", "perm_run_composed.txt")):
     if os.path.exists(os.path.join(G, rep)):
         open(os.path.join(P, f"{r}_{dst}"), "w").write(summary(os.path.join(G, rep)))
-t = open(os.path.join(P, f"{r}_pass_jit_ncu.txt")).read()
+t = open(os.path.join(P, f"{r}_pass_c2.txt")).read()
 rd = float(re.search(r"dram__bytes_read.sum\s+([\d.]+) Mbyte", t).group(1)) * 1e6
 wr = float(re.search(r"dram__bytes_write.sum\s+([\d.]+) Mbyte", t).group(1)) * 1e6
-json.dump({"kernel": "qsim_pass", "workload": "config 2 (24 q, block-fused, low-qubit remap), launch 11 of "
+json.dump({"kernel": "qsim_pass", "workload": "config 2 (24 q, block-fused, low-qubit remap, 3M blocks), launch 11 of "
            "tools/profile_pass.py", "dram_bytes_read_per_launch": int(round(rd)),
            "dram_bytes_write_per_launch": int(round(wr)), "dram_bytes_per_launch": int(round(rd + wr)),
            "algorithmic_bytes_per_launch": 536870912,
-           "source": f"profiles/{r}_pass_jit_ncu.txt (ncu --set full --clock-control none)"},
+           "source": f"profiles/{r}_pass_c2.txt (ncu --set full --clock-control none)"},
           open(os.path.join(P, "pass_traffic.json"), "w"))
 print("collected into profiles/ as", r)
