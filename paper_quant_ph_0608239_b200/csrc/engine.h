@@ -165,6 +165,7 @@ struct PermRunDesc {
     // change into the slow table the per-tile composition starts from.
     // (pre_mask != 0: instances in one contiguous range per CTA; else grid-stride)
     uint32_t pre_mask, slow_mask;
+    int32_t bulk;  // contiguous tiles staged by one bulk copy each (k_perm_run)
 };
 
 }  // namespace qsb

@@ -506,6 +506,33 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// 1D bulk copies (the TMA engine, no tensor map) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+}
+
 constexpr int kPermRunThreads = 512;
 // Composition (PermRunDesc pre_mask / slow_mask): the gather chain of an
 // element is P_jk^-1 o ... with j descending.  Its head, the perms without
@@ -551,7 +578,28 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
         }
         return inst < i_end ? inst : d.n_inst;
     };
-    auto stage = [&](double2 *buf, uint64_t base, uint32_t A) {
+    // Contiguous tiles (the register on the lowest bits, Shor's case): one
+    // thread stages the whole tile with a single bulk copy completing on the
+    // slot's mbarrier; no per-thread copies, and the wait is the data's own
+    // arrival (no CTA barrier).  Otherwise per-element cp.async of the
+    // elements some perm touches.
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const bool bulk = d.bulk != 0 && d.contiguous;
+    if (bulk && threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned bar_phase = 0;  // bit b: parity to wait for on slot b
+    auto stage = [&](double2 *buf, uint64_t base, uint32_t A, int slot) {
+        if (bulk) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of buf
+                mbar_expect_tx(&s_bar[slot], E * (unsigned)sizeof(double2));
+                bulk_g2s(buf, st + base, E * (unsigned)sizeof(double2), &s_bar[slot]);
+            }
+            return;
+        }
         for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
             if (A & xmask[e >> d.t])
                 cp_async16(buf + e, st + base + (d.contiguous ? e : dep_tile(e, d.tile_pos, d.tile_bits)));
@@ -591,17 +639,25 @@ __global__ void __launch_bounds__(kPermRunThreads) k_perm_run(const __grid_const
     uint64_t inst = s_inst[0], base = s_base[0];
     uint32_t A = s_A[0];
     if (inst < d.n_inst) {
-        stage(bufs, base, A);
+        stage(bufs, base, A, 0);
         if (compose) build(A, comp);
     }
-    cp_async_commit();
+    if (!bulk) cp_async_commit();
+    else __syncthreads();  // comp[0] complete before the first gather (the bulk loop has no top barrier)
     for (int b = 0; inst < d.n_inst; b ^= 1) {
         const uint64_t ninst = s_inst[b ^ 1], nbase = s_base[b ^ 1];
         const uint32_t nA = s_A[b ^ 1];
-        if (ninst < d.n_inst) stage(bufs + (size_t)(b ^ 1) * E, nbase, nA);
-        cp_async_commit();  // (possibly empty) group of the next tile
-        cp_async_wait1();   // this thread's copies of the current tile landed
-        __syncthreads();    // ... and everyone's; comp[b] complete
+        if (ninst < d.n_inst) stage(bufs + (size_t)(b ^ 1) * E, nbase, nA, b ^ 1);
+        if (bulk) {
+            // the bulk copy's completion publishes the tile; comp[b] and the
+            // look-ahead slots were published by the previous iteration's barrier
+            mbar_wait(&s_bar[b], (bar_phase >> b) & 1);
+            bar_phase ^= 1u << b;
+        } else {
+            cp_async_commit();  // (possibly empty) group of the next tile
+            cp_async_wait1();   // this thread's copies of the current tile landed
+            __syncthreads();    // ... and everyone's; comp[b] complete
+        }
         if (threadIdx.x == 0) {  // slot b (this tile's) is free: every thread read it last iteration
             uint64_t b2 = 0;
             uint32_t a2 = 0;

@@ -671,6 +671,8 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
             d.slow_mask |= 1u << j;
         }
     }
+    static const int bulk = [] { const char *e = getenv("QSIM_PERMRUN_BULK"); return e ? atoi(e) : 1; }();
+    d.bulk = bulk && d.contiguous;
     if (perm_run_smem(d) > kPermRunSmemMax) FAIL(c, QSIM_ERR_ARG, "permutation run too large for shared memory");
     RangeGuard rg(c, 2, 0);
     for (int i = 0; i < n_local(c); i++) {

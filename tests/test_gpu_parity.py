@@ -539,3 +539,23 @@ def test_gpu_fuzz_long(P, oracle_mod, seed):
     sim.init_basis(init)
     sim.run_circuit(gates)
     assert_parity(sim, oracle_run(oracle_mod, n, init, gates), n)
+
+
+@pytest.mark.parametrize("G,y,X,F", [(247, 194, 14, 8), (899, 2, 12, 10), (35, 3, 10, 6)])
+def test_perm_run_repeat_bitwise(P, oracle_mod, G, y, X, F):
+    """Race canary for the permutation run (bulk-copy staging on mbarriers,
+    composed chain head; compute-sanitizer is unavailable on this pool):
+    eight runs give bitwise-identical states equal to the oracle, for
+    registers of 6, 8 and 10 qubits (in-tile controls, several instances per
+    CTA)."""
+    w = C.shor_order_finding(G, y, X, F)
+    ref = oracle_run(oracle_mod, w.n, w.init, w.gates).amplitudes()
+    first = None
+    for _ in range(8):
+        sim = gpu_run(P, w.n, w.init, w.gates)
+        got = sim.get_amplitudes()
+        sim.close()
+        assert np.max(np.abs(got - ref)) <= TOL
+        if first is None:
+            first = got
+        assert np.array_equal(got, first)
