@@ -390,10 +390,7 @@ JitPass jit_generate(const Step &st)
         }
     }
     const int NS = (int)slot_S.size(), NW = kPassThreads / 32;
-    static const int nouni = env_int("QSIM_JIT_NOUNI", 0);  // TIMING PROBE ONLY (wrong results)
-    if (NS && nouni) {
-        s << " __shared__ unsigned long long utot[" << NS << "];\n if (threadIdx.x < " << NS << ") utot[threadIdx.x] = 0;\n __syncthreads();\n";
-    } else if (NS) {
+    if (NS) {
         s << " __shared__ unsigned long long uw[" << NW * NS << "], utot[" << NS << "];\n";
         s << " {\n";
         for (int k = 0; k < NS; k++) s << "  unsigned long long u" << k << " = 0;\n";
