@@ -73,5 +73,32 @@ int main(void)
     CHECK(qsim_get_amplitudes(c1, 1023, 1, &a[0]));
     if (fabs(nrm - 1.0) > 1e-14 || fabs(a[0].re - 1.0 / 32.0) > 1e-15) return 9;
     CHECK(qsim_destroy(c1));
+    /* whole-register sampling of a 26-qubit GHZ state (k = n > 24: the
+     * two-level sampler): every shot is all zeros or all ones, both occur */
+    qsim_ctx c2 = NULL;
+    const int n2 = 26;
+    CHECK(qsim_create(n2, 1, &c2));
+    CHECK(qsim_init_basis(c2, 0));
+    CHECK(qsim_apply_1q(c2, 0, H));
+    for (int i = 1; i < n2; i++) {
+        int c = 0;
+        CHECK(qsim_apply_controlled(c2, &c, 1, i, X));
+    }
+    int all[26];
+    for (int i = 0; i < n2; i++) all[i] = i;
+    uint64_t shots[64];
+    CHECK(qsim_measure(c2, all, n2, 7, 64, shots));
+    int zeros = 0, ones = 0;
+    for (int s = 0; s < 64; s++) {
+        if (shots[s] == 0) zeros++;
+        else if (shots[s] == (1ULL << n2) - 1) ones++;
+        else return 10;
+    }
+    if (!zeros || !ones) return 11;
+    CHECK(qsim_destroy(c2));
+    /* roofline denominators of this device */
+    double f64 = 0, gbs = 0;
+    if (qsim_probe_peaks(&f64, &gbs) != QSIM_OK || f64 < 1.0 || gbs < 100.0) return 12;
+    printf("abi_client two-level ok: zeros=%d ones=%d fp64=%.1f TF copy=%.0f GB/s\n", zeros, ones, f64, gbs);
     return 0;
 }

@@ -297,7 +297,7 @@ def test_c_client_runs(pkg, tmp_path):
     import subprocess
     r = subprocess.run([_build_c_client(pkg, tmp_path)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr + r.stdout
-    assert "abi_client ok" in r.stdout
+    assert "abi_client ok" in r.stdout and "abi_client two-level ok" in r.stdout
 
 
 def test_jit_key_implies_same_source(pkg):
