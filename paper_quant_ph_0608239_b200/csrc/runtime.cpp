@@ -86,6 +86,9 @@ struct qsim_ctx_s {
     double2 **d_shard_ptrs = nullptr;
     double *d_red = nullptr;
     size_t d_red_cap = 0;
+    // the two-level sampler's own buffers (its rank-order reductions use d_red)
+    double *d_samp = nullptr;
+    size_t d_samp_cap = 0;
     // options
     bool fusion = true, timing = false, block_fusion = true, low_remap = true;
     int remap_lookahead = PlanOptions().remap_lookahead;
@@ -1364,6 +1367,7 @@ qsim_status qsim_destroy(qsim_ctx c)
     if (c->d_ttab) cudaFree(c->d_ttab);
     if (c->d_perm) cudaFree(c->d_perm);
     if (c->d_red) cudaFree(c->d_red);
+    if (c->d_samp) cudaFree(c->d_samp);
     if (c->d_shard_ptrs) cudaFree(c->d_shard_ptrs);
     if (c->h_ops) cudaFreeHost(c->h_ops);
     if (c->h_perm) cudaFreeHost(c->h_perm);
@@ -1681,8 +1685,8 @@ static qsim_status measure_two_level(qsim_ctx c, const int *qubits, int k, uint6
     if (c->sample_batch > 0) batch_rows = std::min(batch_rows, (size_t)c->sample_batch);
     // device: p_hi | CDF | res (n) | rows (batch_rows x per) | bhi, shot_idx, out (n each) | bins | shot_row (u32)
     const size_t need = 2 * BH + n_shots + batch_rows * per + 3 * n_shots + batch_rows + n_shots / 2 + 8;
-    if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
-    double *dp = c->d_red, *dc = dp + BH, *dres = dc + BH, *drows = dres + n_shots;
+    if ((s = ensure_dev(c, c->d_samp, c->d_samp_cap, need)) != QSIM_OK) return s;
+    double *dp = c->d_samp, *dc = dp + BH, *dres = dc + BH, *drows = dres + n_shots;
     uint64_t *dbhi = (uint64_t *)(drows + batch_rows * per), *didx = dbhi + n_shots, *dout = didx + n_shots,
              *dbins = dout + n_shots;
     uint32_t *drow = (uint32_t *)(dbins + batch_rows);

@@ -87,19 +87,32 @@ def test_measure_two_level_batches(P, oracle_mod):
 
 
 def test_measure_whole_register_loopback(P, oracle_mod):
-    """k = n = 25 on 4 SPMD loopback ranks (the NCCL-branch reductions)."""
+    """k = n = 25 on 4 SPMD loopback ranks (the NCCL-branch reductions), with
+    enough shots and small batches that the rank-order reduction buffer is
+    larger than the sampler's first buffers (they must not alias)."""
     n = 25
     gates = C.random_brickwork(n, 2, seed=21)
     o = _oracle(oracle_mod, n, 0, gates)
     ref, tie = o.measure(list(range(n)), 7, 40)
+    qs = [int(q) for q in np.random.default_rng(5).permutation(n)]  # the whole register, permuted order
+    ref2, tie2 = o.measure(qs[:25], 8, 40)
 
     def body(sim, r):
         sim.init_basis(0)
         sim.run_circuit(gates)
-        return sim.measure(list(range(n)), seed=7, shots=40)
+        a = sim.measure(list(range(n)), seed=7, shots=40)
+        sim.set_option("sample_batch", 5)
+        b = sim.measure(qs[:25], seed=8, shots=40)
+        sim.set_option("sample_batch", 0)
+        many = sim.measure(list(range(n)), seed=9, shots=20000)
+        return a, b, many
 
-    for shots in P.run_loopback(n, 4, body):
-        _check(shots, ref, tie, 32)
+    for a, b, many in P.run_loopback(n, 4, body):
+        _check(a, ref, tie, 32)
+        _check(b, ref2, tie2, 32)
+        # 20000 shots of the whole register: the outcome frequencies follow |a|^2
+        p = np.abs(o.amplitudes()) ** 2
+        assert abs(float(np.mean(p[many.astype(np.int64)])) - float(np.sum(p * p))) < 0.2 * float(np.sum(p * p))
 
 
 def test_measure_basis_state_and_limits(P):

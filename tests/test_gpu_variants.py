@@ -27,6 +27,7 @@ elif kind == "qft":
 else:
     gates = C.random_chain(n, 10, seed=5, sweep=True)
 sim = QSim(n, n_ranks=shards, transport="virtual" if shards > 1 else "local")
+sim.set_option("overlap", {overlap})
 sim.init_basis(init)
 sim.run_circuit(gates)
 nrm = sim.norm()
@@ -40,16 +41,16 @@ for first in range(0, 1 << n, chunk):
     err = max(err, float(np.max(np.abs(g - view[first:first + g.size]))))
 st = sim.stats()
 print(json.dumps({{"n": n, "shards": shards, "gates": len(gates), "max_abs_diff": err, "norm_dev": abs(1 - nrm),
-                  "exchanges": st["exchanges"], "passes": st["passes"], "jit_compile_ms": st["jit_compile_ms"],
-                  "jit_kernels": st["jit_kernels"]}}))
+                  "exchanges": st["exchanges"], "overlapped": st["overlapped"], "passes": st["passes"],
+                  "jit_compile_ms": st["jit_compile_ms"], "jit_kernels": st["jit_kernels"]}}))
 '''
 
 
-def _run(n, shards, kind, env=None, timeout=600):
+def _run(n, shards, kind, env=None, timeout=600, overlap=1):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    code = _RUN.format(root=ROOT, n=n, shards=shards, kind=kind)
+    code = _RUN.format(root=ROOT, n=n, shards=shards, kind=kind, overlap=overlap)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout,
                        env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stderr[-3000:]
@@ -63,7 +64,9 @@ def test_large_full_state_parity():
     (n = 33: 128 GiB on the GPU and in host RAM).  Result recorded in
     profiles/r1_parity_33q_8shards.json."""
     n = int(os.environ["QSIM_LARGE_PARITY"])
-    d = _run(n, 8, os.environ.get("QSIM_LARGE_KIND", "chain"), timeout=3600)
+    # overlap = 2: the pass + exchange overlap runs on the virtual shards too
+    d = _run(n, 8, os.environ.get("QSIM_LARGE_KIND", "chain"), timeout=3600,
+             overlap=int(os.environ.get("QSIM_LARGE_OVERLAP", "2")))
     print(json.dumps(d))
     assert d["max_abs_diff"] <= 1e-11 and d["norm_dev"] <= 1e-12
     assert d["exchanges"] >= 1 and d["passes"] >= 1  # 3 nonlocal qubits: the sharded path ran
