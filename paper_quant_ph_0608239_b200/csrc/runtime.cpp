@@ -617,6 +617,13 @@ static qsim_status upload_program(qsim_ctx c, std::vector<Step> &steps)
 static int local_ranks(qsim_ctx c, int i) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? i : c->rank; }
 static int n_local(qsim_ctx c) { return c->transport == QSIM_TRANSPORT_VIRTUAL ? c->P : 1; }
 
+// insertion sort of a few tile positions (bounded, no std::sort threshold games)
+static void sort_small(int *a, int n)
+{
+    for (int i = 1; i < n; i++)
+        for (int j = i; j > 0 && a[j - 1] > a[j]; j--) std::swap(a[j - 1], a[j]);
+}
+
 static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
 {
     PermRunDesc d{};
@@ -624,7 +631,7 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
     // smaller tiles than k_perm's: the run's tables share the shared memory,
     // and more resident CTAs hide the load latency of the gather
     static const int run_tb = [] { const char *e = getenv("QSIM_PERMRUN_TILE"); return e ? atoi(e) : 11; }();
-    int tb = std::max(std::min(run_tb, M), t);
+    int tb = std::min(std::max(std::min(run_tb, M), t), kPermTileBits);  // t <= 12 = kPermTileBits
     const int R = (int)s.run_cm.size();
     while (tb > t && perm_run_smem_bytes(tb, t, R) > kPermRunSmemMax) tb--;
     d.M = M;
@@ -639,7 +646,7 @@ static qsim_status exec_perm_run(qsim_ctx c, const Step &s)
         if (!used[p]) { d.tile_pos[nb++] = p; used[p] = true; }
     int srt[kPermTileBits];
     for (int i = 0; i < tb; i++) srt[i] = d.tile_pos[i];
-    std::sort(srt, srt + tb);
+    sort_small(srt, tb);
     for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
     d.n_inst = 1ULL << (M - tb);
     d.contiguous = 1;
@@ -693,6 +700,7 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
     const int M = c->M, t = (int)s.ptargets.size();
     int tb = std::min(kPermTileBits, M);
     if (tb < t) tb = t;
+    if (tb > kPermTileBits) FAIL(c, QSIM_ERR_ARG, "permutation of %d targets exceeds the %d-bit tile", t, kPermTileBits);
     d.M = M;
     d.t = t;
     d.tile_bits = tb;
@@ -704,7 +712,7 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
         if (!used[p]) { d.tile_pos[nb++] = p; used[p] = true; }
     int srt[kPermTileBits];
     for (int i = 0; i < tb; i++) srt[i] = d.tile_pos[i];
-    std::sort(srt, srt + tb);
+    sort_small(srt, tb);
     for (int i = 0; i < tb; i++) d.tile_sorted[i] = srt[i];
     d.n_inst = 1ULL << (M - tb);
     d.contiguous = 1;
