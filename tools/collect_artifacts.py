@@ -31,7 +31,7 @@ for src, dst in (("bench.json", "bench.json"), ("launches.csv", "bench_launches.
     if os.path.exists(os.path.join(G, src)) and os.path.getsize(os.path.join(G, src)):
         shutil.copy(os.path.join(G, src), os.path.join(P, f"{r}_{dst}"))
 for rep, dst in (("prof_pass.ncu-rep", "pass_c2.txt"), ("prof_qft.ncu-rep", "pass_qft.txt"),
-                 ("prof_perm.ncu-rep", "perm_run_composed.txt")):
+                 ("prof_perm.ncu-rep", "perm_run_bulk.txt")):
     if os.path.exists(os.path.join(G, rep)):
         open(os.path.join(P, f"{r}_{dst}"), "w").write(summary(os.path.join(G, rep)))
 t = open(os.path.join(P, f"{r}_pass_c2.txt")).read()
