@@ -515,6 +515,8 @@ def run_ours(args):
                        "jit_passes_per_step": st_value["jit_launches"] / args.steps,
                        "plan_cache_hits": int(st_value["plan_cache_hits"]),
                        "exchanges_per_step": st_value["exchanges"] / args.steps,
+                       "overlapped_per_step": st_value["overlapped"] / args.steps,
+                       "link_gbs_measured_at_creation": st_value["link_gbs"] or None,
                        "kernels": kernel_roofline(st, pk, 32 << (n - G))},
         }
         if world == 1 and not args.no_per_config:

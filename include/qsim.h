@@ -267,6 +267,8 @@ typedef struct {
     uint64_t overlapped;       /* pass + exchange pairs run overlapped (option "overlap"; counted in
                                   passes and exchanges too) */
     double overlap_ms;         /* event time of the overlapped pairs (timing=1; not in pass_ms/exchange_ms) */
+    double link_gbs;           /* SPMD: partner-link rate per direction measured at creation, minimum over
+                                  the ranks (the planner's link rate); 0 = not measured */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);

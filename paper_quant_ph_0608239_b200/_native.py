@@ -47,7 +47,8 @@ class qsim_stats(ctypes.Structure):
                                                             ("plan_cache_hits", ctypes.c_uint64),
                                                             ("streamed_steps", ctypes.c_uint64),
                                                             ("overlapped", ctypes.c_uint64),
-                                                            ("overlap_ms", ctypes.c_double)]
+                                                            ("overlap_ms", ctypes.c_double),
+                                                            ("link_gbs", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -99,6 +99,10 @@ struct qsim_ctx_s {
     int64_t chunk_mb = 1024;
     int64_t sample_batch = 0;  // two-level sampler: high bins per batch cap (option sample_batch; 0 = by memory)
     double peak_link_gbs = 0;  // planner link rate per direction (option peak_link_gbs; 0 = nominal)
+    // SPMD: the planner's FP64 / HBM / link rates, measured at creation and
+    // reduced to their minimum over the ranks, so that every rank plans with
+    // identical inputs (the plans must agree step for step); 0 = not measured
+    double plan_fp64 = 0, plan_hbm = 0, plan_link_gbs = 0;
     int overlap = 1;  // pass + exchange overlap: 1 = SPMD transports, 2 = also virtual shards, 0 = off
     cudaEvent_t ov_evs[64] = {};
     int ov_next = 0;
@@ -1031,6 +1035,68 @@ static void measured_peaks(double &fp64, double &hbm)
     hbm = b;
 }
 
+// SPMD creation (collective): measure the link rate to the partner rank
+// (rank ^ 1; pieces of up to 64 MiB through the scratch, NCCL send/recv or
+// the loopback copy), take the process's FP64 / HBM probe, and reduce all
+// three to their minimum over the ranks (all-gather), so that every rank's
+// planner sees the same numbers.
+static qsim_status probe_spmd_rates(qsim_ctx c)
+{
+    double f = 0, b = 0;
+    measured_peaks(f, b);
+    double link = 0;
+    const size_t bytes = std::min<size_t>((c->scratch_bytes / 2) / 16 * 16, (size_t)64 << 20);
+    if (bytes >= ((size_t)1 << 20)) {
+        cudaEvent_t e0 = ev_get(c), e1 = ev_get(c);
+        const int peer = c->rank ^ 1;
+        float best = 1e30f;
+        for (int it = 0; it < 4; it++) {
+            CK(c, cudaEventRecord(e0, c->stream));
+            CKC(c, group_start(_err));
+            CKC(c, send(c->scratch, bytes, peer, c->stream, _err));
+            CKC(c, recv((char *)c->scratch + bytes, bytes, peer, c->stream, _err));
+            CKC(c, group_end(_err));
+            CK(c, cudaEventRecord(e1, c->stream));
+            { qsim_status _s = sync_stream(c); if (_s != QSIM_OK) return _s; }
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it) best = std::min(best, ms);
+        }
+        c->event_pool.push_back(e0);
+        c->event_pool.push_back(e1);
+        link = best > 0 ? bytes / (best * 1e-3) / 1e9 : 0;
+    }
+    // min over ranks (a 0 anywhere -> 0: the nominal fallback everywhere)
+    const double mine[3] = {f, b, link};
+    double *dbuf = nullptr;
+    if (cudaMalloc((void **)&dbuf, sizeof(double) * 3 * (c->P + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        FAIL(c, QSIM_ERR_OOM, "rate probe buffer");
+    }
+    std::vector<double> all(3 * c->P);
+    qsim_status st = QSIM_OK;
+    if (cudaMemcpyAsync(dbuf, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) st = QSIM_ERR_CUDA;
+    std::string err;
+    if (st == QSIM_OK && c->comm->all_gather(dbuf, dbuf + 3, 3, c->stream, err)) {
+        c->poisoned = true;
+        c->last_error = err;
+        st = QSIM_ERR_COMM;
+    }
+    if (st == QSIM_OK && cudaMemcpyAsync(all.data(), dbuf + 3, sizeof(double) * 3 * c->P, cudaMemcpyDeviceToHost,
+                                         c->stream) != cudaSuccess)
+        st = QSIM_ERR_CUDA;
+    if (st == QSIM_OK) st = sync_stream(c);
+    cudaFree(dbuf);
+    if (st != QSIM_OK) return st;
+    double m[3] = {all[0], all[1], all[2]};
+    for (int r = 1; r < c->P; r++)
+        for (int k = 0; k < 3; k++) m[k] = std::min(m[k], all[3 * r + k]);
+    c->plan_fp64 = m[0];
+    c->plan_hbm = m[1];
+    c->plan_link_gbs = m[2];
+    return QSIM_OK;
+}
+
 static qsim_status flush(qsim_ctx c)
 {
     if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
@@ -1133,8 +1199,9 @@ static qsim_status flush(qsim_ctx c)
         opt.overlap = c->jit && c->P > 1 &&
                       (c->transport == QSIM_TRANSPORT_VIRTUAL ? c->overlap >= 2 : spmd(c) && c->overlap >= 1);
         if (c->P > 1) {  // the sharded planner weighs alternatives by modelled device time
-            double f = 0, b = 0;
-            measured_peaks(f, b);
+            double f = c->plan_fp64, b = c->plan_hbm;
+            if (!spmd(c)) measured_peaks(f, b);  // one process: the same values for every shard
+            if (spmd(c) && c->plan_link_gbs > 0 && c->peak_link_gbs <= 0) opt.peak_link = c->plan_link_gbs * 1e9;
             if (f > 0) opt.peak_fp64 = PlanOptions::kPassFp64Eff * f;
             if (b > 0) opt.peak_hbm = PlanOptions::kPassHbmEff * b;
             if (c->peak_link_gbs > 0) opt.peak_link = c->peak_link_gbs * 1e9;
@@ -1332,6 +1399,10 @@ qsim_status qsim_create_ext(const qsim_config *cfg, qsim_ctx *out)
         if (!c->comm) {
             fprintf(stderr, "qsim_create_ext: %s\n", err.c_str());
             return bail(QSIM_ERR_COMM);
+        }
+        if (P > 1) {
+            qsim_status ps = probe_spmd_rates(c);
+            if (ps != QSIM_OK) return bail(ps);
         }
     }
     {
@@ -1855,6 +1926,7 @@ qsim_status qsim_get_stats(qsim_ctx c, qsim_stats *out)
     *out = c->stats;
     out->jit_kernels = jit_cache().size();
     out->jit_compile_ms = jit_cache().compile_ms;
+    out->link_gbs = c->plan_link_gbs;
     return QSIM_OK;
 }
 

@@ -54,6 +54,7 @@ def test_loopback_kitchen_sink(P, oracle_mod, ranks, policy):
     for r, (amp, st, _) in enumerate(res):
         assert np.max(np.abs(amp - ref)) <= TOL, (r, np.max(np.abs(amp - ref)))
         assert st["exchanges"] >= 1
+        assert st["link_gbs"] == 0  # 4-KB scratch: no link probe (nominal rate), on every rank alike
     assert all(np.array_equal(res[0][0], x[0]) for x in res)
     # the virtual transport (one context, device copies between its shards)
     # plans the same steps and does the same arithmetic: identical bits (with
@@ -81,6 +82,8 @@ def test_loopback_config5_family(P, oracle_mod, ranks):
         assert abs(1 - nrm) <= 1e-12
         assert np.max(np.abs(ex - o.expectations())) <= 1e-12
         assert st["exchanges"] >= 1
+    # the link rate measured at creation is reduced to one value over the ranks
+    assert res[0][1]["link_gbs"] > 0 and len({st["link_gbs"] for _, st, _ in res}) == 1
 
 
 def test_loopback_noncontiguous_remap_and_readouts(P, oracle_mod):
