@@ -1,6 +1,6 @@
 """Small workloads that exercise every kernel family, for compute-sanitizer
 (racecheck / synccheck / memcheck) runs on one GPU:
-  compute-sanitizer --tool racecheck python tools/sanitize_run.py
+  compute-sanitizer --tool racecheck python tests/sanitize_run.py
 Fused tile passes with shared-memory re-layouts (JIT and interpreter tiers),
 phase runs + the qsim_pass_tab companion kernel (QFT), the permutation run
 (k_perm_run: cp.async double buffer, composed tables) and k_perm, exchanges
