@@ -150,20 +150,27 @@ qsim_status qsim_destroy(qsim_ctx ctx);
 qsim_status qsim_init_basis(qsim_ctx ctx, uint64_t index);
 
 /* Single-qubit gate on qubit q (Eqs. NUM2-NUM5; H, X, Y, R(phi)
- * and any unitary U). */
+ * and any unitary U).  u: host, row-major, copied.  Errors (state untouched):
+ * QSIM_ERR_QUBIT_RANGE, QSIM_ERR_NOT_UNITARY (max |U^dag U - I| > 1e-12),
+ * QSIM_ERR_ARG (NULL u), QSIM_ERR_STATE (before qsim_init_basis). */
 qsim_status qsim_apply_1q(qsim_ctx ctx, int q, const qsim_c128 u[4]);
 
 /* Controlled gate: U on target where all n_controls control qubits are 1
  * (CNOT Eq. NUM6, controlled phase Eq. COMM5 P:285-295,
  * controlled-V Eq. NUM7, Toffoli Eq. NUM8).
- * n_controls <= QSIM_MAX_CONTROLS. */
+ * n_controls <= QSIM_MAX_CONTROLS.  controls, u: host, copied.  Errors (state
+ * untouched): QSIM_ERR_QUBIT_RANGE, QSIM_ERR_DUP_QUBIT (a qubit repeated among
+ * controls and target), QSIM_ERR_NOT_UNITARY, QSIM_ERR_ARG. */
 qsim_status qsim_apply_controlled(qsim_ctx ctx, const int *controls, int n_controls, int target,
                                   const qsim_c128 u[4]);
 
 /* Controlled classical reversible map of a target register (the
  * "conditional operation" of Shor's step 2):
  * |c, w> -> |c, perm[w]> when all controls are 1.  Register bit b of w is
- * qubit targets[b]; n_targets <= QSIM_MAX_PERM_TARGETS. */
+ * qubit targets[b]; n_targets <= QSIM_MAX_PERM_TARGETS; perm: host array of
+ * 2^n_targets entries, copied.  Errors (state untouched): QSIM_ERR_NOT_PERMUTATION
+ * (not a bijection of [0, 2^n_targets)), QSIM_ERR_QUBIT_RANGE,
+ * QSIM_ERR_DUP_QUBIT, QSIM_ERR_ARG. */
 qsim_status qsim_apply_perm(qsim_ctx ctx, const int *controls, int n_controls, const int *targets,
                             int n_targets, const uint32_t *perm);
 
