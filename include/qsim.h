@@ -152,7 +152,8 @@ qsim_status qsim_init_basis(qsim_ctx ctx, uint64_t index);
 /* Single-qubit gate on qubit q (Eqs. NUM2-NUM5; H, X, Y, R(phi)
  * and any unitary U).  u: host, row-major, copied.  Errors (state untouched):
  * QSIM_ERR_QUBIT_RANGE, QSIM_ERR_NOT_UNITARY (max |U^dag U - I| > 1e-12),
- * QSIM_ERR_ARG (NULL u), QSIM_ERR_STATE (before qsim_init_basis). */
+ * QSIM_ERR_ARG (NULL u).  Gates queued before any qsim_init_basis make the
+ * next flush fail with QSIM_ERR_STATE. */
 qsim_status qsim_apply_1q(qsim_ctx ctx, int q, const qsim_c128 u[4]);
 
 /* Controlled gate: U on target where all n_controls control qubits are 1
