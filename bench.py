@@ -477,6 +477,11 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": warm, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling_note": ("N > 1 runs the config-5 family at 33 + log2 N qubits (weak scaling; N = 8 is config 5 "
+                             "at 36 q); its N = 1 point is detail.per_config[config5_family_33q] of the N = 1 line, "
+                             "whose headline is config 2") if world > 1 or args.workload == "config5" else
+                            ("N = 1 headline: config 2; the N > 1 lines run the config-5 family at 33 + log2 N "
+                             "qubits, whose N = 1 point is detail.per_config[config5_family_33q]"),
             "config": {"workload": wname, "n_qubits": n, "gates_per_step": n_o, "shard_qubits": n - G,
                        "parallelism": f"sharded{world}" if world > 1 else "single",
                        "l2": "state %d MiB per GPU > 126 MB L2 (no flush needed)" % ((16 << (n - G)) >> 20)},
