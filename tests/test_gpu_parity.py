@@ -512,10 +512,16 @@ def test_gpu_fuzz(P, oracle_mod, seed):
     sim.set_option("jit", seed % 5 != 4)
     if ranks > 1:
         sim.set_option("global_policy", seed % 3)
+        sim.set_option("overlap", 2 * (seed % 2))  # the pass + exchange overlap on half the seeds
     sim.init_basis(init)
     sim.run_circuit(gates)
     o = oracle_run(oracle_mod, n, init, gates)
     assert_parity(sim, o, n)
+    if n <= 16:  # full-register sampling (one level at k <= 24) vs the oracle's sampler
+        qs = list(range(n))
+        shots = sim.measure(qs, seed=seed, shots=64)
+        ref, tie = o.measure(qs, seed, 64)
+        assert np.array_equal(shots[tie == 0], ref[tie == 0])
     # again with the kernels cached: plan cache on (replay) or off (re-plan,
     # streamed launches)
     sim.set_option("plan_cache", seed % 2)
