@@ -246,7 +246,10 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * exchange whose local bits are not tile bits of the pass runs block by block,
  * each block's transfer overlapping the next block's compute: 1 = on the
  * NCCL / loopback transports [default]; 2 = also on virtual shards, where the
- * transfer is device copy work on the same HBM; 0 = in sequence). */
+ * transfer is device copy work on the same HBM; 0 = in sequence), "desync_ns"
+ * (pass kernels: the first-wave CTAs of SM slot 0 finish this many ns late so
+ * that the two CTAs an SM runs stay out of step -- one re-layouts through
+ * shared memory while the other computes; default 1500, 0 = off). */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {

@@ -158,7 +158,7 @@ JitPass jit_generate(const Step &st)
     const int kQexpOps = 13;
     const int minb = env_int("QSIM_JIT_MINB", kPassMinBlocks);  // CTAs per SM (register cap)
     s << "// minb=" << minb << "\n";
-    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long unused; "
+    s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long desync; "
          "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long fixbits; "
          "unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits + kMaxFix << "]; "
       << (kTsPad ? "int ts_pad[" + std::to_string(kTsPad) + "]; " : std::string())
@@ -761,6 +761,15 @@ JitPass jit_generate(const Step &st)
           << ".y) : \"memory\");\n";
     s << " }\n";
     s << " }\n";
+    // Phase offset between the two CTAs an SM runs.  CTAs of the first wave
+    // start together and, running identical code, stay in step: both re-
+    // layout (shared-memory bound) at the same time and both compute (FP64
+    // bound) at the same time.  The first-wave CTAs of slot 0 (blockIdx <
+    // SM count: the SM's slot-1 CTA is blockIdx + SM count) finish late by
+    // P.desync ns, so every later CTA on the SM starts out of step with its
+    // neighbour.  Branch-free (a branch here changes the kernel's uniform-
+    // register allocation); P.desync = SM count << 32 | ns, 0 = off.
+    s << " { const unsigned long long d = P.desync; __nanosleep(blockIdx.x < (unsigned)(d >> 32) ? (unsigned)d : 0u); }\n";
     s << "}\n";
     const int NTS = (int)tslot_S.size();
     if (NTS) {
@@ -799,8 +808,8 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
     uint8_t *b = buf.data();
     std::memcpy(b + 0, &state, 8);
     std::memcpy(b + 8, &rank_bits, 8);
-    const uint64_t unused = 0;
-    std::memcpy(b + 16, &unused, 8);
+    const uint64_t desync = 0;  // jit_set_desync
+    std::memcpy(b + 16, &desync, 8);
     const void *tab = jit_phase_table();
     std::memcpy(b + 24, &tab, 8);
     std::memcpy(b + kOffInit, &st.pass.init_phys, 8);
@@ -853,6 +862,12 @@ bool jit_set_block(std::vector<uint8_t> &buf, const Step &st, const int *pos, in
     std::memcpy(buf.data() + kOffTs, ts.data(), 4 * ts.size());
     std::memcpy(buf.data() + kOffFix, &fixbits, 8);
     return true;
+}
+
+void jit_set_desync(std::vector<uint8_t> &buf, uint32_t n_sm, uint32_t ns)
+{
+    const uint64_t d = ns ? ((uint64_t)n_sm << 32) | ns : 0;
+    if (buf.size() >= 24) std::memcpy(buf.data() + 16, &d, 8);
 }
 
 void jit_set_ttab(std::vector<uint8_t> &buf, void *ttab)

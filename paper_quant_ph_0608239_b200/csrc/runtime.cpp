@@ -96,6 +96,7 @@ struct qsim_ctx_s {
     int jit = 1;           // 1: pass-specialised NVRTC kernels, 0: interpreter k_pass only
     int global_policy = GP_AUTO;
     int pass_variant = 2;  // k_pass min CTAs per SM (1: <=255 regs, 2: <=128 regs)
+    int desync_ns = 1500;  // JIT pass: first-wave phase offset of the slot-0 CTAs (option desync_ns; 0 = off)
     int64_t chunk_mb = 1024;
     int64_t sample_batch = 0;  // two-level sampler: high bins per batch cap (option sample_batch; 0 = by memory)
     double peak_link_gbs = 0;  // planner link rate per direction (option peak_link_gbs; 0 = nominal)
@@ -762,6 +763,7 @@ static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t count
     if (pp[i].empty()) jit_pack_params(s, c->shards[i], rb, pp[i]);
     if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
     if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
+    jit_set_desync(pp[i], (uint32_t)c->n_sm, (uint32_t)c->desync_ns);
     // (the launch copies the parameter block)
     if (!jit_set_block(pp[i], s, fix_pos, K, fixbits)) FAIL(c, QSIM_ERR_STATE, "jit pass: too many fixed bits");
     size_t sz = pp[i].size();
@@ -1906,6 +1908,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
         if (c->comm) c->comm->timeout_ms = c->comm_timeout_ms;
     }
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
+    else if (k == "desync_ns") c->desync_ns = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 1000000);
     else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
     else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }
     else if (k == "global_policy") {

@@ -39,6 +39,8 @@ def comp(f):
 with cf.ThreadPoolExecutor(16) as ex:
     res = list(ex.map(comp, files))
 sp = [x[1] for x in res]
+if os.environ.get("JIT_SPILLS_VERBOSE"):
+    for r in res: print(r)
 print(json.dumps({"workload": wl, "3m": os.environ.get("QSIM_JIT_3M"), "il": os.environ.get("QSIM_JIT_U4IL"),
                   "kernels": len(res), "spill_total": sum(sp), "spill_max": max(sp),
                   "fp64_per_amp": sum(js["jit"]["fp64_per_amp"])}))
