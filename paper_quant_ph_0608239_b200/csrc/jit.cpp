@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <set>
 #include <functional>
 #include <sstream>
 #include <thread>
@@ -44,6 +45,7 @@ constexpr size_t kOffOut = (kOffTpo + 8 * kTileBits + 15) / 16 * 16;  // the mat
 constexpr int kTpoPad = (int)(kOffOut - kOffTpo) / 8 - kTileBits;     // u64s of padding after tpo
 struct Layout {
     int n_out = 0, n_m = 0;
+    int c_row = 0;  // first row of the host-formed phase factors (4 complex per row)
     size_t off_out = kOffOut, off_m = 0, bytes = 0;
 };
 
@@ -75,6 +77,96 @@ Forms forms_of(const Step &st)
     return f;
 }
 
+// Phase runs: where every OPC_PHASE_ACC term goes.  The generated pass
+// flushes monomial S (a product of register bits) lazily: an op on register
+// bit k flushes the live monomials containing k, a re-layout and the store
+// flush all.  Between two flushes of S (an "epoch") its angle is a sum of
+// terms of four kinds:
+//   const   -- unpredicated on lane, warp and out-of-tile bits: the same in
+//              every thread and tile, so e^{i sum} is formed on the host and
+//              travels in the parameter block (no exponential in the kernel);
+//   uniform -- predicated on out-of-tile bits only (CTA-uniform): summed per
+//              (S, epoch) slot once per tile through shared memory, where its
+//              e^{i sum} is also formed once per tile;
+//   thread  -- predicated on lane / warp bits only: summed per slot and thread
+//              once per launch by the companion kernel qsim_pass_tab, which
+//              stores e^{i sum};
+//   inline  -- the rest (mixed predicates, or too few terms for a table): an
+//              integer accumulator mo_S and one exponential at the flush.
+// The flush multiplies the amplitudes by the product of the parts present
+// (e^{i(a+b)} = e^{ia} e^{ib}).  The dry run below follows the generator's
+// flush rules exactly; jit_generate, layout_of and jit_pack_params share it.
+bool uniform_acc(const KOp &op) { return op.code == OPC_PHASE_ACC && op.mout && !op.mlane && !op.mwarp; }
+bool thread_acc(const KOp &op) { return op.code == OPC_PHASE_ACC && !op.mout && (op.mlane || op.mwarp); }
+bool const_acc(const KOp &op) { return op.code == OPC_PHASE_ACC && !op.mout && !op.mlane && !op.mwarp; }
+uint32_t touching(uint32_t bits)  // monomials that contain one of the register bits
+{
+    uint32_t F = 0;
+    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+        if (S & bits) F |= 1u << S;
+    return F;
+}
+struct PhasePlan {
+    // per op: (slot, sign) of each of its monomial terms, by kind
+    std::vector<std::vector<std::pair<int, int>>> uterms, tterms, cterms;
+    std::vector<uint32_t> slot_S, tslot_S, cslot_S;
+    std::map<std::pair<uint32_t, int>, int> slot_of, tslot_of, cslot_of;  // (monomial, epoch) -> slot
+    std::set<std::pair<uint32_t, int>> inl;                               // (monomial, epoch) with inline terms
+    uint32_t inl_used = 0;                                                // monomials with an accumulator
+};
+PhasePlan phase_plan(const Step &st)
+{
+    PhasePlan pp;
+    const size_t n = st.ops.size();
+    pp.uterms.assign(n, {});
+    pp.tterms.assign(n, {});
+    pp.cterms.assign(n, {});
+    int n_uni = 0, n_thr = 0;
+    for (const KOp &op : st.ops) { n_uni += uniform_acc(op); n_thr += thread_acc(op); }
+    const bool use_u = n_uni >= 8, use_t = n_thr >= 8;
+    int epoch[kAmpsPerThread] = {0};
+    uint32_t live = 0;
+    auto flush = [&](uint32_t F) {
+        F &= live;
+        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
+            if ((F >> S) & 1) epoch[S]++;
+        live &= ~F;
+    };
+    for (size_t o = 0; o < n; o++) {
+        const KOp &op = st.ops[o];
+        if (op.code == OPC_TRANS) { flush(~0u); continue; }
+        if (op.code == OPC_PHASE_FLUSH || op.code == OPC_DATA || op.code == OPC_PHASE) continue;
+        if (op.code == OPC_U4) { flush(touching((1u << op.k) | (1u << (int)op.cfg))); continue; }
+        if (op.code == OPC_PHASE_ACC) {
+            const bool u = use_u && uniform_acc(op), th = use_t && thread_acc(op), c = const_acc(op);
+            const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
+            for (uint32_t T = Z;; T = (T - 1) & Z) {
+                const uint32_t S = O | T;
+                const auto key = std::make_pair(S, epoch[S]);
+                if (u || th || c) {
+                    auto &of = u ? pp.slot_of : th ? pp.tslot_of : pp.cslot_of;
+                    auto &sv = u ? pp.slot_S : th ? pp.tslot_S : pp.cslot_S;
+                    auto it = of.find(key);
+                    if (it == of.end()) {
+                        it = of.emplace(key, (int)sv.size()).first;
+                        sv.push_back(S);
+                    }
+                    (u ? pp.uterms : th ? pp.tterms : pp.cterms)[o].push_back(
+                        {it->second, __builtin_popcount(T) & 1 ? -1 : 1});
+                } else {
+                    pp.inl.insert(key);
+                    pp.inl_used |= 1u << S;
+                }
+                live |= 1u << S;
+                if (!T) break;
+            }
+            continue;
+        }
+        flush(touching(1u << op.k));
+    }
+    return pp;
+}
+
 // Parameter block: out-of-tile predicates (mout, vout) deduplicated by value;
 // matrix rows of 8 doubles: a U2 takes a row, a U4 its row and its 3 OPC_DATA
 // rows; phases share rows (a multiplier takes 2 doubles, an accumulated
@@ -99,6 +191,7 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
             out_idx[o] = (int)k;
         }
         if (op.code == OPC_XS) continue;
+        if (const_acc(op)) continue;  // folded into a host-formed factor (phase_plan)
         if (op.code == OPC_PHASE_ACC) {
             if (acc_col >= 8) { acc_row = L.n_m++; acc_col = 0; }
             m_idx[o] = acc_row;
@@ -119,6 +212,11 @@ Layout layout_of(const Step &st, std::vector<int> &out_idx, std::vector<int> &m_
         } else {
             m_idx[o] = L.n_m++;
         }
+    }
+    {
+        const PhasePlan pp = phase_plan(st);
+        L.c_row = L.n_m;
+        L.n_m += ((int)pp.cslot_S.size() + 3) / 4;
     }
     L.n_out = (int)outs.size();
     L.off_m = L.off_out + 16 * (size_t)std::max(1, L.n_out);
@@ -300,112 +398,39 @@ JitPass jit_generate(const Step &st)
         }
         u4_heavy = w4 >= 2 * w2;
     }
-    // Phase runs (OPC_PHASE_ACC): per-thread integer angle accumulators, one
-    // per monomial S of the register bits (plan.h PhaseRunPlan), live across
-    // the whole pass.  Flushed lazily: an op on register bit k first flushes
-    // only the monomials containing k (the others commute with it); a
-    // re-layout and the store flush all.  The planner's OPC_PHASE_FLUSH marks
-    // are not needed here.
-    uint32_t acc_used = 0, live = 0;
-    for (const KOp &op : st.ops)
-        if (op.code == OPC_PHASE_ACC) {
-            const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
-            for (uint32_t T = Z;; T = (T - 1) & Z) {
-                acc_used |= 1u << (O | T);
-                if (!T) break;
-            }
-        }
-    if (acc_used) {
+    // Phase runs (OPC_PHASE_ACC), see PhasePlan: inline terms go to integer
+    // angle accumulators mo_S, one per monomial S of the register bits (plan.h
+    // PhaseRunPlan), flushed lazily; const / uniform / thread terms arrive as
+    // complex factors.
+    const PhasePlan pp = phase_plan(st);
+    uint32_t live = 0;
+    if (pp.inl_used) {
         s << " unsigned long long";
         bool first_decl = true;
         for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-            if ((acc_used >> S) & 1) { s << (first_decl ? " mo" : ", mo") << S << " = 0"; first_decl = false; }
+            if ((pp.inl_used >> S) & 1) { s << (first_decl ? " mo" : ", mo") << S << " = 0"; first_decl = false; }
         s << ";\n";
     }
-    auto touching = [](uint32_t bits) {  // monomials that contain one of the register bits
-        uint32_t F = 0;
-        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-            if (S & bits) F |= 1u << S;
-        return F;
-    };
-    // CTA-uniform phase terms: an OPC_PHASE_ACC whose predicate is on
-    // out-of-tile bits only (a QFT's controlled phases with the far qubits)
-    // adds the same angle in every thread of the CTA.  Rather than every warp
-    // evaluating all of them, the warps split them, sum per (monomial, flush
-    // epoch) slot, and reduce through shared memory once per tile; the flush
-    // of a monomial adds its slot in.  The epochs come from a dry run of the
-    // lazy-flush rules below.
-    const size_t o_first = 0;
-    auto uniform_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && op.mout && !op.mlane && !op.mwarp; };
-    // Per-thread phase terms (a predicate on lane/warp bits only) are the same
-    // for every tile: a companion kernel (qsim_pass_tab, one CTA, launched
-    // before the pass) sums them per (monomial, flush epoch) slot and thread
-    // into P.ttab, and the flush adds the thread's entry.
-    auto thread_acc = [](const KOp &op) { return op.code == OPC_PHASE_ACC && !op.mout && (op.mlane || op.mwarp); };
-    std::vector<std::vector<std::pair<int, int>>> uterms(st.ops.size()), tterms(st.ops.size());  // (slot, sign)
-    std::vector<uint32_t> slot_S, tslot_S;
-    std::map<std::pair<uint32_t, int>, int> slot_of, tslot_of;  // (monomial, flush epoch) -> slot
     int epoch[kAmpsPerThread] = {0};
-    {
-        int n_uni = 0, n_thr = 0;
-        for (const KOp &op : st.ops) { n_uni += uniform_acc(op); n_thr += thread_acc(op); }
-        const bool use_u = n_uni >= 8, use_t = n_thr >= 8;
-        if (use_u || use_t) {
-            uint32_t sim_live = 0;
-            auto sim_flush = [&](uint32_t F) {
-                F &= sim_live;
-                for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                    if ((F >> S) & 1) epoch[S]++;
-                sim_live &= ~F;
-            };
-            for (size_t o = o_first; o < st.ops.size(); o++) {
-                const KOp &op = st.ops[o];
-                if (op.code == OPC_TRANS) { sim_flush(~0u); continue; }
-                if (op.code == OPC_PHASE_FLUSH || op.code == OPC_DATA || op.code == OPC_PHASE) continue;
-                if (op.code == OPC_U4) { sim_flush(touching((1u << op.k) | (1u << (int)op.cfg))); continue; }
-                if (op.code == OPC_PHASE_ACC) {
-                    const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
-                    for (uint32_t T = Z;; T = (T - 1) & Z) {
-                        const uint32_t S = O | T;
-                        const bool u = use_u && uniform_acc(op), th = use_t && thread_acc(op);
-                        if (u || th) {
-                            auto &of = u ? slot_of : tslot_of;
-                            auto &sv = u ? slot_S : tslot_S;
-                            auto key = std::make_pair(S, epoch[S]);
-                            auto it = of.find(key);
-                            if (it == of.end()) {
-                                it = of.emplace(key, (int)sv.size()).first;
-                                sv.push_back(S);
-                            }
-                            (u ? uterms : tterms)[o].push_back({it->second, __builtin_popcount(T) & 1 ? -1 : 1});
-                        }
-                        sim_live |= 1u << S;
-                        if (!T) break;
-                    }
-                    continue;
-                }
-                sim_flush(touching(1u << op.k));
-            }
-            for (int &e : epoch) e = 0;
-        }
-    }
-    const int NS = (int)slot_S.size(), NW = kPassThreads / 32;
+    const int NS = (int)pp.slot_S.size(), NW = kPassThreads / 32;
     if (NS) {
-        s << " __shared__ unsigned long long uw[" << NW * NS << "], utot[" << NS << "];\n";
+        // CTA-uniform terms: the warps split the ops, sum per slot, reduce
+        // through shared memory once per tile; utc[k] = e^{i sum of slot k}
+        s << " __shared__ unsigned long long uw[" << NW * NS << "];\n __shared__ double2 utc[" << NS << "];\n";
         s << " {\n";
         for (int k = 0; k < NS; k++) s << "  unsigned long long u" << k << " = 0;\n";
         s << "  switch (warp) {\n";
         int next_w = 0;
         std::vector<std::vector<size_t>> by_warp(NW);
-        for (size_t o = o_first; o < st.ops.size(); o++)
-            if (!uterms[o].empty()) { by_warp[next_w].push_back(o); next_w = (next_w + 1) % NW; }
+        for (size_t o = 0; o < st.ops.size(); o++)
+            if (!pp.uterms[o].empty()) { by_warp[next_w].push_back(o); next_w = (next_w + 1) % NW; }
         for (int w = 0; w < NW; w++) {
             s << "  case " << w << ": {\n";
             for (size_t o : by_warp[w]) {
                 const std::string M = "P.m[" + std::to_string(m_idx[o]) + "]";
                 s << "   { const unsigned long long K = ((gcta & P.out[" << out_idx[o] << "][0]) == P.out[" << out_idx[o]
                   << "][1]) ? (unsigned long long)__double_as_longlong(" << M << "[" << m_col[o] << "]) : 0ULL;";
-                for (auto &t : uterms[o]) s << " u" << t.first << (t.second < 0 ? " -= K;" : " += K;");
+                for (auto &t : pp.uterms[o]) s << " u" << t.first << (t.second < 0 ? " -= K;" : " += K;");
                 s << " }\n";
             }
             s << "   break; }\n";
@@ -416,24 +441,54 @@ JitPass jit_generate(const Step &st)
         s << " for (int k = warp; k < " << NS << "; k += " << NW << ") {\n"
              "  unsigned long long v = lane < " << NW << " ? uw[lane * " << NS << " + k] : 0ULL;\n";
         for (int d = 1; d < NW; d <<= 1) s << "  v += __shfl_xor_sync(0xffffffffu, v, " << d << ");\n";
-        s << "  if (lane == 0) utot[k] = v;\n }\n __syncthreads();\n";
+        s << "  if (lane == 0) utc[k] = qexp(v, P.ptab);\n }\n __syncthreads();\n";
     }
+    auto cmul = [&](const std::string &a, const std::string &b, const std::string &out) {  // out = a * b
+        s << "  const double2 " << out << " = make_double2(fma(" << a << ".x, " << b << ".x, -" << a << ".y * " << b
+          << ".y), fma(" << a << ".x, " << b << ".y, " << a << ".y * " << b << ".x));\n";
+        fpc += 4;
+    };
     auto flush = [&](uint32_t F) {
         F &= live;
         if (!F) return;
         s << " { // flush monomials 0x" << std::hex << F << std::dec << "\n";
+        // factor f_S of every flushed monomial: the product of its parts
         for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++) {
             if (!((F >> S) & 1)) continue;
-            auto it = slot_of.find(std::make_pair(S, epoch[S]));
-            if (it != slot_of.end()) s << "  mo" << S << " += utot[" << it->second << "];\n";
-            auto jt = tslot_of.find(std::make_pair(S, epoch[S]));
-            if (jt != tslot_of.end())
-                s << "  mo" << S << " += __ldg(P.ttab + " << jt->second * kPassThreads << " + threadIdx.x);\n";
+            const auto key = std::make_pair(S, epoch[S]);
+            std::vector<std::string> parts;
+            if (pp.inl.count(key)) {
+                s << "  const double2 ei" << S << " = qexp(mo" << S << ", P.ptab); mo" << S << " = 0;\n";
+                fpc += kQexpOps;
+                parts.push_back("ei" + std::to_string(S));
+            }
+            auto ct = pp.cslot_of.find(key);
+            if (ct != pp.cslot_of.end()) {
+                const int k = ct->second, row = L.c_row + k / 4, col = 2 * (k % 4);
+                s << "  const double2 ec" << S << " = make_double2(P.m[" << row << "][" << col << "], P.m[" << row << "]["
+                  << col + 1 << "]);\n";
+                parts.push_back("ec" + std::to_string(S));
+            }
+            auto it = pp.slot_of.find(key);
+            if (it != pp.slot_of.end()) parts.push_back("utc[" + std::to_string(it->second) + "]");
+            auto jt = pp.tslot_of.find(key);
+            if (jt != pp.tslot_of.end()) {
+                s << "  const double2 et" << S << " = __ldg(reinterpret_cast<const double2 *>(P.ttab) + "
+                  << jt->second * kPassThreads << " + threadIdx.x);\n";
+                parts.push_back("et" + std::to_string(S));
+            }
+            std::string f = parts.empty() ? std::string("make_double2(1.0, 0.0)") : parts[0];
+            for (size_t q = 1; q < parts.size(); q++) {
+                const std::string nf = "f" + std::to_string(S) + "_" + std::to_string(q);
+                cmul(f, parts[q], nf);
+                f = nf;
+            }
+            s << "  const double2 em" << S << " = " << f << ";\n";
             epoch[S]++;
         }
-        // e^{i theta_i}, theta_i = sum of acc[S] over S in F, S subset of i: per
-        // distinct register angle (A) or per monomial (B), the cheaper
-        const double kExp = 20, kMul = 4;
+        // apply: per monomial (B: every amplitude times each of its factors)
+        // or per distinct register key (A: the product of the key's factors
+        // once, then one multiply per amplitude), the cheaper
         auto key_of = [&](uint32_t i) {
             uint32_t key = 0;
             for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
@@ -442,54 +497,61 @@ JitPass jit_generate(const Step &st)
         };
         std::vector<uint32_t> keys;
         int nregs = 0;
+        double costA = 0, costB = 0;
         for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++) {
             const uint32_t key = key_of(i);
             if (!key) continue;
             nregs++;
-            if (std::find(keys.begin(), keys.end(), key) == keys.end()) keys.push_back(key);
+            costB += 4 * __builtin_popcount(key);
+            if (std::find(keys.begin(), keys.end(), key) == keys.end()) {
+                keys.push_back(key);
+                costA += 4 * (__builtin_popcount(key) - 1);
+            }
         }
-        const double costA = keys.size() * kExp + nregs * kMul;
-        double costB = 0;
-        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-            if ((F >> S) & 1) costB += kExp + kMul * (double)(kAmpsPerThread >> __builtin_popcount(S));
+        costA += 4 * nregs;
         auto mul = [&](const std::string &e, const std::string &v) {
             s << "  { const double p1 = -" << e << ".y * " << v << ".y, p2 = " << e << ".y * " << v << ".x; " << v
               << ".x = fma(" << e << ".x, " << v << ".x, p1); " << v << ".y = fma(" << e << ".x, " << v
               << ".y, p2); }\n";
+            fpc += 4;
         };
-        if (costB >= costA) {
+        if (costA < costB) {
             std::vector<char> emitted(keys.size(), 0);
             for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++) {
                 const uint32_t key = key_of(i);
                 if (!key) continue;
                 const size_t k = std::find(keys.begin(), keys.end(), key) - keys.begin();
+                const std::string ek = "ek" + std::to_string(k);
                 if (!emitted[k]) {
-                    std::string e;
-                    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                        if ((key >> S) & 1) e += (e.empty() ? "mo" : " + mo") + std::to_string(S);
-                    s << "  const double2 ex" << k << " = qexp(" << e << ", P.ptab);\n";
+                    std::string f;
+                    int q = 0;
+                    for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++) {
+                        if (!((key >> S) & 1)) continue;
+                        const std::string e = "em" + std::to_string(S);
+                        if (f.empty()) f = e;
+                        else {
+                            const std::string nf = ek + "_" + std::to_string(q++);
+                            cmul(f, e, nf);
+                            f = nf;
+                        }
+                    }
+                    s << "  const double2 " << ek << " = " << f << ";\n";
                     emitted[k] = 1;
-                    fpc += kQexpOps;
                 }
-                mul("ex" + std::to_string(k), A(i));
-                fpc += 4;
+                mul(ek, A(i));
             }
         } else {
-            for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                if ((F >> S) & 1) { s << "  const double2 em" << S << " = qexp(mo" << S << ", P.ptab);\n"; fpc += kQexpOps; }
             for (uint32_t i = 0; i < (uint32_t)kAmpsPerThread; i++)
                 for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-                    if (((F >> S) & 1) && (S & i) == S) { mul("em" + std::to_string(S), A(i)); fpc += 4; }
+                    if (((F >> S) & 1) && (S & i) == S) mul("em" + std::to_string(S), A(i));
         }
-        for (uint32_t S = 0; S < (uint32_t)kAmpsPerThread; S++)
-            if ((F >> S) & 1) s << "  mo" << S << " = 0;\n";
         s << " }\n";
         live &= ~F;
     };
     int n_had = 0;
     for (const KOp &op : st.ops) n_had += jit_hadamard(op);
     if (n_had) s << " double hs = 1.0;  // product of the Hadamard-form scales applied so far\n";
-    for (size_t o = o_first; o < st.ops.size(); o++) {
+    for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];
         if (op.code == OPC_TRANS) {
             flush(live);
@@ -620,7 +682,7 @@ JitPass jit_generate(const Step &st)
             continue;
         }
         materialize(op.mreg | (is_phase ? 0u : 1u << op.k));
-        if (!uterms[o].empty() || !tterms[o].empty()) {  // summed per slot elsewhere, added at the flush
+        if (!pp.uterms[o].empty() || !pp.tterms[o].empty() || !pp.cterms[o].empty()) {  // a factor at the flush
             const uint32_t O = op.mreg & op.vreg, Z = op.mreg & ~op.vreg;
             for (uint32_t T = Z;; T = (T - 1) & Z) {
                 live |= 1u << (O | T);
@@ -771,7 +833,7 @@ JitPass jit_generate(const Step &st)
     // register allocation); P.desync = SM count << 32 | ns, 0 = off.
     s << " { const unsigned long long d = P.desync; __nanosleep(blockIdx.x < (unsigned)(d >> 32) ? (unsigned)d : 0u); }\n";
     s << "}\n";
-    const int NTS = (int)tslot_S.size();
+    const int NTS = (int)pp.tslot_S.size();
     if (NTS) {
         // companion kernel: the per-thread phase slots, once per launch (not per tile)
         s << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads
@@ -779,16 +841,19 @@ JitPass jit_generate(const Step &st)
              " const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
         for (int k = 0; k < NTS; k++) s << " unsigned long long t" << k << " = 0;\n";
         for (size_t o = 0; o < st.ops.size(); o++) {
-            if (tterms[o].empty()) continue;
+            if (pp.tterms[o].empty()) continue;
             const KOp &op = st.ops[o];
             s << " { const unsigned long long K = (true";
             if (op.mlane) s << " && ((lane & " << op.mlane << ") == " << op.vlane << ")";
             if (op.mwarp) s << " && ((warp & " << op.mwarp << ") == " << op.vwarp << ")";
             s << ") ? (unsigned long long)__double_as_longlong(P.m[" << m_idx[o] << "][" << m_col[o] << "]) : 0ULL;";
-            for (auto &t : tterms[o]) s << " t" << t.first << (t.second < 0 ? " -= K;" : " += K;");
+            for (auto &t : pp.tterms[o]) s << " t" << t.first << (t.second < 0 ? " -= K;" : " += K;");
             s << " }\n";
         }
-        for (int k = 0; k < NTS; k++) s << " P.ttab[" << k * kPassThreads << " + threadIdx.x] = t" << k << ";\n";
+        // e^{i sum} per slot and thread (2 u64 per entry)
+        for (int k = 0; k < NTS; k++)
+            s << " reinterpret_cast<double2 *>(P.ttab)[" << k * kPassThreads << " + threadIdx.x] = qexp(t" << k
+              << ", P.ptab);\n";
         s << "}\n";
     }
     JitPass jp;
@@ -823,6 +888,20 @@ void jit_pack_params(const Step &st, void *state, uint64_t rank_bits, std::vecto
         std::memcpy(b + kOffTs + 4 * t, &st.pass.tile_sorted[t], 4);
         const uint64_t mo = 1ULL << st.pass.tp_out[t];
         std::memcpy(b + kOffTpo + 8 * t, &mo, 8);
+    }
+    {
+        // const phase terms: e^{2 pi i c / 2^64} per (monomial, epoch) slot, c
+        // the wrapped sum of the slot's unpredicated angles (phase_plan)
+        const PhasePlan pp = phase_plan(st);
+        std::vector<uint64_t> acc(pp.cslot_S.size(), 0);
+        for (size_t o = 0; o < st.ops.size(); o++)
+            for (auto &t : pp.cterms[o]) acc[t.first] += t.second < 0 ? (uint64_t)0 - st.ops[o].cfg : st.ops[o].cfg;
+        for (size_t k = 0; k < acc.size(); k++) {
+            const long double turns = (long double)(int64_t)acc[k] / 18446744073709551616.0L;  // in [-1/2, 1/2)
+            const long double a = 2.0L * 3.141592653589793238462643383279502884L * turns;
+            const double f[2] = {(double)cosl(a), (double)sinl(a)};
+            std::memcpy(b + L.off_m + 64 * (L.c_row + k / 4) + 16 * (k % 4), f, 16);
+        }
     }
     for (size_t o = 0; o < st.ops.size(); o++) {
         const KOp &op = st.ops[o];

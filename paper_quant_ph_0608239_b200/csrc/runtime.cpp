@@ -73,7 +73,7 @@ struct qsim_ctx_s {
     bool plan_cache = true;
     // device program buffers (d_ops: interpreter programs longer than its parameter block)
     KOp *d_ops = nullptr;
-    unsigned long long *d_ttab = nullptr;  // per-thread phase slots of the current JIT pass (qsim_pass_tab)
+    unsigned long long *d_ttab = nullptr;  // per-thread phase factors (double2) of the current JIT pass (qsim_pass_tab)
     size_t d_ttab_cap = 0;
     size_t d_ops_cap = 0;
     uint32_t *d_perm = nullptr;
@@ -756,7 +756,7 @@ static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t count
     CUfunction tabfn = jit_cache().find_tab(pc.jkeys[si], nts);
     if (!fn) FAIL(c, QSIM_ERR_STATE, "jit pass kernel missing");
     qsim_status st;
-    if (tabfn && (st = ensure_dev(c, c->d_ttab, c->d_ttab_cap, (size_t)nts * kPassThreads)) != QSIM_OK) return st;
+    if (tabfn && (st = ensure_dev(c, c->d_ttab, c->d_ttab_cap, (size_t)2 * nts * kPassThreads)) != QSIM_OK) return st;
     const uint64_t rb = (uint64_t)local_ranks(c, i) << c->M;
     auto &pp = pc.params[si];
     if (pp.size() != (size_t)n_local(c)) pp.assign(n_local(c), {});
