@@ -161,6 +161,37 @@ def pass_roofline(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float)
     return 1e3 * t, slots
 
 
+# shared-memory bandwidth of a re-layout (16 STS.128 + 16 LDS.128 per thread,
+# 2 CTAs/SM) measured by tools/relayout_bench.cu on a B200:
+# profiles/r2_relayout_bench.jsonl (0.92 of 128 B/clk/SM at 1965 MHz)
+SMEM_RELAYOUT_GBS = 34.5e3
+
+
+def pass_serial_bound(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float):
+    """Per-pass bound that counts the shared-memory re-layouts: a re-layout
+    moves the whole tile through shared memory (32 B/amp: write + read)
+    between barriers, and measured (tools/relayout_bench.cu) it does not hide
+    under the FP64 work of the co-resident CTA, so each pass needs
+    max(FP64 + re-layout time, HBM time) with the generated code's executed
+    FP64 instructions.  Returns (ms per step, re-layouts per step)."""
+    from paper_quant_ph_0608239_b200 import plan_json
+    G = (world - 1).bit_length()
+    amps = float(1 << (n - G))
+    d = json.loads(plan_json(n, world, gates, key_check=True))
+    fps = d["jit"]["fp64_per_amp"]
+    passes = [st for st in d["plan"]["steps"] if st["type"] == "pass"]
+    if len(fps) != len(passes):
+        return None, None
+    t = 0.0
+    nr = 0
+    for st, fp in zip(passes, fps):
+        r = sum(1 for op in st["ops"] if op["code"] == 4)
+        nr += r
+        t += max(2.0 * fp * amps / (fp64_tflops * 1e12) + r * 32.0 * amps / (SMEM_RELAYOUT_GBS * 1e9),
+                 32.0 * amps / (hbm_gbs * 1e9))
+    return 1e3 * t, nr
+
+
 def sigma_gate_flop_per_amp(gates) -> float:
     """SURVEY §8(d) algorithmic FP64 flops per amplitude of the unfused gate
     list: a general (complex) 2x2 costs 14 per touched amplitude, an exact
@@ -467,6 +498,7 @@ def run_ours(args):
     fp64_ach = (2.0 * st["pass_fp64_slots"] / (pass_ms / 1e3) / 1e12) if pass_ms > 0 else None
     hbm_ach = (st["pass_amp_bytes"] / (pass_ms / 1e3) / 1e9) if pass_ms > 0 else None
     t_min_ms, _ = pass_roofline(n, world, gates, fp64_peak, hbm_peak)
+    t_ser_ms, relayouts = pass_serial_bound(n, world, gates, fp64_peak, hbm_peak)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tp):
@@ -511,6 +543,13 @@ def run_ours(args):
                          # per-launch bound max(FP64, HBM) summed over the passes of a step
                          "per_pass_bound": {"t_min_ms_per_step": t_min_ms,
                                             "frac": (t_min_ms * rf_steps / pass_ms) if pass_ms > 0 else None},
+                         # the same with the shared-memory re-layouts in series with the FP64 work
+                         "fp64_plus_relayout_bound": {
+                             "t_min_ms_per_step": t_ser_ms, "relayouts_per_step": relayouts,
+                             "smem_gbs": SMEM_RELAYOUT_GBS,
+                             "smem_source": "measured re-layout bandwidth, tools/relayout_bench.cu "
+                                            "(profiles/r2_relayout_bench.jsonl)",
+                             "frac": (t_ser_ms * rf_steps / pass_ms) if (pass_ms > 0 and t_ser_ms) else None},
                          "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": (hbm_ach / hbm_peak) if hbm_ach else None, "peak_source": pk["hbm_src"],
                                  "bytes_per_launch": 32 << (n - G)}},

@@ -27,7 +27,8 @@ def summary(rep):
 
 for src, dst in (("bench.json", "bench.json"), ("launches.csv", "bench_launches.csv"),
                  ("configs.jsonl", "configs.jsonl"), ("paper.jsonl", "paper_benchmarks.jsonl"),
-                 ("sweep30.jsonl", "position_sweep_30q.jsonl"), ("bench_reference.json", "bench_reference.json")):
+                 ("sweep30.jsonl", "position_sweep_30q.jsonl"), ("bench_reference.json", "bench_reference.json"),
+                 ("relayout_bench.jsonl", "relayout_bench.jsonl"), ("gran_bench.jsonl", "tile_granularity_30q.jsonl")):
     if os.path.exists(os.path.join(G, src)) and os.path.getsize(os.path.join(G, src)):
         shutil.copy(os.path.join(G, src), os.path.join(P, f"{r}_{dst}"))
 for rep, dst in (("prof_pass.ncu-rep", "pass_c2.txt"), ("prof_qft.ncu-rep", "pass_qft.txt"),

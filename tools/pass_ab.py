@@ -19,6 +19,8 @@ elif wl.startswith("chain"):  # config-5 family at n qubits, e.g. chain28
     w = C.Workload("chain", n, 0, C.random_chain(n, 10, seed=5, sweep=True), {})
 elif wl.startswith("qft"):
     w = C.qft_basis(int(wl[3:]), 12345)
+elif wl.startswith("hall"):  # H on all n qubits (the paper's scaling test)
+    w = C.h_on_all(int(wl[4:]))
 elif wl == "shor":  # config 3 (28 q)
     w = C.config3_shor()
 else:

@@ -26,3 +26,7 @@ python tools/bench_paper.py > gpurun_out/paper.jsonl 2> gpurun_out/paper.err; ec
 python tools/sweep.py 30 > gpurun_out/sweep30.jsonl 2>&1; echo "sweep=$?"
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
 echo "reference=$?"
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/relayout_bench tools/relayout_bench.cu && \
+/tmp/relayout_bench > gpurun_out/relayout_bench.jsonl 2>&1; echo "relayout_bench=$?"
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/gran_bench tools/gran_bench.cu && \
+/tmp/gran_bench 30 > gpurun_out/gran_bench.jsonl 2>&1; echo "gran_bench=$?"

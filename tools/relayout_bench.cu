@@ -3,7 +3,15 @@
 // threads x 16 amplitudes in registers; per round two 3M 4x4 blocks (13 FP64
 // instructions per amplitude each, matrices as kernel-parameter constants)
 // and one re-layout (16 STS.128, barrier, 16 LDS.128, barrier).  Variants:
-// compute only, re-layout only, both; 2 CTAs/SM (as qsim_pass) or 1.
+// compute only, re-layout only, both; 2 CTAs/SM (as qsim_pass) or 1; 64- and
+// 32-bit shared-memory accesses; a first-wave phase offset (desync); warp-
+// specialised (half the warps compute, half move shared memory); warp-local
+// re-layouts without CTA barriers; two tiles per 512-thread CTA with and
+// without a ping-pong turn on the FP64 pipe (named barriers); shuffle
+// exchanges; one wave in phase / with the slot-1 CTAs in anti-phase.
+// Finding: compute alone runs at the DFMA peak and a re-
+// layout alone at ~0.9 of 128 B/clk/SM, but barrier-synchronised re-layouts
+// and FP64 work of the same or the co-resident CTA mostly serialise.
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o relayout_bench relayout_bench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -112,6 +120,25 @@ __global__ void __launch_bounds__(256, MINB) k_body(double2 *out, int rounds, un
                 got.x = __shfl_xor_sync(0xffffffffu, send.x, lb);
                 got.y = __shfl_xor_sync(0xffffffffu, send.y, lb);
                 if (hi) lo_r = got; else hi_r = got;
+            }
+        }
+    } else if (MODE == 13 || MODE == 14) {  // one wave; 14: slot-1 CTAs start with the re-layout (anti-phase)
+        const bool rot = MODE == 14 && ((blockIdx.x / 148) & 1);
+#pragma unroll
+        for (int r = 0; r < kRounds; r++) {
+            if (!rot) {
+                u4<0, 1>(a, P.m[2 * r]);
+                u4<2, 3>(a, P.m[2 * r + 1]);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i++) sm[i * 256 + t] = a[i];
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 16; i++) a[i] = sm[i * 256 + ((t + 17 * i + r) & 255)];
+            __syncthreads();
+            if (rot) {
+                u4<0, 1>(a, P.m[2 * r]);
+                u4<2, 3>(a, P.m[2 * r + 1]);
             }
         }
     } else if (MODE == 4) {  // warp-specialised: warps 0-3 compute, 4-7 move shared memory (no CTA barriers)
@@ -275,6 +302,17 @@ int main()
     rep("relayout 32-bit, 2 CTA/SM", run<9, 2>(out, grid2, rounds, 0, sm64, P));
     rep("relayout 64-bit, 1 CTA/SM", run<8, 1>(out, grid2, rounds, 0, sm120, P));
     rep("both 64-bit, 2 CTA/SM", run<10, 2>(out, grid2, rounds, 0, sm64, P));
+    {
+        // one wave (2 CTAs per SM), 16x the work per CTA via repeated launches is not the same; use grid = 296
+        const double f = 296.0 / grid2;
+        auto rep1 = [&](const char *name, float ms) {
+            printf("{\"variant\": \"%s\", \"ms\": %.4f, \"fp64_tflops\": %.2f}\n", name, ms, 2 * fp64 * f / (ms * 1e-3) / 1e12);
+        };
+        rep1("one wave: compute only", run<1, 2>(out, 296, rounds, 0, sm64, P));
+        rep1("one wave: relayout only", run<2, 2>(out, 296, rounds, 0, sm64, P));
+        rep1("one wave: both, in phase", run<13, 2>(out, 296, rounds, 0, sm64, P));
+        rep1("one wave: both, slot 1 anti-phase", run<14, 2>(out, 296, rounds, 0, sm64, P));
+    }
     rep("shuffle exchange (half the registers), 2 CTA/SM", run<11, 2>(out, grid2, rounds, 0, sm64, P));
     rep("compute + shuffle exchange, 2 CTA/SM", run<12, 2>(out, grid2, rounds, 0, sm64, P));
     rep("warp-specialised half compute / half smem, 2 CTA/SM", run<4, 2>(out, grid2, rounds, 0, sm64, P));
