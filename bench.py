@@ -163,8 +163,8 @@ def pass_roofline(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float)
 
 # shared-memory bandwidth of a re-layout (16 STS.128 + 16 LDS.128 per thread,
 # 2 CTAs/SM) measured by tools/relayout_bench.cu on a B200:
-# profiles/r2_relayout_bench.jsonl (0.92 of 128 B/clk/SM at 1965 MHz)
-SMEM_RELAYOUT_GBS = 34.5e3
+# profiles/r2_relayout_bench.jsonl (0.88 of 128 B/clk/SM at 1965 MHz)
+SMEM_RELAYOUT_GBS = 32.9e3
 
 
 def pass_serial_bound(n: int, world: int, gates, fp64_tflops: float, hbm_gbs: float):
