@@ -3,6 +3,7 @@
 // shards / NCCL), reductions, sampling and readout.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -303,6 +304,10 @@ static cudaEvent_t ev_get(qsim_ctx c)
     return e;
 }
 
+// NVTX ranges (header-only NVTX3: a no-op unless a tool such as Nsight
+// Systems injects itself) name every engine phase on the host timeline.
+static const char *const kRangeName[] = {"qsim pass", "qsim generic gate", "qsim permutation",
+                                         "qsim exchange", "qsim readout", "qsim overlapped pass+exchange"};
 struct RangeGuard {
     qsim_ctx c;
     int cat;
@@ -310,6 +315,7 @@ struct RangeGuard {
     cudaEvent_t a = nullptr;
     RangeGuard(qsim_ctx c_, int cat_, uint64_t bytes_) : c(c_), cat(cat_), bytes(bytes_)
     {
+        nvtxRangePushA(kRangeName[cat]);
         if (c->timing) {
             a = ev_get(c);
             cudaEventRecord(a, c->stream);
@@ -322,6 +328,7 @@ struct RangeGuard {
             cudaEventRecord(b, c->stream);
             c->ranges.push_back({a, b, cat, bytes});
         }
+        nvtxRangePop();
     }
 };
 
@@ -1099,7 +1106,16 @@ static qsim_status probe_spmd_rates(qsim_ctx c)
     return QSIM_OK;
 }
 
+static qsim_status flush_impl(qsim_ctx c);
 static qsim_status flush(qsim_ctx c)
+{
+    nvtxRangePushA("qsim flush (plan + launch)");
+    const qsim_status st = flush_impl(c);
+    nvtxRangePop();
+    return st;
+}
+
+static qsim_status flush_impl(qsim_ctx c)
 {
     if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
     if (!c->init_pending && c->queue.empty()) return QSIM_OK;

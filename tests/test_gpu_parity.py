@@ -342,6 +342,50 @@ def test_config3_full(P, oracle_mod):
     assert ok.sum() > 1900 and np.array_equal(shots[ok], ref[ok])
 
 
+def phase_kinds_circuit(n, seed):
+    """Long runs of diagonal phases whose terms take every form the JIT phase
+    runs have (jit.cpp PhasePlan): unpredicated R (host-formed factors),
+    controlled phases with far controls (CTA-uniform slots), with controls on
+    lane/warp-range qubits (per-thread slots), mixed and sparse ones
+    (accumulators), split into several flush epochs by interleaved H gates."""
+    r = np.random.default_rng(seed)
+    gates = [G.one_q(q, G.H) for q in range(n)]
+    for rnd in range(6):
+        for _ in range(3 * n):
+            kind = r.integers(4)
+            q = int(r.integers(n))
+            phi = float(r.uniform(-math.pi, math.pi))
+            if kind == 0:
+                gates.append(G.one_q(q, G.R(phi)))
+            elif kind == 1:
+                c = int(r.integers(n))
+                if c != q:
+                    gates.append(G.cphase(c, q, phi))
+            elif kind == 2:
+                a, b = (int(x) for x in r.choice(n, 2, replace=False))
+                if q not in (a, b):
+                    gates.append(G.ctrl([a, b], q, G.R(phi)))
+            else:
+                c = n - 1 - int(r.integers(3))
+                if c != q:
+                    gates.append(G.cphase(c, q, phi))
+        for q in r.choice(n, 3, replace=False):
+            gates.append(G.one_q(int(q), G.H if rnd % 2 else G.haar_u2(G.SplitMix64(seed + rnd))))
+    return gates
+
+
+@pytest.mark.parametrize("n,ranks", [(14, 1), (18, 1), (21, 1), (18, 4)])
+def test_phase_run_factor_kinds(P, oracle_mod, n, ranks):
+    """Phase runs with host-formed, per-tile, per-launch and accumulated
+    factors in the same passes vs the oracle (and the interpreter tier)."""
+    gates = phase_kinds_circuit(n, 100 + n)
+    o = oracle_run(oracle_mod, n, 5, gates)
+    for jit in (1, 0):
+        sim = gpu_run(P, n, 5, gates, ranks=ranks, jit=jit)
+        assert_parity(sim, o, n)
+        sim.close()
+
+
 @pytest.mark.parametrize("ranks", [1, 2, 4, 8])
 def test_qft_closed_form(P, ranks):
     n, x0 = 20, 0xABCDE
