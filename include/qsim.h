@@ -249,7 +249,10 @@ qsim_status qsim_get_layout(qsim_ctx ctx, int *phys_of_qubit);
  * transfer is device copy work on the same HBM; 0 = in sequence), "desync_ns"
  * (pass kernels: the first-wave CTAs of SM slot 0 finish this many ns late so
  * that the two CTAs an SM runs stay out of step -- one re-layouts through
- * shared memory while the other computes; default 1500, 0 = off). */
+ * shared memory while the other computes; default 1500, 0 = off),
+ * "fuse_readout" (1 = qsim_expectations runs the last pass of its flush as a
+ * readout variant that also sums |a|^2 per tile bit, so <Q_i> needs no second
+ * read of the state [default]; 0 = separate reduction kernels). */
 qsim_status qsim_set_option(qsim_ctx ctx, const char *key, int64_t value);
 
 typedef struct {
@@ -280,6 +283,8 @@ typedef struct {
     double overlap_ms;         /* event time of the overlapped pairs (timing=1; not in pass_ms/exchange_ms) */
     double link_gbs;           /* SPMD: partner-link rate per direction measured at creation, minimum over
                                   the ranks (the planner's link rate); 0 = not measured */
+    uint64_t fused_readouts;   /* qsim_expectations calls served by the readout variant of the last pass
+                                  (option "fuse_readout"): no separate read of the state */
 } qsim_stats;
 
 qsim_status qsim_get_stats(qsim_ctx ctx, qsim_stats *out);
@@ -308,8 +313,9 @@ const char *qsim_last_error(qsim_ctx ctx);
  * (0 = default 6); bits 17-19 = candidate gate list + 1 to plan alone
  * (0 = all, costed; each candidate's modelled time is reported under
  * "candidates"); bit 20 = cost the plan for a transport that overlaps a pass
- * with the exchange after it (the runtime's "overlap" on NCCL/loopback).  Returns
- * QSIM_ERR_ARG if buf is too small. */
+ * with the exchange after it (the runtime's "overlap" on NCCL/loopback); bit 21
+ * = with bits 0-1 = 2 or bit 10, also generate / compile every pass's readout
+ * variant (option "fuse_readout").  Returns QSIM_ERR_ARG if buf is too small. */
 qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, size_t n_gates,
                            int flags, char *buf, size_t buf_bytes);
 

@@ -48,7 +48,8 @@ class qsim_stats(ctypes.Structure):
                                                             ("streamed_steps", ctypes.c_uint64),
                                                             ("overlapped", ctypes.c_uint64),
                                                             ("overlap_ms", ctypes.c_double),
-                                                            ("link_gbs", ctypes.c_double)]
+                                                            ("link_gbs", ctypes.c_double),
+                                                            ("fused_readouts", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

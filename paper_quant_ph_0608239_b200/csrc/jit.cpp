@@ -36,7 +36,8 @@ int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
 // parameter block layout (the JP struct of the generated source)
 constexpr int kMaxFix = 4;  // instance bits a launch may fix (jit_set_block)
-constexpr size_t kOffInit = 32, kOffTtab = 40, kOffFix = 48, kOffTpm = 56, kOffTs = kOffTpm + 8 * kTileBits;
+constexpr size_t kOffInit = 32, kOffTtab = 40, kOffFix = 48, kOffRed = 56, kOffTpm = 64,
+                 kOffTs = kOffTpm + 8 * kTileBits;
 // 16-B aligned (the matrix rows that follow are read as 128-bit constants)
 constexpr size_t kOffTpo = (kOffTs + 4 * (kTileBits + kMaxFix) + 15) / 16 * 16;
 constexpr int kTsPad = (int)(kOffTpo - kOffTs) / 4 - (kTileBits + kMaxFix);  // ints of padding after ts
@@ -258,6 +259,7 @@ JitPass jit_generate(const Step &st)
     s << "// minb=" << minb << "\n";
     s << "struct __align__(16) JP { double2 *st; unsigned long long rank_bits; unsigned long long desync; "
          "const double2 *ptab; unsigned long long init_phys; unsigned long long *ttab; unsigned long long fixbits; "
+         "double *red; "
          "unsigned long long tpm[" << kTileBits << "]; int ts[" << kTileBits + kMaxFix << "]; "
       << (kTsPad ? "int ts_pad[" + std::to_string(kTsPad) + "]; " : std::string())
       << "unsigned long long tpo[" << kTileBits << "]; "
@@ -812,6 +814,58 @@ JitPass jit_generate(const Step &st)
         fpc += 2 * kAmpsPerThread;
     }
     materialize(1);  // register bit 0 lies inside one 256-bit store
+    if (st.jit_readout) {
+        // <Q_i> fused into the pass: per tile bit t the sum of |a|^2 over the
+        // tile's amplitudes with bit t set, and the tile total (index 12),
+        // in a fixed order (deterministic).  Register bit j holds tile bit
+        // nib(cur, j), except that a pending flip of bit j (stored with the
+        // slot address XORed, see Flip) exchanges its 0 and 1 halves.
+        const int NWR = kPassThreads / 32;
+        s << " {\n  __shared__ double rsum[" << NWR * (kTileBits + 1) << "];\n";
+        for (int i = 0; i < kAmpsPerThread; i++)
+            s << "  const double rp" << i << " = fma(" << A(i) << ".x, " << A(i) << ".x, " << A(i) << ".y * " << A(i)
+              << ".y);\n";
+        // fixed-order tree sums over a register subset
+        auto tree = [&](std::vector<int> idx) {
+            std::vector<std::string> t;
+            for (int i : idx) t.push_back("rp" + std::to_string(i));
+            while (t.size() > 1) {
+                std::vector<std::string> u;
+                for (size_t k = 0; k + 1 < t.size(); k += 2) u.push_back("(" + t[k] + " + " + t[k + 1] + ")");
+                if (t.size() & 1) u.push_back(t.back());
+                t.swap(u);
+            }
+            return t.empty() ? std::string("0.0") : t[0];
+        };
+        std::vector<int> all;
+        for (int i = 0; i < kAmpsPerThread; i++) all.push_back(i);
+        s << "  const double rtot = " << tree(all) << ";\n";
+        std::vector<std::string> val(kTileBits);
+        for (int j = 0; j < kRegBits; j++) {
+            std::vector<int> one, zero;
+            for (int i = 0; i < kAmpsPerThread; i++) ((i >> j) & 1 ? one : zero).push_back(i);
+            std::string fp = "false";
+            for (const Flip &f : flips)
+                if (f.k == j) fp = "(" + fp + ") != (" + f.pred + ")";
+            s << "  const double rb" << j << " = (" << fp << ") ? " << tree(zero) << " : " << tree(one) << ";\n";
+            val[nib(cur, j)] = "rb" + std::to_string(j);
+        }
+        for (int j = 0; j < 5; j++) val[nib(cur, kLaneNib + j)] = "(((lane >> " + std::to_string(j) + ") & 1) ? rtot : 0.0)";
+        for (int j = 0; j < kWarpBits; j++)
+            val[nib(cur, kWarpNib + j)] = "(((warp >> " + std::to_string(j) + ") & 1) ? rtot : 0.0)";
+        val.push_back("rtot");
+        for (int t = 0; t <= kTileBits; t++) {
+            s << "  { double v = " << val[t] << ";";
+            for (int d = 16; d > 0; d >>= 1) s << " v += __shfl_xor_sync(0xffffffffu, v, " << d << ");";
+            s << " if (lane == 0) rsum[warp * " << kTileBits + 1 << " + " << t << "] = v; }\n";
+        }
+        s << "  __syncthreads();\n  if (threadIdx.x < " << kTileBits + 1 << ") { double v = rsum[threadIdx.x];";
+        s << " for (int w = 1; w < " << NWR << "; w++) v += rsum[w * " << kTileBits + 1 << " + threadIdx.x];";
+        s << " P.red[(unsigned long long)blockIdx.x * " << kTileBits + 1 << " + threadIdx.x] = v; }\n }\n";
+        // |a|^2, the total, both halves per register bit, the warp butterflies
+        fpc += 2.0 * kAmpsPerThread + (kAmpsPerThread - 1) + kRegBits * 2 * (kAmpsPerThread / 2 - 1) +
+               (kTileBits + 1) * 5;
+    }
     s << " {\n  double2 *p = P.st + base + (" << gaddr(cur, "TPO") << ");\n";
     {
         const uint64_t cfs = cur;
@@ -941,6 +995,11 @@ bool jit_set_block(std::vector<uint8_t> &buf, const Step &st, const int *pos, in
     std::memcpy(buf.data() + kOffTs, ts.data(), 4 * ts.size());
     std::memcpy(buf.data() + kOffFix, &fixbits, 8);
     return true;
+}
+
+void jit_set_red(std::vector<uint8_t> &buf, double *red)
+{
+    if (buf.size() >= kOffRed + 8) std::memcpy(buf.data() + kOffRed, &red, 8);
 }
 
 void jit_set_desync(std::vector<uint8_t> &buf, uint32_t n_sm, uint32_t ns)
@@ -1137,6 +1196,7 @@ std::string jit_key(const Step &st)
     auto put = [&](uint64_t v) { k.append(reinterpret_cast<const char *>(&v), 8); };
     put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) |
         ((uint64_t)(st.pass.fresh != 0) << 48) | ((uint64_t)(st.jit_block != 0) << 49) |
+        ((uint64_t)(st.jit_readout != 0) << 50) |
         ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
     put(st.pass.cfg0);
     {

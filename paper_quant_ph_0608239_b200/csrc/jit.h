@@ -53,6 +53,8 @@ void jit_set_init(std::vector<uint8_t> &buf, uint64_t init_phys);
 // enumerates the other non-tile bits; 2^(M - 12 - K) instances); K = 0
 // undoes it.  false if K is too large.
 bool jit_set_block(std::vector<uint8_t> &buf, const Step &st, const int *pos, int K, uint64_t fixbits);
+// readout variant (Step::jit_readout): where the per-tile bit sums go
+void jit_set_red(std::vector<uint8_t> &buf, double *red);
 // first-wave phase offset of the slot-0 CTAs (see jit_generate), ns; 0 = off
 void jit_set_desync(std::vector<uint8_t> &buf, uint32_t n_sm, uint32_t ns);
 // device table (n_tslots x kPassThreads uint64) qsim_pass_tab writes and the pass reads

@@ -936,6 +936,30 @@ void launch_expect(const double2 *st, int M, double *partial, double *out, cudaS
     k_expect_final<<<M + 1, 256, 0, s>>>(partial, cb, M, out);
 }
 
+// Physical-bit sums of one shard from the per-tile partials the readout
+// variant of its last pass wrote (fixed order: strided per thread, then the
+// block butterfly, as k_expect_final).
+__global__ void __launch_bounds__(256) k_expect_fused(const double *__restrict__ partial,
+                                                      const __grid_constant__ FusedExpectDesc d, double *__restrict__ out)
+{
+    __shared__ double red[32];
+    const int o = blockIdx.x;  // physical bit o < M, or o == M: total
+    constexpr int W = kTileBits + 1;
+    const int t = o < d.M ? d.tile_of[o] : kTileBits, ib = o < d.M ? d.inst_bit[o] : 0;
+    double s = 0.0;
+    for (uint64_t c = threadIdx.x; c < d.n_inst; c += blockDim.x) {
+        if (t >= 0) s += partial[c * W + t];
+        else s += ((c >> ib) & 1) ? partial[c * W + kTileBits] : 0.0;
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[o] = s;
+}
+
+void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *out, cudaStream_t s)
+{
+    k_expect_fused<<<d.M + 1, 256, 0, s>>>(partial, d, out);
+}
+
 // <Q_q> in logical order from S shards' physical-bit sums (phys[s*(M+1) + p],
 // p < M: bit p set, p == M: total), shard s holding rank s:
 // out[q] = sum over s in order of (p < M ? phys_s[p] : rank bit p-M of s ? phys_s[M] : 0)

@@ -39,6 +39,17 @@ struct ExpectMap {
     int n, M, S;          // logical qubits, local bits, shards (rank s = index s)
     int phys_of[64];      // logical qubit -> physical bit
 };
+// <Q_b> of a shard from the readout variant of its last pass (Step::
+// jit_readout): partial[tile * (kTileBits + 1) + t] = sum of |a|^2 over the
+// tile's amplitudes with tile bit t set (t < kTileBits), t = kTileBits the
+// tile total.
+struct FusedExpectDesc {
+    int M;
+    int tile_of[64];     // physical bit -> tile bit of the pass (-1: an instance bit)
+    int inst_bit[64];    // physical bit -> bit of the tile (instance) index, for instance bits
+    uint64_t n_inst;
+};
+void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *out /* M + 1 */, cudaStream_t s);
 void launch_expect_logical(const double *phys /* S x (M+1) */, const ExpectMap &m, double *out /* n */,
                            cudaStream_t s);
 void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *out,

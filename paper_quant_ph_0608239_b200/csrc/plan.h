@@ -80,6 +80,11 @@ struct Step {
     // cover the tiles whose fixed local bits equal the launch's fixbits,
     // jit_set_block; the overlapped pass + exchange)
     int jit_block = 0;
+    // ST_PASS, JIT tier: 1 = the readout variant (the pass also writes, per
+    // tile, the sums of |a|^2 over the amplitudes with each tile bit set and
+    // the tile total to P.red[tile * 13 + ...]: <Q_i> fused into the last pass
+    // before qsim_expectations)
+    int jit_readout = 0;
 };
 
 struct PlanOptions {

@@ -86,6 +86,16 @@ struct qsim_ctx_s {
     cudaEvent_t upload_done = nullptr;
     double2 **d_shard_ptrs = nullptr;
     double *d_red = nullptr;
+    // <Q_i> fused into the last pass (option fuse_readout): expectations_impl
+    // asks for it (want_readout), flush runs that pass's readout variant
+    // (readout_step) writing per-tile partials into d_rdo, and the readout
+    // then reduces those (readout_ready) instead of reading the state again
+    int fuse_readout = 1;
+    bool want_readout = false, readout_ready = false;
+    int64_t readout_step = -1;
+    double *d_rdo = nullptr;
+    size_t d_rdo_cap = 0;
+    FusedExpectDesc rdo_desc{};
     size_t d_red_cap = 0;
     // the two-level sampler's own buffers (its rank-order reductions use d_red)
     double *d_samp = nullptr;
@@ -754,7 +764,7 @@ static qsim_status exec_perm(qsim_ctx c, const Step &s)
 // variant's launch over the tiles whose local bits fix_pos equal fixbits'.
 static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t count, cudaStream_t stream, bool with_tab,
                                     CUfunction fn = nullptr, const int *fix_pos = nullptr, int K = 0,
-                                    uint64_t fixbits = 0)
+                                    uint64_t fixbits = 0, double *red = nullptr)
 {
     PlanCache &pc = c->pc;
     const Step &s = pc.steps[si];
@@ -771,6 +781,7 @@ static qsim_status launch_jit_range(qsim_ctx c, size_t si, int i, uint64_t count
     if (s.pass.fresh) jit_set_init(pp[i], s.pass.init_phys);  // changes between flushes
     if (tabfn) jit_set_ttab(pp[i], c->d_ttab);
     jit_set_desync(pp[i], (uint32_t)c->n_sm, (uint32_t)c->desync_ns);
+    jit_set_red(pp[i], red);
     // (the launch copies the parameter block)
     if (!jit_set_block(pp[i], s, fix_pos, K, fixbits)) FAIL(c, QSIM_ERR_STATE, "jit pass: too many fixed bits");
     size_t sz = pp[i].size();
@@ -965,10 +976,28 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
     case ST_PASS: {
         RangeGuard rg(c, 0, (uint64_t)n_local(c) * (32ULL << M));
         CUfunction fn = c->jit ? jit_cache().find(pc.jkeys[si]) : nullptr;
+        // the readout variant when this is the last data step before qsim_expectations
+        CUfunction rfn = nullptr;
+        if (fn && (int64_t)si == c->readout_step) {
+            Step rv = s;
+            rv.jit_readout = 1;
+            const std::string rkey = jit_key(rv);
+            rfn = jit_cache().find(rkey);
+            if (!rfn) {
+                std::string jerr;
+                if (jit_cache().compile({&rv}, jerr)) rfn = jit_cache().find(rkey);
+            }
+            const size_t W = kTileBits + 1;
+            if (rfn && ensure_dev(c, c->d_rdo, c->d_rdo_cap, (size_t)n_local(c) * s.pass.n_inst * W) != QSIM_OK)
+                rfn = nullptr;
+        }
         for (int i = 0; i < n_local(c); i++) {
             const uint64_t rb = (uint64_t)local_ranks(c, i) << M;
             if (fn) {
-                if ((st = launch_jit_range(c, si, i, s.pass.n_inst, c->stream, i == 0)) != QSIM_OK) return st;
+                double *red = rfn ? c->d_rdo + (size_t)i * s.pass.n_inst * (kTileBits + 1) : nullptr;
+                if ((st = launch_jit_range(c, si, i, s.pass.n_inst, c->stream, i == 0, rfn, nullptr, 0, 0, red)) !=
+                    QSIM_OK)
+                    return st;
                 c->stats.jit_launches++;
             } else {
                 PassDesc d = s.pass;
@@ -982,6 +1011,17 @@ static qsim_status exec_step(qsim_ctx c, size_t si)
                 const double fpt = fn ? jit_cache().fp64_per_thread(pc.jkeys[si]) : -1.0;
                 c->stats.pass_fp64_slots += fpt >= 0 ? fpt * kPassThreads * (double)s.pass.n_inst : pass_fp64_slots(s, M);
             }
+        }
+        if (rfn) {  // the tile bits' and instance bits' physical positions after the store
+            FusedExpectDesc &d = c->rdo_desc;
+            d.M = M;
+            d.n_inst = s.pass.n_inst;
+            for (int b = 0; b < 64; b++) d.tile_of[b] = -1, d.inst_bit[b] = -1;
+            for (int t = 0; t < kTileBits; t++) d.tile_of[s.pass.tp_out[t]] = t;
+            for (int b = 0, k = 0; b < M; b++)
+                if (d.tile_of[b] < 0) d.inst_bit[b] = k++;
+            c->readout_ready = true;
+            c->stats.fused_readouts++;
         }
         break;
     }
@@ -1117,6 +1157,8 @@ static qsim_status flush(qsim_ctx c)
 
 static qsim_status flush_impl(qsim_ctx c)
 {
+    c->readout_ready = false;
+    c->readout_step = -1;
     if (c->poisoned) FAIL(c, QSIM_ERR_STATE, "context poisoned: %s", c->last_error.c_str());
     if (!c->init_pending && c->queue.empty()) return QSIM_OK;
     if (!c->init_pending && !c->initialized) FAIL(c, QSIM_ERR_STATE, "gates queued before qsim_init_basis");
@@ -1186,7 +1228,8 @@ static qsim_status flush_impl(qsim_ctx c)
     // a pass whose successor is not planned yet waits for it when the state is
     // sharded (it may be an exchange to overlap with)
     auto wait_successor = [&](const std::vector<Step> &out, size_t i) {
-        return c->overlap && c->jit && c->P > 1 && out[i].type == ST_PASS && i + 1 == out.size();
+        return ((c->overlap && c->P > 1) || c->want_readout) && c->jit && out[i].type == ST_PASS &&
+               i + 1 == out.size();
     };
     size_t next = 0;  // first step not launched yet
     if (hit) {
@@ -1273,6 +1316,11 @@ static qsim_status flush_impl(qsim_ctx c)
         c->stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj).count();
         for (size_t i = next; i < steps.size(); i++)
             if (steps[i].type == ST_PASS) pc.jkeys[i] = jit_key(steps[i]);
+    }
+    if (c->want_readout && c->jit) {  // the last data step, if a pass not launched yet, fuses the readout
+        size_t L = steps.size();
+        while (L > 0 && steps[L - 1].type == ST_RELABEL) L--;
+        if (L > next && steps[L - 1].type == ST_PASS) c->readout_step = (int64_t)(L - 1);
     }
     for (size_t i = next, used = 1; i < steps.size(); i += used)
         if ((st = launch_one(i, &used)) != QSIM_OK) return st;
@@ -1464,6 +1512,7 @@ qsim_status qsim_destroy(qsim_ctx c)
     if (c->d_ttab) cudaFree(c->d_ttab);
     if (c->d_perm) cudaFree(c->d_perm);
     if (c->d_red) cudaFree(c->d_red);
+    if (c->d_rdo) cudaFree(c->d_rdo);
     if (c->d_samp) cudaFree(c->d_samp);
     if (c->d_shard_ptrs) cudaFree(c->d_shard_ptrs);
     if (c->h_ops) cudaFreeHost(c->h_ops);
@@ -1711,8 +1760,12 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
 {
     if (!out) return QSIM_ERR_ARG;
     if (!c->initialized && !c->init_pending) FAIL(c, QSIM_ERR_STATE, "readout before qsim_init_basis");
+    c->want_readout = c->fuse_readout != 0;
     qsim_status s = flush(c);
+    c->want_readout = false;
     if (s != QSIM_OK) return s;
+    const bool fused = c->readout_ready;
+    c->readout_ready = false;
     const int M = c->M, cb = std::min(12, M), n = c->n, S = spmd(c) ? c->P : n_local(c);
     const uint64_t nch = 1ULL << (M - cb);
     const size_t plen = nch * (cb + 1), vlen = (size_t)M + 1;
@@ -1722,7 +1775,11 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
     double *own = c->d_red + plen, *all = own + (size_t)n_local(c) * vlen, *res = all + (size_t)S * vlen;
     RangeGuard rg(c, 4, 0);
     for (int i = 0; i < n_local(c); i++) {
-        launch_expect(c->shards[i], M, c->d_red, own + (size_t)i * vlen, c->stream);
+        if (fused)  // from the last pass's per-tile partials: no second read of the state
+            launch_expect_fused(c->d_rdo + (size_t)i * c->rdo_desc.n_inst * (kTileBits + 1), c->rdo_desc,
+                                own + (size_t)i * vlen, c->stream);
+        else
+            launch_expect(c->shards[i], M, c->d_red, own + (size_t)i * vlen, c->stream);
         LAUNCHED(c);
     }
     const double *phys = own;
@@ -1924,6 +1981,7 @@ qsim_status qsim_set_option(qsim_ctx c, const char *key, int64_t value)
         if (c->comm) c->comm->timeout_ms = c->comm_timeout_ms;
     }
     else if (k == "pass_variant") c->pass_variant = value == 1 ? 1 : 2;
+    else if (k == "fuse_readout") c->fuse_readout = value ? 1 : 0;
     else if (k == "desync_ns") c->desync_ns = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 1000000);
     else if (k == "jit") { c->jit = value != 0; c->pc.valid = false; }
     else if (k == "plan_cache") { c->plan_cache = value != 0; c->pc.valid = false; }
@@ -2018,6 +2076,15 @@ qsim_status qsim_plan_json(int n_qubits, int n_ranks, const qsim_gate *gates, si
         std::vector<const Step *> ps;
         for (const Step &s : steps)
             if (s.type == ST_PASS) ps.push_back(&s);
+        std::vector<Step> rvs;  // readout variants (bit 21)
+        if ((fusion >> 21) & 1) {
+            rvs.reserve(ps.size());
+            for (const Step *s : ps) {
+                rvs.push_back(*s);
+                rvs.back().jit_readout = 1;
+            }
+            for (const Step &s : rvs) ps.push_back(&s);
+        }
         std::string err;
         int nk = 0;
         double ms = 0;

@@ -133,7 +133,8 @@ GLOBAL_POLICY = {"remap": 0, "pairwise": 1, "auto": 2}
 
 def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1, policy: Optional[str] = None,
               block_fusion: bool = True, low_remap: bool = True, remap_lookahead: Optional[int] = None,
-              key_check: bool = False, candidate: Optional[int] = None, overlap: bool = False) -> str:
+              key_check: bool = False, candidate: Optional[int] = None, overlap: bool = False,
+              readout: bool = False) -> str:
     """Host-only planner introspection (no GPU needed).  fusion=2 also
     NVRTC-compiles the pass-specialised kernels (reported under "jit");
     key_check=True only generates their sources and checks that equal kernel-
@@ -143,12 +144,14 @@ def plan_json(n: int, n_ranks: int, gates: Sequence, fusion: int = 1, policy: Op
     plans only the planner's i-th candidate gate list (sharded plans cost
     several; each one's modelled time is reported under "candidates");
     overlap=True costs them for a transport that overlaps a pass with the
-    exchange after it (the runtime does on NCCL / loopback)."""
+    exchange after it (the runtime does on NCCL / loopback); readout=True also
+    generates (compiles, with fusion=2) every pass's readout variant."""
     arr, keep = pack_gates(gates)
     flags = (int(fusion) | (((GLOBAL_POLICY[policy] + 1) << 4) if policy else 0) | (0 if block_fusion else 0x100)
              | (0 if low_remap else 0x200) | (0x400 if key_check else 0)
              | (((remap_lookahead + 1) & 31) << 12 if remap_lookahead is not None else 0)
-             | (((candidate + 1) & 7) << 17 if candidate is not None else 0) | (1 << 20 if overlap else 0))
+             | (((candidate + 1) & 7) << 17 if candidate is not None else 0) | (1 << 20 if overlap else 0)
+             | (1 << 21 if readout else 0))
     cap = 1 << 26
     while True:
         buf = ctypes.create_string_buffer(cap)

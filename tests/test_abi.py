@@ -235,6 +235,9 @@ def test_jit_kernels_compile_for_sm100a(pkg):
     w = C.qft_basis(20, 777)
     d = json.loads(_plan(pkg, 20, 1, w.gates, fusion=2))
     assert d["jit"]["ok"], d["jit"]["error"]
+    # readout variants (<Q_i> fused into the last pass), with deferred flips
+    d = json.loads(pkg.plan_json(14, 2, gates, fusion=2, readout=True))
+    assert d["jit"]["ok"], d["jit"]["error"]
 
 
 @pytest.mark.parametrize("policy", ["remap", "pairwise", "auto"])

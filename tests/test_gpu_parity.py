@@ -184,6 +184,50 @@ def test_expectations_async(P, oracle_mod, ranks):
         assert np.max(np.abs(ex - oracle_run(oracle_mod, n, 3, g).expectations())) <= 1e-12
 
 
+@pytest.mark.parametrize("ranks", [1, 4])
+def test_fused_readout(P, oracle_mod, ranks):
+    """<Q_i> fused into the last pass (readout variant, option fuse_readout):
+    equal to the separate reduction's and the oracle's to 1e-13, on circuits
+    whose last pass ends with deferred predicated swaps, phase runs, a fresh
+    single pass, and one whose last data step is a permutation run (no
+    fusion: the separate reduction runs)."""
+    w3 = C.shor_order_finding(35, 3, 8, 6)
+    cases = [(14, 5, kitchen_sink(14, seed=4)), (16, 0, C.random_brickwork(16, 5, seed=8)),
+             (18, 77, C.qft_basis(18, 77).gates), (13, 1, [G.one_q(q, G.H) for q in range(13)]),
+             (w3.n, w3.init, w3.gates[:1 + max(i for i, g in enumerate(w3.gates) if g.kind == G.G_PERM)])]
+    for n, init, gates in cases:
+        ref = oracle_run(oracle_mod, n, init, gates).expectations()
+        got = {}
+        for fuse in (1, 0):
+            sim = P.QSim(n, n_ranks=ranks, transport="local" if ranks == 1 else "virtual")
+            sim.set_option("fuse_readout", fuse)
+            sim.init_basis(init)
+            sim.run_circuit(gates)
+            got[fuse] = sim.expectations()
+            st = sim.stats()
+            sim.close()
+            assert np.max(np.abs(got[fuse] - ref)) <= 1e-13, (n, fuse)
+            if not fuse:
+                assert st["fused_readouts"] == 0
+        assert np.max(np.abs(got[1] - got[0])) <= 1e-13
+
+
+def test_fused_readout_loopback(P, oracle_mod):
+    """The fused readout on 4 loopback ranks (SPMD: per-rank partials, all-
+    gathered and combined in rank order)."""
+    n, gates = 16, C.random_chain(16, 3, seed=21, sweep=True)
+
+    def body(sim, r):
+        sim.init_basis(9)
+        sim.run_circuit(gates)
+        return sim.expectations(), sim.stats()["fused_readouts"]
+
+    ref = oracle_run(oracle_mod, n, 9, gates).expectations()
+    for ex, nf in P.run_loopback(n, 4, body):
+        assert np.max(np.abs(ex - ref)) <= 1e-13
+        assert nf >= 1
+
+
 def test_perm_run_max_shared_memory(P, oracle_mod):
     """12-qubit register, 20 controlled perms: runs of 12 and 8 whose tables
     and double-buffered tiles take up to 224 KB of shared memory per CTA."""
