@@ -814,16 +814,20 @@ JitPass jit_generate(const Step &st)
         fpc += 2 * kAmpsPerThread;
     }
     materialize(1);  // register bit 0 lies inside one 256-bit store
+    std::ostringstream ro;  // the readout variant's reduction, emitted after the stores
     if (st.jit_readout) {
         // <Q_i> fused into the pass: per tile bit t the sum of |a|^2 over the
         // tile's amplitudes with bit t set, and the tile total (index 12),
         // in a fixed order (deterministic).  Register bit j holds tile bit
         // nib(cur, j), except that a pending flip of bit j (stored with the
         // slot address XORed, see Flip) exchanges its 0 and 1 halves.
+        // (emitted after the stores, so that they leave before the reduction's
+        // shuffles and barrier; only the pending flips' predicates, which the
+        // store consumes, are evaluated here)
         const int NWR = kPassThreads / 32;
-        s << " {\n  __shared__ double rsum[" << NWR * (kTileBits + 1) << "];\n";
+        ro << " {\n  __shared__ double rsum[" << NWR * (kTileBits + 1) << "];\n";
         for (int i = 0; i < kAmpsPerThread; i++)
-            s << "  const double rp" << i << " = fma(" << A(i) << ".x, " << A(i) << ".x, " << A(i) << ".y * " << A(i)
+            ro << "  const double rp" << i << " = fma(" << A(i) << ".x, " << A(i) << ".x, " << A(i) << ".y * " << A(i)
               << ".y);\n";
         // fixed-order tree sums over a register subset
         auto tree = [&](std::vector<int> idx) {
@@ -839,7 +843,7 @@ JitPass jit_generate(const Step &st)
         };
         std::vector<int> all;
         for (int i = 0; i < kAmpsPerThread; i++) all.push_back(i);
-        s << "  const double rtot = " << tree(all) << ";\n";
+        ro << "  const double rtot = " << tree(all) << ";\n";
         std::vector<std::string> val(kTileBits);
         for (int j = 0; j < kRegBits; j++) {
             std::vector<int> one, zero;
@@ -847,7 +851,8 @@ JitPass jit_generate(const Step &st)
             std::string fp = "false";
             for (const Flip &f : flips)
                 if (f.k == j) fp = "(" + fp + ") != (" + f.pred + ")";
-            s << "  const double rb" << j << " = (" << fp << ") ? " << tree(zero) << " : " << tree(one) << ";\n";
+            s << " const bool rf" << j << " = " << fp << ";\n";
+            ro << "  const double rb" << j << " = rf" << j << " ? " << tree(zero) << " : " << tree(one) << ";\n";
             val[nib(cur, j)] = "rb" + std::to_string(j);
         }
         for (int j = 0; j < 5; j++) val[nib(cur, kLaneNib + j)] = "(((lane >> " + std::to_string(j) + ") & 1) ? rtot : 0.0)";
@@ -855,13 +860,13 @@ JitPass jit_generate(const Step &st)
             val[nib(cur, kWarpNib + j)] = "(((warp >> " + std::to_string(j) + ") & 1) ? rtot : 0.0)";
         val.push_back("rtot");
         for (int t = 0; t <= kTileBits; t++) {
-            s << "  { double v = " << val[t] << ";";
-            for (int d = 16; d > 0; d >>= 1) s << " v += __shfl_xor_sync(0xffffffffu, v, " << d << ");";
-            s << " if (lane == 0) rsum[warp * " << kTileBits + 1 << " + " << t << "] = v; }\n";
+            ro << "  { double v = " << val[t] << ";";
+            for (int d = 16; d > 0; d >>= 1) ro << " v += __shfl_xor_sync(0xffffffffu, v, " << d << ");";
+            ro << " if (lane == 0) rsum[warp * " << kTileBits + 1 << " + " << t << "] = v; }\n";
         }
-        s << "  __syncthreads();\n  if (threadIdx.x < " << kTileBits + 1 << ") { double v = rsum[threadIdx.x];";
-        s << " for (int w = 1; w < " << NWR << "; w++) v += rsum[w * " << kTileBits + 1 << " + threadIdx.x];";
-        s << " P.red[(unsigned long long)blockIdx.x * " << kTileBits + 1 << " + threadIdx.x] = v; }\n }\n";
+        ro << "  __syncthreads();\n  if (threadIdx.x < " << kTileBits + 1 << ") { double v = rsum[threadIdx.x];";
+        ro << " for (int w = 1; w < " << NWR << "; w++) v += rsum[w * " << kTileBits + 1 << " + threadIdx.x];";
+        ro << " P.red[(unsigned long long)blockIdx.x * " << kTileBits + 1 << " + threadIdx.x] = v; }\n }\n";
         // |a|^2, the total, both halves per register bit, the warp butterflies
         fpc += 2.0 * kAmpsPerThread + (kAmpsPerThread - 1) + kRegBits * 2 * (kAmpsPerThread / 2 - 1) +
                (kTileBits + 1) * 5;
@@ -876,6 +881,7 @@ JitPass jit_generate(const Step &st)
           << A(2 * j) << ".x), \"d\"(" << A(2 * j) << ".y), \"d\"(" << A(2 * j + 1) << ".x), \"d\"(" << A(2 * j + 1)
           << ".y) : \"memory\");\n";
     s << " }\n";
+    s << ro.str();
     s << " }\n";
     // Phase offset between the two CTAs an SM runs.  CTAs of the first wave
     // start together and, running identical code, stay in step: both re-

@@ -937,27 +937,76 @@ void launch_expect(const double2 *st, int M, double *partial, double *out, cudaS
 }
 
 // Physical-bit sums of one shard from the per-tile partials the readout
-// variant of its last pass wrote (fixed order: strided per thread, then the
-// block butterfly, as k_expect_final).
-__global__ void __launch_bounds__(256) k_expect_fused(const double *__restrict__ partial,
-                                                      const __grid_constant__ FusedExpectDesc d, double *__restrict__ out)
+// variant of its last pass wrote, in two fixed-order levels (deterministic).
+// Level 1: block b reduces the R = min(4096, n_inst) consecutive tiles
+// [bR, (b+1)R) for every tile bit, every low instance bit (< log2 R: bit ib
+// of the tile index within the block) and the total; the partial rows are
+// read once, contiguously.  Level 2: bit o from the level-1 rows (a high
+// instance bit is a bit of the block index b).
+constexpr int kFusedRow = kTileBits + 1 + 12;  // tile bits, total, low instance bits
+__global__ void __launch_bounds__(256) k_expect_fused1(const double *__restrict__ partial, int logR,
+                                                       double *__restrict__ out1)
+{
+    constexpr int W = kTileBits + 1;
+    __shared__ double ws[8][kFusedRow];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint64_t R = 1ULL << logR, base = (uint64_t)blockIdx.x << logR;
+    double acc[kFusedRow];
+#pragma unroll
+    for (int j = 0; j < kFusedRow; j++) acc[j] = 0.0;
+    for (uint64_t j = t; j < R; j += 256) {
+        const double *row = partial + (base + j) * W;
+#pragma unroll
+        for (int q = 0; q < W; q++) acc[q] += row[q];
+        const double tot = row[kTileBits];
+#pragma unroll
+        for (int ib = 0; ib < 12; ib++)
+            if (ib < logR && ((j >> ib) & 1)) acc[W + ib] += tot;
+    }
+#pragma unroll
+    for (int q = 0; q < kFusedRow; q++) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) ws[w][q] = v;
+    }
+    __syncthreads();
+    if (t < kFusedRow) {
+        double v = ws[0][t];
+        for (int k = 1; k < 8; k++) v += ws[k][t];
+        out1[(uint64_t)blockIdx.x * kFusedRow + t] = v;
+    }
+}
+__global__ void __launch_bounds__(256) k_expect_fused2(const double *__restrict__ out1, uint64_t nb, int logR,
+                                                       const __grid_constant__ FusedExpectDesc d,
+                                                       double *__restrict__ out)
 {
     __shared__ double red[32];
     const int o = blockIdx.x;  // physical bit o < M, or o == M: total
-    constexpr int W = kTileBits + 1;
     const int t = o < d.M ? d.tile_of[o] : kTileBits, ib = o < d.M ? d.inst_bit[o] : 0;
     double s = 0.0;
-    for (uint64_t c = threadIdx.x; c < d.n_inst; c += blockDim.x) {
-        if (t >= 0) s += partial[c * W + t];
-        else s += ((c >> ib) & 1) ? partial[c * W + kTileBits] : 0.0;
+    for (uint64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+        const double *row = out1 + b * kFusedRow;
+        if (t >= 0) s += row[t];
+        else if (ib < logR) s += row[kTileBits + 1 + ib];
+        else s += ((b >> (ib - logR)) & 1) ? row[kTileBits] : 0.0;
     }
     s = block_sum(s, red);
     if (threadIdx.x == 0) out[o] = s;
 }
 
-void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *out, cudaStream_t s)
+size_t expect_fused_scratch(uint64_t n_inst)
 {
-    k_expect_fused<<<d.M + 1, 256, 0, s>>>(partial, d, out);
+    const int logR = n_inst >= 4096 ? 12 : __builtin_ctzll(n_inst);
+    return (size_t)(n_inst >> logR) * kFusedRow;
+}
+
+void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *scratch, double *out, cudaStream_t s)
+{
+    const int logR = d.n_inst >= 4096 ? 12 : __builtin_ctzll(d.n_inst);
+    const uint64_t nb = d.n_inst >> logR;
+    k_expect_fused1<<<(unsigned)nb, 256, 0, s>>>(partial, logR, scratch);
+    k_expect_fused2<<<d.M + 1, 256, 0, s>>>(scratch, nb, logR, d, out);
 }
 
 // <Q_q> in logical order from S shards' physical-bit sums (phys[s*(M+1) + p],

@@ -49,7 +49,10 @@ struct FusedExpectDesc {
     int inst_bit[64];    // physical bit -> bit of the tile (instance) index, for instance bits
     uint64_t n_inst;
 };
-void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *out /* M + 1 */, cudaStream_t s);
+// scratch: expect_fused_scratch(n_inst) doubles
+size_t expect_fused_scratch(uint64_t n_inst);
+void launch_expect_fused(const double *partial, const FusedExpectDesc &d, double *scratch, double *out /* M + 1 */,
+                         cudaStream_t s);
 void launch_expect_logical(const double *phys /* S x (M+1) */, const ExpectMap &m, double *out /* n */,
                            cudaStream_t s);
 void launch_sample(const double *p, int k, uint64_t seed, uint64_t n_shots, double *cdf, uint64_t *out,

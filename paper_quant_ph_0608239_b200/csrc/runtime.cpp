@@ -1768,15 +1768,16 @@ static qsim_status expectations_impl(qsim_ctx c, double *out, bool sync)
     c->readout_ready = false;
     const int M = c->M, cb = std::min(12, M), n = c->n, S = spmd(c) ? c->P : n_local(c);
     const uint64_t nch = 1ULL << (M - cb);
-    const size_t plen = nch * (cb + 1), vlen = (size_t)M + 1;
+    const size_t plen = std::max<size_t>(nch * (cb + 1), fused ? expect_fused_scratch(c->rdo_desc.n_inst) : 0),
+                 vlen = (size_t)M + 1;
     // partial sums | this process's shard vectors | all ranks' vectors (NCCL) | logical result
     const size_t need = plen + (size_t)n_local(c) * vlen + (size_t)S * vlen + n;
     if ((s = ensure_dev(c, c->d_red, c->d_red_cap, need)) != QSIM_OK) return s;
     double *own = c->d_red + plen, *all = own + (size_t)n_local(c) * vlen, *res = all + (size_t)S * vlen;
     RangeGuard rg(c, 4, 0);
     for (int i = 0; i < n_local(c); i++) {
-        if (fused)  // from the last pass's per-tile partials: no second read of the state
-            launch_expect_fused(c->d_rdo + (size_t)i * c->rdo_desc.n_inst * (kTileBits + 1), c->rdo_desc,
+        if (fused)  // from the last pass's per-tile partials: no second read of the state (d_red as scratch)
+            launch_expect_fused(c->d_rdo + (size_t)i * c->rdo_desc.n_inst * (kTileBits + 1), c->rdo_desc, c->d_red,
                                 own + (size_t)i * vlen, c->stream);
         else
             launch_expect(c->shards[i], M, c->d_red, own + (size_t)i * vlen, c->stream);
