@@ -192,7 +192,8 @@ def test_fused_readout(P, oracle_mod, ranks):
     single pass, and one whose last data step is a permutation run (no
     fusion: the separate reduction runs)."""
     w3 = C.shor_order_finding(35, 3, 8, 6)
-    cases = [(14, 5, kitchen_sink(14, seed=4)), (16, 0, C.random_brickwork(16, 5, seed=8)),
+    w1 = C.config1_adder()
+    cases = [(14, 5, kitchen_sink(14, seed=4)), (w1.n, w1.init, w1.gates), (16, 0, C.random_brickwork(16, 5, seed=8)),
              (18, 77, C.qft_basis(18, 77).gates), (13, 1, [G.one_q(q, G.H) for q in range(13)]),
              (w3.n, w3.init, w3.gates[:1 + max(i for i, g in enumerate(w3.gates) if g.kind == G.G_PERM)])]
     for n, init, gates in cases:
