@@ -617,6 +617,11 @@ def test_gpu_fuzz(P, oracle_mod, seed):
     sim.init_basis(init)
     sim.run_circuit(gates)
     assert_parity(sim, o, n)
+    # <Q_i> straight after the circuit (fused into its last pass when that is
+    # a JIT pass) vs the oracle
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-13
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("QSIM_FUZZ_LONG_SEEDS", "2"))))
@@ -633,7 +638,11 @@ def test_gpu_fuzz_long(P, oracle_mod, seed):
     sim = P.QSim(n, n_ranks=ranks, transport="local" if ranks == 1 else "virtual")
     sim.init_basis(init)
     sim.run_circuit(gates)
-    assert_parity(sim, oracle_run(oracle_mod, n, init, gates), n)
+    o = oracle_run(oracle_mod, n, init, gates)
+    assert_parity(sim, o, n)
+    sim.init_basis(init)
+    sim.run_circuit(gates)
+    assert np.max(np.abs(sim.expectations() - o.expectations())) <= 1e-13
 
 
 @pytest.mark.parametrize("G,y,X,F", [(247, 194, 14, 8), (899, 2, 12, 10), (35, 3, 10, 6)])
