@@ -30,3 +30,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/relayout_bench tools/re
 /tmp/relayout_bench > gpurun_out/relayout_bench.jsonl 2>&1; echo "relayout_bench=$?"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/gran_bench tools/gran_bench.cu && \
 /tmp/gran_bench 30 > gpurun_out/gran_bench.jsonl 2>&1; echo "gran_bench=$?"
+ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio,smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio,smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio,smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio,smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio,smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio --clock-control none -k regex:^qsim_pass$ -s 28 -c 14 -o gpurun_out/prof_perpass -f \
+    python tools/profile_pass.py 3 > gpurun_out/ncu_perpass.log 2>&1; echo "perpass=$?"
