@@ -232,6 +232,69 @@ __global__ void __launch_bounds__(512, 1) k_pingpong(double2 *out, const __grid_
     out[(blockIdx.x * 2 + g) * 256 + t] = acc;
 }
 
+// Two tiles per thread, software-pipelined: while one tile's re-layout goes
+// through shared memory (its own 64-KB buffer), the same warps compute the
+// other tile; one barrier per re-layout (the other tile's barrier is the
+// write-after-read fence).  1 CTA/SM, 256 threads x 2 x 16 amplitudes.
+__global__ void __launch_bounds__(256, 1) k_two_tiles(double2 *out, const __grid_constant__ MP P)
+{
+    extern __shared__ double2 sm[];
+    const int t = threadIdx.x;
+    double2 *bufA = sm, *bufB = sm + 4096;
+    double2 a[16], b[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        a[i] = make_double2(t * 1e-3 + i, blockIdx.x * 1e-6);
+        b[i] = make_double2(t * 2e-3 + i, blockIdx.x * 2e-6);
+    }
+    u4<0, 1>(a, P.m[0]);
+    u4<2, 3>(a, P.m[1]);
+#pragma unroll
+    for (int r = 0; r < kRounds; r++) {
+        // A re-layout under B compute
+#pragma unroll
+        for (int i = 0; i < 16; i++) bufA[i * 256 + t] = a[i];
+        u4<0, 1>(b, P.m[2 * r]);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 16; i++) a[i] = bufA[i * 256 + ((t + 17 * i + r) & 255)];
+        u4<2, 3>(b, P.m[2 * r + 1]);
+        // B re-layout under A compute
+#pragma unroll
+        for (int i = 0; i < 16; i++) bufB[i * 256 + t] = b[i];
+        if (r + 1 < kRounds) u4<0, 1>(a, P.m[2 * r + 2]);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 16; i++) b[i] = bufB[i * 256 + ((t + 17 * i + r) & 255)];
+        if (r + 1 < kRounds) u4<2, 3>(a, P.m[2 * r + 3]);
+    }
+    double2 acc = a[0];
+#pragma unroll
+    for (int i = 1; i < 16; i++) { acc.x += a[i].x + b[i].x; acc.y += a[i].y + b[i].y; }
+    out[(blockIdx.x * 2) * 256 + t] = acc;
+}
+
+float run_two(double2 *out, int grid, const MP &P)
+{
+    const int smem = 128 * 1024;
+    cudaFuncSetAttribute(k_two_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_two_tiles<<<grid, 256, smem>>>(out, P);
+    float best = 1e9;
+    for (int rep = 0; rep < 3; rep++) {
+        cudaEventRecord(e0);
+        k_two_tiles<<<grid, 256, smem>>>(out, P);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    return best;
+}
+
 template <int PP>
 float run_pp(double2 *out, int grid, const MP &P)
 {
@@ -326,6 +389,8 @@ int main()
     rep("compute + shuffle exchange, 2 CTA/SM", run<12, 2>(out, grid2, rounds, 0, sm64, P));
     rep("warp-specialised half compute / half smem, 2 CTA/SM", run<4, 2>(out, grid2, rounds, 0, sm64, P));
     rep("compute + warp-local relayout, 2 CTA/SM", run<5, 2>(out, grid2, rounds, 0, sm64, P));
+    rep("two tiles per thread, pipelined (re-layout of one under the compute of the other), 1 CTA/SM",
+        run_two(out, grid2 / 2, P));
     rep("two groups in one 512-thread CTA, no ping-pong", run_pp<0>(out, grid2 / 2, P));
     rep("two groups in one 512-thread CTA, ping-pong", run_pp<1>(out, grid2 / 2, P));
     rep("compute, 1 CTA/SM (128-reg cap)", run<1, 2>(out, grid2, rounds, 0, sm120, P));
