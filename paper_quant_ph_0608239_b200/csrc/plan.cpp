@@ -813,6 +813,49 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     bool in_tile[64] = {false};
     in_tile[0] = in_tile[1] = in_tile[2] = true;
     std::vector<std::pair<int, int>> relabels;
+    if (G > 0) {
+        // Sharded plans: after an exchange the first not-done gates of a
+        // nearest-neighbour circuit (a chain's staircase) sit on qubits spread
+        // over the register, and the greedy first-use order fills the tile with
+        // them, so each pass advances the front only a little (config-5 family
+        // at 36 q / 8 ranks: ~20 gates per pass).  Candidate tiles: the greedy
+        // one and windows of consecutive logical qubits starting at the first
+        // frontier qubits; each is scored by a dry run of the collection and the
+        // window is preset when it takes clearly more gates.
+        auto dry = [&](const std::vector<int> &preset) {
+            Planner Q = *this;
+            std::vector<char> d2 = done;
+            std::vector<int> fb = preset;
+            bool it[64] = {false};
+            it[0] = it[1] = it[2] = true;
+            for (int b : preset) it[b] = true;
+            return collect_pass(Q, gates, d2, first, opt, nullptr, fb, it, nullptr);
+        };
+        const size_t base_score = dry({});
+        std::vector<int> front;  // logical qubits of the first not-done non-diagonal gates, in order
+        for (size_t i = first; i < gates.size() && front.size() < 8; i++) {
+            if (done[i]) continue;
+            for (int q = 0; q < n && front.size() < 8; q++)
+                if (((gates[i].qN >> q) & 1) && std::find(front.begin(), front.end(), q) == front.end()) front.push_back(q);
+        }
+        size_t best = base_score;
+        std::vector<int> best_w;
+        for (int f : front)
+            for (int off : {0, -3, -6}) {
+                std::vector<int> w;
+                for (int q = std::max(0, f + off); q < n && (int)w.size() < kTileBits - 3; q++) {
+                    const int pb = phys_of[q];
+                    if (pb >= 3 && pb < M) w.push_back(pb);
+                }
+                if ((int)w.size() < kTileBits - 3) continue;
+                const size_t sc = dry(w);
+                if (sc > best) { best = sc; best_w = w; }
+            }
+        if (!best_w.empty() && best >= base_score + base_score / 4 + 2) {
+            freeb = best_w;
+            for (int b : best_w) in_tile[b] = true;
+        }
+    }
     collect_pass(*this, gates, done, first, opt, &pops, freeb, in_tile, &relabels);
     // tile: physical bits 0,1,2 + the free bits (first-use order), filled up to 12
     std::vector<int> order;
