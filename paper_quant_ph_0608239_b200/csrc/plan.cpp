@@ -813,7 +813,11 @@ void Planner::build_pass(const std::vector<GateRec> &gates, std::vector<char> &d
     bool in_tile[64] = {false};
     in_tile[0] = in_tile[1] = in_tile[2] = true;
     std::vector<std::pair<int, int>> relabels;
-    if (G > 0) {
+    static const int win_env = [] {
+        const char *v = getenv("QSIM_PLAN_WINDOWS");
+        return v ? atoi(v) : -1;
+    }();
+    if (win_env == 1 || (win_env < 0 && G > 0)) {
         // Sharded plans: after an exchange the first not-done gates of a
         // nearest-neighbour circuit (a chain's staircase) sit on qubits spread
         // over the register, and the greedy first-use order fills the tile with
