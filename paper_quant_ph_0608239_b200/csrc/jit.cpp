@@ -50,6 +50,8 @@ struct Layout {
     size_t off_out = kOffOut, off_m = 0, bytes = 0;
 };
 
+constexpr int kJitBarDefault = 3;  // re-layout barrier form, see QSIM_JIT_BAR below
+
 // generator variant (env, for A/B experiments): minimum CTAs per SM.  A
 // persistent grid with L2 prefetch of the next tile and 1 or 3 CTAs/SM were
 // measured slower on config 2 (register spills / occupancy).
@@ -550,6 +552,32 @@ JitPass jit_generate(const Step &st)
         s << " }\n";
         live &= ~F;
     };
+    // Re-layout barriers (QSIM_JIT_BAR, A/B switch): 0 = a CTA barrier after
+    // the stores and after the loads; 1 = the second one deferred to just
+    // before the next re-layout's stores (warps start computing as soon as
+    // their own loads are done); 2 = as 1, and each barrier spans only the
+    // warps that exchange data: those equal on the warp slots whose tile bit
+    // stays put (kept slot w2: bar 1/2 over 4 warps, w1: 3/4, w0: 5/6; all
+    // kept: the warp alone); 3 = as 2 with the w2 groups only.  Warp w runs
+    // on SM sub-partition w % 4, so a w2 group spans all four and the two
+    // groups interleave their FP64 and shared-memory phases on each; a w0 or
+    // w1 group sits on two sub-partitions and leaves the other two's FP64
+    // pipes idle while it re-lays out (measured slower).  Every warp runs the
+    // same barrier sequence and a barrier id always names the same warp set,
+    // so named barriers cannot mix.
+    const int bar_mode = env_int("QSIM_JIT_BAR", kJitBarDefault);
+    int n_trans = 0;
+    uint32_t prev_keep = 0;
+    auto group_bar = [&](uint32_t keep) -> std::string {
+        const uint32_t all = (1u << kWarpBits) - 1;
+        if (kWarpBits != 3 || keep == 0) return BAR;
+        if (keep == all) return "__syncwarp();";
+        if (bar_mode >= 3 && !((keep >> 2) & 1)) return BAR;
+        const int j = (keep >> 2) & 1 ? 2 : (keep >> 1) & 1 ? 1 : 0;
+        const int id0 = j == 2 ? 1 : j == 1 ? 3 : 5;
+        return "asm volatile(\"bar.sync %0, 128;\" :: \"r\"(" + std::to_string(id0) + " + ((warp >> " +
+               std::to_string(j) + ") & 1)) : \"memory\");";
+    };
     int n_had = 0;
     for (const KOp &op : st.ops) n_had += jit_hadamard(op);
     if (n_had) s << " double hs = 1.0;  // product of the Hadamard-form scales applied so far\n";
@@ -558,15 +586,25 @@ JitPass jit_generate(const Step &st)
         if (op.code == OPC_TRANS) {
             flush(live);
             s << " {\n";
+            // warp slots whose tile bit stays put through this re-layout: the
+            // warps that differ only there never exchange data
+            uint32_t keep = 0;
+            for (int j = 0; j < kWarpBits; j++)
+                if (nib(cur, kWarpNib + j) == nib(op.cfg, kWarpNib + j)) keep |= 1u << j;
+            if (bar_mode >= 1 && n_trans > 0)  // WAR: the previous re-layout's reads of what we overwrite
+                s << "  " << group_bar(bar_mode >= 2 ? keep & prev_keep : 0) << "\n";
             smem_z(cur, "a");
             const uint64_t cfa = cur;
             flip_mask("zfa", "int", [&](int k) { return std::to_string(swz_host(1 << nib(cfa, k))); });
             for (int i = 0; i < kAmpsPerThread; i++) s << "  sm[(zza ^ zfa) ^ " << zreg(cur, i) << "] = " << A(i) << ";\n";
-            s << "  " << BAR << "\n";
+            s << "  " << (bar_mode >= 2 ? group_bar(keep) : BAR) << "\n";  // RAW
             cur = op.cfg;
             smem_z(cur, "b");
             for (int i = 0; i < kAmpsPerThread; i++) s << "  " << A(i) << " = sm[zzb ^ " << zreg(cur, i) << "];\n";
-            s << "  " << BAR << "\n }\n";
+            if (bar_mode == 0) s << "  " << BAR << "\n";
+            s << " }\n";
+            prev_keep = keep;
+            n_trans++;
             continue;
         }
         if (op.code == OPC_PHASE_FLUSH) continue;  // lazy flush (above)
@@ -1203,7 +1241,7 @@ std::string jit_key(const Step &st)
     put((uint64_t)env_int("QSIM_JIT_MINB", kPassMinBlocks) |
         ((uint64_t)(st.pass.fresh != 0) << 48) | ((uint64_t)(st.jit_block != 0) << 49) |
         ((uint64_t)(st.jit_readout != 0) << 50) |
-        ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20));
+        ((uint64_t)env_int("QSIM_JIT_U4IL", 0) << 20) | ((uint64_t)env_int("QSIM_JIT_BAR", kJitBarDefault) << 28));
     put(st.pass.cfg0);
     {
         const Forms fm = forms_of(st);
