@@ -240,6 +240,31 @@ def test_jit_kernels_compile_for_sm100a(pkg):
     assert d["jit"]["ok"], d["jit"]["error"]
 
 
+def test_relayout_barrier_forms(pkg, tmp_path, monkeypatch):
+    """Re-layout barriers of the config-2 kernels (jit.cpp QSIM_JIT_BAR = 3):
+    CTA barriers, warp barriers, and named barriers over one CTA half whose id
+    is a function of the top warp bit only (an id always names the same four
+    warps, so barriers of different forms cannot mix); the generated code
+    holds at most two barriers per re-layout and all three forms occur."""
+    monkeypatch.setenv("QSIM_JIT_DUMP", str(tmp_path))
+    w = C.config2_random()
+    d = json.loads(_plan(pkg, w.n, 1, w.gates, fusion=2))
+    assert d["jit"]["ok"], d["jit"]["error"]
+    srcs = [open(tmp_path / f).read() for f in sorted(os.listdir(tmp_path)) if f.endswith(".cu")]
+    assert len(srcs) == d["jit"]["kernels"]
+    n_cta = n_warp = n_half = n_trans = 0
+    for src in srcs:
+        named = re.findall(r'bar\.sync %0, (\d+);" :: "r"\(([^)]*\)[^)]*)\)', src)
+        for cnt, idx in named:
+            assert cnt == "128" and idx.replace(" ", "") == "1+((warp>>2)&1", idx
+        n_half += len(named)
+        n_warp += src.count("__syncwarp();")
+        n_cta += src.count("__syncthreads();")
+        n_trans += src.count("const int zzb")
+    assert n_half > 0 and n_warp > 0 and n_cta > 0
+    assert n_half + n_warp + n_cta <= 2 * n_trans
+
+
 @pytest.mark.parametrize("policy", ["remap", "pairwise", "auto"])
 def test_plan_global_policies(pkg, oracle_mod, policy):
     """Gates on nonlocal qubits by K-pair remap or by pairwise
