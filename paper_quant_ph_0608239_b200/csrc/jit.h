@@ -10,7 +10,9 @@
 // identical states); phase runs (exact integer angle accumulation per
 // monomial, lazily flushed, CTA-uniform and per-thread terms summed once per
 // tile / launch) and Hadamard-form gates (sum/difference, one scale at the
-// store) round differently and agree to 1e-13.
+// store) round differently and agree to 1e-13.  A re-layout's barriers span
+// only the warps that exchange data through it (a CTA half when the top warp
+// slot keeps its tile bit, the warp alone when all warp slots do).
 #pragma once
 #include <cuda.h>
 
