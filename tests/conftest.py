@@ -13,6 +13,14 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long CPU test")
 
 
+def pytest_collection_modifyitems(config, items):
+    # the full-size parity tests (minutes of CPU oracle time at 28 q) run last, so that
+    # under -x or a wall-clock limit every shorter GPU test has already reported
+    heavy = [it for it in items if it.fspath.basename == "test_gpu_fullsize.py"]
+    if heavy:
+        items[:] = [it for it in items if it.fspath.basename != "test_gpu_fullsize.py"] + heavy
+
+
 @pytest.fixture(scope="session")
 def oracle_mod():
     import oracle
