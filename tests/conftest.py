@@ -16,9 +16,10 @@ def pytest_configure(config):
 def pytest_collection_modifyitems(config, items):
     # the full-size parity tests (minutes of CPU oracle time at 28 q) run last, so that
     # under -x or a wall-clock limit every shorter GPU test has already reported
-    heavy = [it for it in items if it.fspath.basename == "test_gpu_fullsize.py"]
+    is_heavy = lambda it: "test_gpu_fullsize.py::" in it.nodeid  # noqa: E731
+    heavy = [it for it in items if is_heavy(it)]
     if heavy:
-        items[:] = [it for it in items if it.fspath.basename != "test_gpu_fullsize.py"] + heavy
+        items[:] = [it for it in items if not is_heavy(it)] + heavy
 
 
 @pytest.fixture(scope="session")
