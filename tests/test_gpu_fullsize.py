@@ -35,7 +35,10 @@ def P():
 
 
 def _need_gpu_bytes(nbytes):
+    import gc
     import torch
+    gc.collect()
+    torch.cuda.empty_cache()  # these tests run last: blocks cached by earlier tests are not "free" to mem_get_info
     free, _ = torch.cuda.mem_get_info()
     if free < nbytes:
         pytest.skip(f"needs {nbytes >> 30} GiB free on the GPU")
